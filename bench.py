@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""sFISTA throughput on B200 (BASELINE.json metric: Mpixel*iterations/s).
+
+Workload (N=1): BASELINE configs[1] = cfg2 — 1024x1024 phantom (200 rect + 100 disks), 63x63
+two-Gaussian PSF, reflective BC (Toeplitz+Hankel factors), r=5, lam=0.01, x>=0, 200 iterations.
+Headline dtype float64 (the reference computes in fp64); the float32 variant of the same config is
+reported under "variants". One step = one complete 200-iteration solve. N>1: independent replicas
+(cfg2 does not shard), weak scaling, value = total Mpix*it/s over ranks, time = max over
+ranks. Inputs are L2-resident during a solve by design (40 MB working set); L2 is flushed (256 MiB
+write) between timed steps.
+
+--impl reference: the CPU oracle port of kronblur's hot path (oracle/kronblur_port.py; the reference
+is pure Python/numpy and cannot travel to the GPU box) on the host cores, threaded over column
+blocks; each step = one cfg2 iteration. Rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = "cfg2"
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", default=CFG)
+    p.add_argument("--dtype", default="float64", choices=["float64", "float32"])
+    p.add_argument("--no-variants", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def algorithmic(cfg):
+    """Per pixel*iteration: flops F = 8 r w (forward + adjoint, 2 passes each, w MACs per tap
+    row), compulsory bytes 8*sizeof(T) (sweep 1 reads Y, B writes R; sweep 2 reads R, Y, X_prev,
+    writes X, Y) — SURVEY §8(d)."""
+    return 8 * cfg.r * cfg.w
+
+
+def measured_peaks():
+    try:
+        with open(MEASURED) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in rows if num(r[0]) is not None]
+        loaded = [s for s in sm if s is not None and s > 500] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": num(rows[0][1]), "reasons": reasons, "samples": len(rows)}
+
+
+def build_problem(cfg, dtype, seed=0, device="cuda"):
+    import paper_1901_00913_b200 as kb
+    from paper_1901_00913_b200 import workloads as W
+
+    X, psf, B = W.make_image_data(cfg, seed=seed, device=device)
+    op = kb.decompose(psf, kb.BoundaryCondition(cfg.bc), s=cfg.r, shape=(cfg.m, cfg.m))
+    L = kb.lipschitz(op, iters=50, seed=seed, dtype="float64")
+    return X, psf, B, op, L
+
+
+def run_b200(args):
+    import torch
+
+    import paper_1901_00913_b200 as kb
+    from paper_1901_00913_b200 import workloads as W
+    from paper_1901_00913_b200.device import INT_MAX, device_operator, fma_peak
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = W.CONFIGS[args.config]
+    m, iters = cfg.m, cfg.iters
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    X, psf, B, op, L = build_problem(cfg, args.dtype, seed=rank)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def measure(dtype, steps, warmup, clocks=False):
+        dev = device_operator(op, dtype)
+        _, beta = kb.momentum_table(iters)
+        Bd = torch.from_numpy(B).to("cuda", dev.tdtype)
+        Xd, Yd = torch.zeros_like(Bd), torch.zeros_like(Bd)
+        flag = torch.full((1,), INT_MAX, dtype=torch.int32, device="cuda")
+        stream = torch.cuda.current_stream()
+        times = []
+        sampler = ClockSampler(local)
+        for s in range(warmup + steps):
+            Xd.zero_()
+            Yd.zero_()
+            flush.zero_()
+            if s == warmup:
+                barrier()
+                torch.cuda.synchronize()
+                if clocks:
+                    sampler.__enter__()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dev.sfista_run(Bd, Xd, Yd, beta, 0, iters, L, cfg.lam, True, flag, use_graph=True)
+            e1.record(stream)
+            if s >= warmup:
+                e1.synchronize()
+                times.append(e0.elapsed_time(e1))
+        torch.cuda.synchronize()
+        barrier()
+        if clocks:
+            sampler.__exit__(None, None, None)
+        assert int(flag.item()) > iters, "non-finite iterate in benchmark run"
+        return dev, Bd, sum(times) / len(times), (sampler.summary() if clocks else None)
+
+    dev, Bd, ms, clocks = measure(args.dtype, args.steps, args.warmup, clocks=True)
+    ms = max_over_ranks(ms)
+    mpix_it = m * m * iters / 1e6
+    value = world * mpix_it / (ms / 1e3)
+
+    # ---- e2e: public API with host buffers (H2D of B and X0, D2H of x inside the region)
+    cfgsolve = kb.SolveConfig(lam=cfg.lam, lipschitz=L, max_iter=iters, record_history=False)
+    opts = kb.SolveOptions(dtype=args.dtype, project=True, use_graph=True)
+    for _ in range(args.warmup):
+        kb.sfista(op, B, cfgsolve, options=opts)
+    e2e_t = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        run = kb.sfista(op, B, cfgsolve, options=opts)
+        torch.cuda.synchronize()
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = max_over_ranks(sum(e2e_t) / len(e2e_t))
+    esz = 8 if args.dtype == "float64" else 4
+    e2e = {"value": world * mpix_it / e2e_s, "unit": "Mpixel*iterations/s",
+           "h2d_bytes_per_step": 2 * m * m * esz, "d2h_bytes_per_step": m * m * esz}
+
+    # ---- roofline of the iteration kernels (CUDA events, same stream)
+    kern_ms = dev.time_passes(Bd, Bd, L, cfg.lam, reps=20)
+    it_ms = sum(kern_ms)
+    F = algorithmic(cfg)
+    flops_it = F * m * m
+    peak_fma = fma_peak(args.dtype)
+    peaks, peak_kind = measured_peaks()
+    achieved_tf = flops_it / (it_ms * 1e-3) / 1e12
+    hbm_gbs = 8 * esz * m * m / (it_ms * 1e-3) / 1e9
+    roofline = {
+        "bound": "fma",
+        "kernel": "one sFISTA iteration = kb_pass_a(fwd) + kb_pass_b(resid) + kb_pass_a(adj) + kb_pass_b(update)",
+        "achieved": round(achieved_tf, 3), "peak": round(peak_fma, 3), "unit": "TFLOP/s",
+        "frac": round(achieved_tf / peak_fma, 4),
+        "peak_source": f"measured live by kb_fma_peak ({args.dtype} FMA chains) in this run",
+        "per_kernel_ms": [round(x, 5) for x in kern_ms],
+        "traffic": None,
+        "hbm": {"achieved": round(hbm_gbs, 1), "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                "frac": round(hbm_gbs / peaks.get("hbm_gbs", 6550.0), 4), "peak_source": peak_kind,
+                "algorithmic_bytes_per_px_it": 8 * esz},
+        "algorithmic_flops_per_px_it": F,
+    }
+
+    variants = {}
+    if not args.no_variants and world == 1 and "float32" in cfg.dtypes and args.dtype != "float32":
+        _, _, ms32, _ = measure("float32", max(2, args.steps // 2), 2)
+        variants["float32"] = {"value": mpix_it / (ms32 / 1e3), "ms_per_step": ms32}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, op, B, L, iters_sample=2)
+
+    if rank == 0:
+        line = {
+            "metric": "sFISTA Mpixel*iterations/s",
+            "value": round(value, 2),
+            "unit": "Mpixel*iterations/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64" if args.dtype == "float64" else "f32",
+            "data": "synthetic (seeded phantom + PSF + exact-level Gaussian noise, BASELINE cfg2)",
+            "config": {"workload": f"{args.config}: {m}x{m} {cfg.bc} BC, w={cfg.w}, r={cfg.r}, "
+                                   f"lam={cfg.lam}, x>=0, {iters} iterations per step",
+                       "global_batch": world, "parallelism": f"replicas{world}",
+                       "l2": "flushed between steps (256 MiB write); 40 MB working set is L2-resident within a solve"},
+            "e2e": e2e,
+            "roofline": roofline,
+            "gpu_launches": 4 * iters * args.steps,
+            "clocks": clocks,
+            "impl": "b200",
+        }
+        if variants:
+            line["variants"] = variants
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(cfg, op, B, L, iters_sample=2, threads=None):
+    """Oracle port (kronblur's FFT hot path in numpy) on the host: a bounded sample of
+    `iters_sample` projected iterations of the same workload."""
+    from oracle import kronblur_port as port
+
+    threads = threads or cpu_threads()
+    pop = port.PortOperator(op)
+    port.set_threads(threads)
+    t0 = time.perf_counter()
+    port.sfista(pop, B, L, cfg.lam, iters_sample, project=True)
+    dt = time.perf_counter() - t0
+    return {"value": round(cfg.m * cfg.m * iters_sample / dt / 1e6, 4), "unit": "Mpixel*iterations/s",
+            "cores": threads, "kind": "port",
+            "sample": f"{iters_sample} projected sFISTA iterations of {cfg.name} ({cfg.m}x{cfg.m}, fp64, "
+                      f"numpy pocketfft path threaded over column blocks), {dt:.2f} s"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import paper_1901_00913_b200 as kb
+    from oracle import kronblur_port as port
+    from paper_1901_00913_b200 import workloads as W
+
+    cfg = W.CONFIGS[args.config]
+    X, psf, B = W.make_image_data(cfg, seed=0, device="cpu")
+    op = kb.decompose(psf, kb.BoundaryCondition(cfg.bc), s=cfg.r, shape=(cfg.m, cfg.m))
+    threads = cpu_threads()
+    port.set_threads(threads)
+    pop = port.PortOperator(op)
+    L = port.estimate_lipschitz(lambda v: port.kron_apply(pop, v),
+                                lambda v: port.kron_apply_adjoint(pop, v), (cfg.m, cfg.m), 2, 0)
+    times = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        port.sfista(pop, B, L, cfg.lam, 1, project=True)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    step = sum(times) / len(times)
+    value = cfg.m * cfg.m / step / 1e6
+    line = {
+        "metric": "sFISTA Mpixel*iterations/s", "value": round(value, 4), "unit": "Mpixel*iterations/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE cfg2)",
+        "config": {"workload": f"{args.config}: one projected sFISTA iteration per step on the CPU port",
+                   "global_batch": 1, "parallelism": "cpu"},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(value, 4), "unit": "Mpixel*iterations/s", "cores": threads,
+                         "kind": "port", "sample": f"1 iteration of {cfg.name} per step"},
+        "e2e": {"value": round(value, 4), "unit": "Mpixel*iterations/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

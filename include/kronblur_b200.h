@@ -1,0 +1,124 @@
+/*
+ * kronblur_b200.h — C ABI of the B200 (sm_100a) sFISTA hot path.
+ *
+ * The reference package (kronblur, pure Python) has no native interface of its own; this header is
+ * what its solver layer would bind through ctypes. Each entry point names the
+ * reference function it replaces. All array pointers are DEVICE pointers to contiguous row-major
+ * (batch, m, n) planes of the operator's dtype (float64 or float32); `stream` is a cudaStream_t
+ * (pass torch.cuda.current_stream().cuda_stream). Every call is stream ordered and returns a
+ * KB_* status; kb_last_error() gives the message of the last failing call on this thread.
+ *
+ * Band convention: along an axis the factor F(c) (kronblur structured.py:111-123) acts as the
+ * stencil y[s] = sum_d c_d * x~(s - d) with c_d = c[j + d] (c the length-n generator, j its
+ * 1-based anchor). A band is given as its first offset `dlo` and its `w` taps c_dlo..c_{dlo+w-1}
+ * for every term (zero outside). bc = KB_BC_ZERO means Toeplitz factors (zero extension),
+ * KB_BC_REFLECTIVE means Toeplitz+Hankel factors (single half-sample fold at each edge).
+ */
+#ifndef KRONBLUR_B200_H
+#define KRONBLUR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KB_OK 0
+#define KB_ERR_ARGUMENT 2 /* kronblur.errors.ArgumentError (CLI exit code 2, cli.py:34) */
+#define KB_ERR_CUDA 3     /* CUDA runtime failure */
+#define KB_ERR_NUMERIC 4  /* kronblur.errors.NumericError */
+
+#define KB_F64 0
+#define KB_F32 1
+
+#define KB_BC_ZERO 0
+#define KB_BC_REFLECTIVE 1
+
+typedef struct kb_op kb_op; /* immutable device copy of a KronOperator's factor bands */
+
+/* Library version string and the sm target it was built for. */
+const char* kb_version(void);
+/* Message of the last failing call on the calling thread ("" if none). */
+const char* kb_last_error(void);
+
+/*
+ * Upload a KronOperator (kron.py:61-86) — or `batch` operators of equal shape and term count —
+ * as device tap tables. a_* describe the H_i (axis 0) bands, b_* the K_i (axis 1) bands; the
+ * value arrays are [batch][r][w] float64. bc_a / bc_b select Toeplitz or Toeplitz+Hankel per
+ * axis (decompose() uses the same kind on both, kron.py:185-195). Replaces the per-factor
+ * FFT plans built by structured.py:97-108.
+ */
+int kb_op_create(kb_op** out, int dtype, int m, int n, int r, int batch, int bc_a, int bc_b,
+                 int a_dlo, int a_w, const double* a_taps, int b_dlo, int b_w,
+                 const double* b_taps);
+int kb_op_destroy(kb_op* op);
+/* Device workspace (bytes) the calls below need for this operator. */
+size_t kb_workspace_bytes(const kb_op* op);
+
+/* Y = sum_i H_i X K_i^T  — kron.py:218-225 (kron_apply). */
+int kb_apply(const kb_op* op, const void* X, void* Y, void* work, void* stream);
+/* X = sum_i H_i^T Y K_i  — kron.py:228-235 (kron_apply_adjoint). */
+int kb_apply_adjoint(const kb_op* op, const void* Y, void* X, void* work, void* stream);
+
+/*
+ * `iters` sFISTA iterations k = k0+1 .. k0+iters of solvers.py:168-174 (the _engine loop body,
+ * no history): R = A Y - B; G = A^T R; x = (L y - G)/(L + lam^2) [then x = max(x, 0) keeping NaN
+ * when project != 0]; y = x + beta[k-1] (x - x_prev). X holds x_{k0} on entry and x_{k0+iters}
+ * on exit, Y holds y_{k0+1} on entry and y_{k0+iters+1} on exit (both in place).
+ * beta: host array, beta[k-1] = (t_k - 1)/t_{k+1} from momentum_next (solvers.py:96-101).
+ * L: host array [batch] (SolveConfig.lipschitz per image). nonfinite: device int, atomically
+ * min-ed with the first k whose x had a non-finite entry (solvers.py:175-176); initialise it
+ * to INT_MAX. norms: optional device double[iters][4][batch] receiving per iteration
+ * ||x_k - x_{k-1}||^2, ||x_{k-1}||^2, ||x_k||^2 (solvers.py:178-179), or NULL.
+ * use_graph != 0 captures the launch sequence in a CUDA graph (same arithmetic).
+ */
+int kb_sfista_run(const kb_op* op, const void* B, void* X, void* Y, void* work,
+                  const double* beta, int k0, int iters, const double* L, double lam,
+                  int project, int* nonfinite, double* norms, int use_graph, void* stream);
+
+/*
+ * Power iteration of solvers.py:104-130 on A^T A: v (device, normalised start vector drawn on
+ * the host from rand.stream(seed, "lipschitz")) is overwritten; w is a scratch plane of the same
+ * size. hist (device double[iters][2][batch]) receives rho_k = <v_k, w_k> and ||w_k||^2 per
+ * iteration; the host applies the zero-operator rule and the 1.05 safety factor.
+ */
+int kb_power_iter(const kb_op* op, void* v, void* w, void* work, int iters, double* hist,
+                  void* stream);
+
+/*
+ * Row-block sharded operator application (multi-GPU halo exchange): like kb_apply /
+ * kb_apply_adjoint on the local rows [g0, g0+m_local) of a global m_global x n image whose
+ * plane pointer X addresses local row 0 and whose rows -halo_lo .. m_local+halo_hi-1 are
+ * readable (filled by the neighbours). The operator must have been created with m = m_local.
+ */
+int kb_apply_block(const kb_op* op, int adjoint, const void* X, void* Y, void* work, int g0,
+                   int m_global, int halo_lo, int halo_hi, void* stream);
+/* sFISTA epilogue pieces for the sharded solver: R = A Y - B and the fused adjoint+update,
+ * each on a local row block (same halo contract as kb_apply_block). */
+int kb_block_residual(const kb_op* op, const void* Yh, const void* B, void* R, void* work,
+                      int g0, int m_global, int halo_lo, int halo_hi, void* stream);
+int kb_block_update(const kb_op* op, const void* Rh, void* X, void* Y, void* work, int g0,
+                    int m_global, int halo_lo, int halo_hi, double beta, int k, double L,
+                    double lam, int project, int* nonfinite, void* stream);
+
+/*
+ * Measurement helpers used by bench.py (no reference counterpart).
+ * kb_fma_peak: FMA throughput of this GPU in TFLOP/s for dtype (roofline denominator).
+ * kb_time_passes: average device time (ms, CUDA events on `stream`) of each of the four kernels of
+ * one sFISTA iteration, `reps` back-to-back launches each: ms4 = {forward pass A, forward pass B
+ * (residual epilogue), adjoint pass A, adjoint pass B (update epilogue, beta = 0)}. X/Yio are
+ * overwritten.
+ */
+int kb_fma_peak(int dtype, float* tflops, void* stream);
+int kb_time_passes(const kb_op* op, const void* Y, const void* B, void* R, void* X, void* Yio,
+                   void* work, int reps, const double* L, double lam, int* nonfinite,
+                   float* ms4, void* stream);
+
+/* Maximum half band width supported per axis. */
+int kb_max_half_width(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KRONBLUR_B200_H */

@@ -1,0 +1,46 @@
+"""B200-native sFISTA hot path with the kronblur solver/operator API (arXiv 1901.00913).
+
+Drop-in entry points (same names, signatures and error behaviour as the reference package
+``kronblur``): ``sfista``, ``kron_apply``, ``kron_apply_adjoint``, ``estimate_lipschitz``,
+``objective_matrix``, ``decompose``. The arithmetic of the first four runs in the sm_100a kernels of
+``libkb_b200.so`` (C ABI: include/kronblur_b200.h); ``decompose`` is the one-time host setup.
+``install()`` reroutes an imported ``kronblur`` to these functions.
+"""
+
+from .errors import ArgumentError, CapacityError, FormatError, KronblurError, NumericError
+from .kron import (
+    KronOperator,
+    KronTerm,
+    decompose,
+    kron_apply,
+    kron_apply_adjoint,
+    kron_to_dense,
+    truncation_error,
+)
+from .psf import BoundaryCondition, Psf, pad_to, unvec, vec
+from .solvers import (
+    LIPSCHITZ_SAFETY,
+    IterationRecord,
+    SolveConfig,
+    SolveOptions,
+    SolveRun,
+    estimate_lipschitz,
+    lipschitz,
+    make_ops,
+    momentum_next,
+    momentum_table,
+    objective,
+    objective_matrix,
+    sfista,
+    sfista_batch,
+)
+from .structured import FactorKind, StructuredFactor, factor_band, factor_to_dense, hank, toep, toep_plus_hank
+
+__version__ = "0.1.0"
+
+
+def install(kronblur_module=None):
+    """Patch an imported ``kronblur`` so its solver path runs here (see install.py)."""
+    from .install import install as _install
+
+    return _install(kronblur_module)

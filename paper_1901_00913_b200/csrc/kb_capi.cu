@@ -1,0 +1,740 @@
+// kb_capi.cu — C ABI (include/kronblur_b200.h) over the sm_100a pass kernels.
+//
+// Owns the device tap tables of an operator, the workspace layout, and the native iteration
+// loop of the sFISTA engine (kronblur solvers.py:168-174) including optional CUDA-graph
+// capture of the whole launch sequence. No torch types cross this boundary.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/kronblur_b200.h"
+#include "kb_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define KB_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return fail(KB_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e));     \
+  } while (0)
+
+#define KB_TRY(...)           \
+  do {                        \
+    int _rc = (__VA_ARGS__);  \
+    if (_rc != KB_OK) return _rc; \
+  } while (0)
+
+constexpr int kMaxHalf = 1024;
+constexpr int kRA = 8;   // pass A rows per warp
+constexpr int kRB = 16;  // pass B columns per warp
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct GraphCache {
+  std::mutex mu;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<unsigned char> key;
+};
+
+}  // namespace
+
+struct kb_op {
+  int dtype, m, n, r, batch, bc_a, bc_b;
+  int Ha, Wpa, Hb, Wpb;
+  int G;
+  void* ta_conv = nullptr;  // [batch][r][Wpa] taps c_{H-k}
+  void* ta_corr = nullptr;  // [batch][r][Wpa] taps c_{k-H}
+  void* tb_conv = nullptr;
+  void* tb_corr = nullptr;
+  GraphCache* graph = nullptr;
+};
+
+namespace {
+
+size_t elem(const kb_op* op) { return op->dtype == KB_F64 ? 8 : 4; }
+size_t plane_elems(const kb_op* op) { return (size_t)op->m * op->n; }
+
+// workspace: [Z: batch*r planes][R: batch planes][partials][scalars]
+struct Work {
+  void* z;
+  void* rp;
+  void* fold;  // [batch][m][2*Hb] adjoint column-fold corrections
+  double* partials;
+  double* scal;  // [4][batch]: L, denom
+  size_t bytes;
+};
+
+int pass_b_blocks(const kb_op* op) {
+  const int TQ = kb::kNW * kRB;
+  return ((op->n + TQ - 1) / TQ) * ((op->m + 31) / 32);
+}
+
+Work layout(const kb_op* op, void* base) {
+  Work w;
+  size_t off = 0;
+  const size_t pe = plane_elems(op) * elem(op);
+  unsigned char* b = static_cast<unsigned char*>(base);
+  w.z = b ? b + off : nullptr;
+  off = align_up(off + pe * op->r * op->batch, 256);
+  w.rp = b ? b + off : nullptr;
+  off = align_up(off + pe * op->batch, 256);
+  w.fold = b ? b + off : nullptr;
+  off = align_up(off + elem(op) * (size_t)op->batch * op->m * 2 * std::max(op->Hb, 1), 256);
+  w.partials = b ? reinterpret_cast<double*>(b + off) : nullptr;
+  off = align_up(off + sizeof(double) * 4 * (size_t)op->batch * pass_b_blocks(op), 256);
+  w.scal = b ? reinterpret_cast<double*>(b + off) : nullptr;
+  off = align_up(off + sizeof(double) * 4 * (size_t)op->batch, 256);
+  w.bytes = off;
+  return w;
+}
+
+int pick_group(int r, int gmax) {
+  int best = 1;
+  long best_cost = LONG_MAX;
+  static const int cands[] = {8, 6, 5, 4, 3, 2, 1};
+  for (int G : cands) {
+    if (G > gmax) continue;
+    const long groups = (r + G - 1) / G;
+    const long cost = groups * (G + 2);  // padded term work + per-group tile re-read
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = G;
+    }
+  }
+  return best;
+}
+
+// Opt a kernel into the full 227 KB of shared memory (minus its static shared memory). Keyed by
+// the kernel's address: instantiations that differ only in a template value share a type.
+std::mutex g_smem_mu;
+std::unordered_map<const void*, int> g_smem_limit;
+
+template <typename K>
+int allow_smem(K kernel, size_t dyn_bytes) {
+  const void* key = reinterpret_cast<const void*>(kernel);
+  int limit;
+  {
+    std::lock_guard<std::mutex> lock(g_smem_mu);
+    auto it = g_smem_limit.find(key);
+    if (it == g_smem_limit.end()) {
+      cudaFuncAttributes attr;
+      KB_CUDA(cudaFuncGetAttributes(&attr, kernel));
+      limit = 227 * 1024 - (int)attr.sharedSizeBytes;
+      KB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
+      g_smem_limit[key] = limit;
+    } else {
+      limit = it->second;
+    }
+  }
+  if (dyn_bytes > (size_t)limit) return fail(KB_ERR_ARGUMENT, "band too wide for the shared-memory tile");
+  return KB_OK;
+}
+
+template <typename T, int G>
+int launch_a_g(const T* in, long long in_bs, T* z, long long z_ps, long long z_bs, int r,
+               const T* tin, long long t_bs, const kb::AxisGeom& g, const double* nw2, int batch,
+               cudaStream_t s) {
+  constexpr int TP = kb::kNW * kRA;
+  const size_t smem = sizeof(T) * ((size_t)(TP + g.Wp - 1) * 32 + (size_t)G * g.Wp);
+  auto kern = kb::kb_pass_a<T, G, kRA>;
+  KB_TRY(allow_smem(kern, smem));
+  dim3 grid((g.other + 31) / 32, (g.len + TP - 1) / TP, batch);
+  dim3 block(32, kb::kNW);
+  kern<<<grid, block, smem, s>>>(in, in_bs, z, z_ps, z_bs, r, tin, t_bs, g, nw2);
+  KB_CUDA(cudaGetLastError());
+  return KB_OK;
+}
+
+template <typename T>
+int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeom& g,
+             const double* nw2, cudaStream_t s) {
+  const long long in_bs = (long long)plane_elems(op);
+  const long long z_ps = (long long)g.len * g.other;
+  const long long z_bs = z_ps * op->r;
+  const long long t_bs = (long long)op->r * g.Wp;
+#define KB_A(GG) return launch_a_g<T, GG>(in, in_bs, z, z_ps, z_bs, op->r, tin, t_bs, g, nw2, op->batch, s)
+  switch (op->G) {
+    case 1: KB_A(1);
+    case 2: KB_A(2);
+    case 3: KB_A(3);
+    case 4: KB_A(4);
+    case 5: KB_A(5);
+    default: break;
+  }
+  if constexpr (sizeof(T) == 4) {  // fp32 keeps larger term groups in registers
+    switch (op->G) {
+      case 6: KB_A(6);
+      case 8: KB_A(8);
+      default: break;
+    }
+  }
+#undef KB_A
+  return fail(KB_ERR_ARGUMENT, "unsupported term group size");
+}
+
+template <typename T, int MODE>
+int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g,
+             const kb::Epi<T>& e, cudaStream_t s) {
+  constexpr int TQ = kb::kNW * kRB;
+  const int S = (TQ + g.Wp - 1) | 1;
+  const size_t smem = sizeof(T) * (2 * 32 * (size_t)S + 2 * (size_t)g.Wp);
+  auto kern = kb::kb_pass_b<T, kRB, MODE>;
+  KB_TRY(allow_smem(kern, smem));
+  const long long z_ps = (long long)g.len * g.other;
+  const long long z_bs = z_ps * op->r;
+  const long long t_bs = (long long)op->r * g.Wp;
+  dim3 grid((g.len + TQ - 1) / TQ, (g.other + 31) / 32, op->batch);
+  dim3 block(32, kb::kNW);
+  kern<<<grid, block, smem, s>>>(z, z_ps, z_bs, op->r, tin, t_bs, g, e);
+  KB_CUDA(cudaGetLastError());
+  return KB_OK;
+}
+
+// Local row block of a (possibly sharded) image: rows [g0, g0+m) of m_global, with halo rows.
+struct RowBlock {
+  int g0, mg, hlo, hhi;
+};
+
+kb::AxisGeom geom_a(const kb_op* op, int adjoint, const RowBlock& rb) {
+  kb::AxisGeom g;
+  g.len = op->m;
+  g.other = op->n;
+  g.H = op->Ha;
+  g.Wp = op->Wpa;
+  g.fill = !adjoint && op->bc_a == KB_BC_REFLECTIVE;
+  g.g0 = rb.g0;
+  g.Mg = rb.mg;
+  g.halo_lo = rb.hlo;
+  g.halo_hi = rb.hhi;
+  return g;
+}
+
+kb::AxisGeom geom_b(const kb_op* op, int adjoint) {
+  kb::AxisGeom g;
+  g.len = op->n;
+  g.other = op->m;
+  g.H = op->Hb;
+  g.Wp = op->Wpb;
+  g.fill = !adjoint && op->bc_b == KB_BC_REFLECTIVE;
+  g.g0 = 0;
+  g.Mg = op->n;
+  g.halo_lo = 0;
+  g.halo_hi = 0;
+  return g;
+}
+
+template <typename T>
+kb::Epi<T> epi_base(const kb_op* op, int mode) {
+  kb::Epi<T> e;
+  std::memset(&e, 0, sizeof(e));
+  e.mode = mode;
+  e.bstride = (long long)plane_elems(op);
+  return e;
+}
+
+// Stage 0/2: pass A (forward / adjoint) incl. the adjoint's row fold. Stage 1/3 go through
+// stage_b below (the column fold is launched just before pass B).
+template <typename T>
+int stage_a(const kb_op* op, int adjoint, const T* in, const Work& w, const RowBlock& rb,
+            const double* nw2, cudaStream_t s) {
+  T* z = static_cast<T*>(w.z);
+  const kb::AxisGeom ga = geom_a(op, adjoint, rb);
+  KB_TRY(launch_a<T>(op, in, z, static_cast<const T*>(adjoint ? op->ta_corr : op->ta_conv), ga, nw2, s));
+  if (adjoint && op->bc_a == KB_BC_REFLECTIVE && op->Ha > 0) {
+    const long long z_ps = (long long)op->m * op->n;
+    dim3 grid((op->n + 127) / 128, 2 * op->Ha, op->batch);
+    kb::kb_fold_rows<T><<<grid, 128, 0, s>>>(in, z_ps, z, z_ps, z_ps * op->r, op->r,
+                                              static_cast<const T*>(op->ta_conv),
+                                              (long long)op->r * op->Wpa, ga);
+    KB_CUDA(cudaGetLastError());
+  }
+  return KB_OK;
+}
+
+template <typename T, int MODE>
+int stage_b(const kb_op* op, int adjoint, kb::Epi<T> e, const Work& w, cudaStream_t s) {
+  const T* z = static_cast<const T*>(w.z);
+  const kb::AxisGeom gb = geom_b(op, adjoint);
+  if (adjoint && op->bc_b == KB_BC_REFLECTIVE && op->Hb > 0) {
+    const int slots = 2 * op->Hb;
+    const int bx = (slots + 31) / 32 * 32;
+    const int by = std::max(1, 256 / bx);
+    dim3 grid((op->m + by - 1) / by, 1, op->batch);
+    const long long z_ps = (long long)op->m * op->n;
+    kb::kb_fold_cols<T><<<grid, dim3(bx, by), 0, s>>>(z, z_ps, z_ps * op->r, op->r,
+                                                       static_cast<const T*>(op->tb_conv),
+                                                       (long long)op->r * op->Wpb, gb,
+                                                       static_cast<T*>(w.fold));
+    KB_CUDA(cudaGetLastError());
+    e.fold = static_cast<const T*>(w.fold);
+    e.foldH = op->Hb;
+  }
+  return launch_b<T, MODE>(op, z, static_cast<const T*>(adjoint ? op->tb_corr : op->tb_conv), gb, e, s);
+}
+
+// ---- operator application (one direction) ------------------------------------------------
+template <typename T>
+int apply_t(const kb_op* op, int adjoint, const T* X, T* Y, const Work& w, const RowBlock& rb,
+            cudaStream_t s) {
+  KB_TRY(stage_a<T>(op, adjoint, X, w, rb, nullptr, s));
+  kb::Epi<T> e = epi_base<T>(op, kb::EPI_PLAIN);
+  e.out = Y;
+  return stage_b<T, kb::EPI_PLAIN>(op, adjoint, e, w, s);
+}
+
+template <typename T>
+int residual_t(const kb_op* op, const T* Y, const T* B, T* R, const Work& w, const RowBlock& rb,
+               cudaStream_t s) {
+  KB_TRY(stage_a<T>(op, 0, Y, w, rb, nullptr, s));
+  kb::Epi<T> e = epi_base<T>(op, kb::EPI_RESID);
+  e.out = R;
+  e.bsub = B;
+  return stage_b<T, kb::EPI_RESID>(op, 0, e, w, s);
+}
+
+template <typename T>
+kb::Epi<T> update_epi(const kb_op* op, T* X, T* Y, const Work& w, double beta, int k,
+                      const double* Ldev, const double* ddev, int project, int* nonfinite,
+                      bool norms) {
+  kb::Epi<T> e = epi_base<T>(op, kb::EPI_UPDATE);
+  e.x = X;
+  e.y = Y;
+  e.L = Ldev;
+  e.denom = ddev;
+  e.beta = beta;
+  e.project = project;
+  e.k = k;
+  e.nonfinite = nonfinite;
+  e.partials = w.partials;
+  e.want_norms = norms;
+  return e;
+}
+
+template <typename T>
+int update_t(const kb_op* op, const T* R, T* X, T* Y, const Work& w, const RowBlock& rb,
+             double beta, int k, const double* Ldev, const double* ddev, int project,
+             int* nonfinite, double* norms_out, cudaStream_t s) {
+  KB_TRY(stage_a<T>(op, 1, R, w, rb, nullptr, s));
+  KB_TRY((stage_b<T, kb::EPI_UPDATE>(op, 1, update_epi<T>(op, X, Y, w, beta, k, Ldev, ddev, project,
+                                                          nonfinite, norms_out != nullptr), w, s)));
+  if (norms_out) {
+    kb::kb_reduce_partials<<<op->batch, 256, 0, s>>>(w.partials, pass_b_blocks(op), 3, norms_out,
+                                                      op->batch, 1);
+    KB_CUDA(cudaGetLastError());
+  }
+  return KB_OK;
+}
+
+template <typename T>
+int sfista_launches(const kb_op* op, const T* B, T* X, T* Y, const Work& w, const double* beta,
+                    int k0, int iters, int project, int* nonfinite, double* norms,
+                    cudaStream_t s) {
+  T* R = static_cast<T*>(w.rp);
+  const RowBlock rb{0, op->m, 0, 0};
+  for (int it = 0; it < iters; ++it) {
+    const int k = k0 + it + 1;
+    KB_TRY(residual_t<T>(op, Y, B, R, w, rb, s));
+    KB_TRY(update_t<T>(op, R, X, Y, w, rb, beta[k - 1], k, w.scal, w.scal + op->batch, project,
+                       nonfinite, norms ? norms + (size_t)it * 4 * op->batch : nullptr, s));
+  }
+  return KB_OK;
+}
+
+template <typename T>
+int power_t(const kb_op* op, T* v, T* wbuf, const Work& w, int iters, double* hist,
+            cudaStream_t s) {
+  T* u = static_cast<T*>(w.rp);
+  const RowBlock rb{0, op->m, 0, 0};
+  for (int k = 0; k < iters; ++k) {
+    T* cur = (k & 1) ? wbuf : v;   // holds w_{k-1} (unnormalised) or v_0
+    T* nxt = (k & 1) ? v : wbuf;
+    const double* nw2 = k == 0 ? nullptr : hist + (size_t)(k - 1) * 2 * op->batch + op->batch;
+    KB_TRY(stage_a<T>(op, 0, cur, w, rb, nw2, s));
+    kb::Epi<T> e1 = epi_base<T>(op, kb::EPI_PLAIN);
+    e1.out = u;
+    KB_TRY((stage_b<T, kb::EPI_PLAIN>(op, 0, e1, w, s)));
+    KB_TRY(stage_a<T>(op, 1, u, w, rb, nullptr, s));
+    kb::Epi<T> e2 = epi_base<T>(op, kb::EPI_POWER);
+    e2.out = nxt;
+    e2.vin = cur;
+    e2.vnw2 = nw2;
+    e2.partials = w.partials;
+    KB_TRY((stage_b<T, kb::EPI_POWER>(op, 1, e2, w, s)));
+    kb::kb_reduce_partials<<<op->batch, 256, 0, s>>>(w.partials, pass_b_blocks(op), 2,
+                                                      hist + (size_t)k * 2 * op->batch,
+                                                      op->batch, 1);
+    KB_CUDA(cudaGetLastError());
+  }
+  return KB_OK;
+}
+
+int check_op(const kb_op* op) {
+  if (!op) return fail(KB_ERR_ARGUMENT, "null operator handle");
+  return KB_OK;
+}
+
+// table build: conv[k] = c_{H-k}, corr[k] = c_{k-H}, k in [0, 2H], zero elsewhere
+template <typename T>
+void build_tables(int dlo, int w, const double* taps, int nrows, int H, int Wp,
+                  std::vector<T>& conv, std::vector<T>& corr) {
+  conv.assign((size_t)nrows * Wp, T(0));
+  corr.assign((size_t)nrows * Wp, T(0));
+  for (int row = 0; row < nrows; ++row) {
+    for (int t = 0; t < w; ++t) {
+      const int d = dlo + t;
+      const double c = taps[(size_t)row * w + t];
+      conv[(size_t)row * Wp + (H - d)] = (T)c;
+      corr[(size_t)row * Wp + (H + d)] = (T)c;
+    }
+  }
+}
+
+template <typename T>
+int upload_tables(kb_op* op, int dlo, int w, const double* taps, int H, int Wp, void** conv_d,
+                  void** corr_d) {
+  std::vector<T> conv, corr;
+  const int nrows = op->batch * op->r;
+  build_tables<T>(dlo, w, taps, nrows, H, Wp, conv, corr);
+  const size_t bytes = conv.size() * sizeof(T);
+  KB_CUDA(cudaMalloc(conv_d, bytes));
+  KB_CUDA(cudaMalloc(corr_d, bytes));
+  KB_CUDA(cudaMemcpy(*conv_d, conv.data(), bytes, cudaMemcpyHostToDevice));
+  KB_CUDA(cudaMemcpy(*corr_d, corr.data(), bytes, cudaMemcpyHostToDevice));
+  return KB_OK;
+}
+
+void free_op(kb_op* op) {
+  if (!op) return;
+  cudaFree(op->ta_conv);
+  cudaFree(op->ta_corr);
+  cudaFree(op->tb_conv);
+  cudaFree(op->tb_corr);
+  if (op->graph) {
+    if (op->graph->exec) cudaGraphExecDestroy(op->graph->exec);
+    delete op->graph;
+  }
+  delete op;
+}
+
+
+// ---- measurement helpers (bench.py) --------------------------------------------------------
+template <typename T>
+__global__ void kb_fma_burn(T* out, int iters, T a, T b) {
+  T x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = T(threadIdx.x + i) * T(1e-3);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = kb::kb_fma(x[i], a, b);
+  }
+  T s = T(0);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == T(-12345.678)) out[0] = s;  // never true; keeps the chains alive
+}
+
+template <typename T>
+int fma_peak_t(float* tflops, cudaStream_t s) {
+  int dev = 0, sms = 0;
+  KB_CUDA(cudaGetDevice(&dev));
+  KB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  T* out = nullptr;
+  KB_CUDA(cudaMalloc(&out, sizeof(T)));
+  const int blocks = sms * 8, threads = 256, iters = sizeof(T) == 8 ? 4096 : 16384;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  kb_fma_burn<T><<<blocks, threads, 0, s>>>(out, iters, T(0.999999), T(1e-7));  // warm-up
+  cudaEventRecord(e0, s);
+  const int reps = 5;
+  for (int r = 0; r < reps; ++r) kb_fma_burn<T><<<blocks, threads, 0, s>>>(out, iters, T(0.999999), T(1e-7));
+  cudaEventRecord(e1, s);
+  cudaError_t ce = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  if (ce != cudaSuccess) return fail(KB_ERR_CUDA, cudaGetErrorString(ce));
+  const double flops = 2.0 * 8.0 * (double)iters * threads * blocks * reps;
+  *tflops = (float)(flops / (ms * 1e-3) / 1e12);
+  return KB_OK;
+}
+
+template <typename T>
+int time_passes_t(const kb_op* op, const T* Y, const T* B, T* R, T* X, T* Yio, const Work& w,
+                  int reps, float* ms4, int* nonfinite, cudaStream_t s) {
+  cudaEvent_t ev[8];
+  for (auto& e : ev) cudaEventCreate(&e);
+  const RowBlock rb{0, op->m, 0, 0};
+  kb::Epi<T> er = epi_base<T>(op, kb::EPI_RESID);
+  er.out = R;
+  er.bsub = B;
+  const kb::Epi<T> eu = update_epi<T>(op, X, Yio, w, 0.0, 1, w.scal, w.scal + op->batch, 1,
+                                      nonfinite, false);
+  int rc = KB_OK;
+  for (int phase = 0; phase < 4 && rc == KB_OK; ++phase) {
+    for (int rep = -1; rep < reps && rc == KB_OK; ++rep) {  // rep -1: untimed warm-up
+      if (rep == 0) cudaEventRecord(ev[2 * phase], s);
+      switch (phase) {
+        case 0: rc = stage_a<T>(op, 0, Y, w, rb, nullptr, s); break;
+        case 1: rc = stage_b<T, kb::EPI_RESID>(op, 0, er, w, s); break;
+        case 2: rc = stage_a<T>(op, 1, R, w, rb, nullptr, s); break;
+        default: rc = stage_b<T, kb::EPI_UPDATE>(op, 1, eu, w, s); break;
+      }
+    }
+    cudaEventRecord(ev[2 * phase + 1], s);
+  }
+  cudaError_t ce = cudaEventSynchronize(ev[7]);
+  if (rc == KB_OK && ce == cudaSuccess) {
+    for (int phase = 0; phase < 4; ++phase) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[2 * phase], ev[2 * phase + 1]);
+      ms4[phase] = ms / reps;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (rc != KB_OK) return rc;
+  if (ce != cudaSuccess) return fail(KB_ERR_CUDA, cudaGetErrorString(ce));
+  return KB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* kb_version(void) { return "kronblur_b200 0.1 sm_100a"; }
+const char* kb_last_error(void) { return g_err.c_str(); }
+int kb_max_half_width(void) { return kMaxHalf; }
+
+int kb_op_create(kb_op** out, int dtype, int m, int n, int r, int batch, int bc_a, int bc_b,
+                 int a_dlo, int a_w, const double* a_taps, int b_dlo, int b_w,
+                 const double* b_taps) {
+  if (!out) return fail(KB_ERR_ARGUMENT, "null output handle");
+  *out = nullptr;
+  if (dtype != KB_F64 && dtype != KB_F32) return fail(KB_ERR_ARGUMENT, "dtype must be KB_F64 or KB_F32");
+  if (m < 1 || n < 1 || r < 1 || batch < 1) return fail(KB_ERR_ARGUMENT, "m, n, r, batch must be >= 1");
+  if (a_w < 1 || b_w < 1 || !a_taps || !b_taps) return fail(KB_ERR_ARGUMENT, "empty band");
+  if ((bc_a != KB_BC_ZERO && bc_a != KB_BC_REFLECTIVE) || (bc_b != KB_BC_ZERO && bc_b != KB_BC_REFLECTIVE))
+    return fail(KB_ERR_ARGUMENT, "bad boundary condition");
+  const int Ha = std::max(std::abs(a_dlo), std::abs(a_dlo + a_w - 1));
+  const int Hb = std::max(std::abs(b_dlo), std::abs(b_dlo + b_w - 1));
+  if (Ha > kMaxHalf || Hb > kMaxHalf) return fail(KB_ERR_ARGUMENT, "band half width exceeds kb_max_half_width()");
+  kb_op* op = new kb_op();
+  op->dtype = dtype;
+  op->m = m;
+  op->n = n;
+  op->r = r;
+  op->batch = batch;
+  op->bc_a = bc_a;
+  op->bc_b = bc_b;
+  op->Ha = Ha;
+  op->Hb = Hb;
+  op->Wpa = (2 * Ha + 1 + kb::kUB - 1) / kb::kUB * kb::kUB;
+  op->Wpb = (2 * Hb + 1 + kb::kUB - 1) / kb::kUB * kb::kUB;
+  op->G = pick_group(r, dtype == KB_F64 ? 5 : 8);
+  op->graph = new GraphCache();
+  int rc;
+  if (dtype == KB_F64) {
+    rc = upload_tables<double>(op, a_dlo, a_w, a_taps, Ha, op->Wpa, &op->ta_conv, &op->ta_corr);
+    if (rc == KB_OK) rc = upload_tables<double>(op, b_dlo, b_w, b_taps, Hb, op->Wpb, &op->tb_conv, &op->tb_corr);
+  } else {
+    rc = upload_tables<float>(op, a_dlo, a_w, a_taps, Ha, op->Wpa, &op->ta_conv, &op->ta_corr);
+    if (rc == KB_OK) rc = upload_tables<float>(op, b_dlo, b_w, b_taps, Hb, op->Wpb, &op->tb_conv, &op->tb_corr);
+  }
+  if (rc != KB_OK) {
+    free_op(op);
+    return rc;
+  }
+  *out = op;
+  return KB_OK;
+}
+
+int kb_op_destroy(kb_op* op) {
+  free_op(op);
+  return KB_OK;
+}
+
+size_t kb_workspace_bytes(const kb_op* op) { return op ? layout(op, nullptr).bytes : 0; }
+
+int kb_apply(const kb_op* op, const void* X, void* Y, void* work, void* stream) {
+  KB_TRY(check_op(op));
+  Work w = layout(op, work);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (op->dtype == KB_F64)
+    return apply_t<double>(op, 0, static_cast<const double*>(X), static_cast<double*>(Y), w, RowBlock{0, op->m, 0, 0}, s);
+  return apply_t<float>(op, 0, static_cast<const float*>(X), static_cast<float*>(Y), w, RowBlock{0, op->m, 0, 0}, s);
+}
+
+int kb_apply_adjoint(const kb_op* op, const void* Y, void* X, void* work, void* stream) {
+  KB_TRY(check_op(op));
+  Work w = layout(op, work);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (op->dtype == KB_F64)
+    return apply_t<double>(op, 1, static_cast<const double*>(Y), static_cast<double*>(X), w, RowBlock{0, op->m, 0, 0}, s);
+  return apply_t<float>(op, 1, static_cast<const float*>(Y), static_cast<float*>(X), w, RowBlock{0, op->m, 0, 0}, s);
+}
+
+int kb_apply_block(const kb_op* op, int adjoint, const void* X, void* Y, void* work, int g0,
+                   int m_global, int halo_lo, int halo_hi, void* stream) {
+  KB_TRY(check_op(op));
+  if (g0 < 0 || g0 + op->m > m_global || halo_lo < 0 || halo_hi < 0)
+    return fail(KB_ERR_ARGUMENT, "bad row block");
+  Work w = layout(op, work);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (op->dtype == KB_F64)
+    return apply_t<double>(op, adjoint, static_cast<const double*>(X), static_cast<double*>(Y), w, RowBlock{g0, m_global, halo_lo, halo_hi}, s);
+  return apply_t<float>(op, adjoint, static_cast<const float*>(X), static_cast<float*>(Y), w, RowBlock{g0, m_global, halo_lo, halo_hi}, s);
+}
+
+int kb_block_residual(const kb_op* op, const void* Yh, const void* B, void* R, void* work,
+                      int g0, int m_global, int halo_lo, int halo_hi, void* stream) {
+  KB_TRY(check_op(op));
+  if (g0 < 0 || g0 + op->m > m_global || halo_lo < 0 || halo_hi < 0)
+    return fail(KB_ERR_ARGUMENT, "bad row block");
+  Work w = layout(op, work);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (op->dtype == KB_F64)
+    return residual_t<double>(op, static_cast<const double*>(Yh), static_cast<const double*>(B), static_cast<double*>(R), w, RowBlock{g0, m_global, halo_lo, halo_hi}, s);
+  return residual_t<float>(op, static_cast<const float*>(Yh), static_cast<const float*>(B), static_cast<float*>(R), w, RowBlock{g0, m_global, halo_lo, halo_hi}, s);
+}
+
+int kb_block_update(const kb_op* op, const void* Rh, void* X, void* Y, void* work, int g0,
+                    int m_global, int halo_lo, int halo_hi, double beta, int k, double L,
+                    double lam, int project, int* nonfinite, void* stream) {
+  KB_TRY(check_op(op));
+  if (op->batch != 1) return fail(KB_ERR_ARGUMENT, "row-block update needs batch == 1");
+  if (g0 < 0 || g0 + op->m > m_global || halo_lo < 0 || halo_hi < 0)
+    return fail(KB_ERR_ARGUMENT, "bad row block");
+  Work w = layout(op, work);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const double host[2] = {L, L + lam * lam};
+  KB_CUDA(cudaMemcpyAsync(w.scal, host, sizeof(host), cudaMemcpyHostToDevice, s));
+  if (op->dtype == KB_F64)
+    return update_t<double>(op, static_cast<const double*>(Rh), static_cast<double*>(X), static_cast<double*>(Y), w, RowBlock{g0, m_global, halo_lo, halo_hi}, beta, k, w.scal, w.scal + 1, project, nonfinite, nullptr, s);
+  return update_t<float>(op, static_cast<const float*>(Rh), static_cast<float*>(X), static_cast<float*>(Y), w, RowBlock{g0, m_global, halo_lo, halo_hi}, beta, k, w.scal, w.scal + 1, project, nonfinite, nullptr, s);
+}
+
+int kb_sfista_run(const kb_op* op, const void* B, void* X, void* Y, void* work,
+                  const double* beta, int k0, int iters, const double* L, double lam,
+                  int project, int* nonfinite, double* norms, int use_graph, void* stream) {
+  KB_TRY(check_op(op));
+  if (!B || !X || !Y || !work || !beta || !L || !nonfinite) return fail(KB_ERR_ARGUMENT, "null argument");
+  if (iters < 0 || k0 < 0) return fail(KB_ERR_ARGUMENT, "iters and k0 must be >= 0");
+  if (iters == 0) return KB_OK;
+  Work w = layout(op, work);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<double> host(2 * (size_t)op->batch);
+  for (int b = 0; b < op->batch; ++b) {
+    host[b] = L[b];
+    host[op->batch + b] = L[b] + lam * lam;
+  }
+  KB_CUDA(cudaMemcpyAsync(w.scal, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  // cudaMemcpyAsync from pageable memory returns after staging, so `host` may go out of scope.
+  auto body = [&](cudaStream_t cs) -> int {
+    if (op->dtype == KB_F64)
+      return sfista_launches<double>(op, static_cast<const double*>(B), static_cast<double*>(X),
+                                     static_cast<double*>(Y), w, beta, k0, iters, project, nonfinite, norms, cs);
+    return sfista_launches<float>(op, static_cast<const float*>(B), static_cast<float*>(X),
+                                  static_cast<float*>(Y), w, beta, k0, iters, project, nonfinite, norms, cs);
+  };
+  if (!use_graph) return body(s);
+
+  // graph path: key = every pointer and scalar the captured launches bake in
+  std::vector<unsigned char> key;
+  auto put = [&](const void* p, size_t nb) {
+    const unsigned char* c = static_cast<const unsigned char*>(p);
+    key.insert(key.end(), c, c + nb);
+  };
+  put(&B, sizeof(B)); put(&X, sizeof(X)); put(&Y, sizeof(Y)); put(&work, sizeof(work));
+  put(&k0, sizeof(k0)); put(&iters, sizeof(iters)); put(&project, sizeof(project));
+  put(&nonfinite, sizeof(nonfinite)); put(&norms, sizeof(norms));
+  put(beta + k0, sizeof(double) * iters);
+  GraphCache* gc = op->graph;
+  std::lock_guard<std::mutex> lock(gc->mu);
+  if (!gc->exec || gc->key != key) {
+    if (gc->exec) {
+      cudaGraphExecDestroy(gc->exec);
+      gc->exec = nullptr;
+    }
+    cudaStream_t cs;
+    KB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t graph;
+    cudaError_t ce = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (ce != cudaSuccess) {
+      cudaStreamDestroy(cs);
+      return fail(KB_ERR_CUDA, std::string("begin capture: ") + cudaGetErrorString(ce));
+    }
+    const int rc = body(cs);
+    ce = cudaStreamEndCapture(cs, &graph);
+    cudaStreamDestroy(cs);
+    if (rc != KB_OK) {
+      if (ce == cudaSuccess) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (ce != cudaSuccess) return fail(KB_ERR_CUDA, std::string("end capture: ") + cudaGetErrorString(ce));
+    ce = cudaGraphInstantiate(&gc->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) {
+      gc->exec = nullptr;
+      return fail(KB_ERR_CUDA, std::string("instantiate: ") + cudaGetErrorString(ce));
+    }
+    gc->key = key;
+  }
+  KB_CUDA(cudaGraphLaunch(gc->exec, s));
+  return KB_OK;
+}
+
+int kb_power_iter(const kb_op* op, void* v, void* wb, void* work, int iters, double* hist,
+                  void* stream) {
+  KB_TRY(check_op(op));
+  if (!v || !wb || !work || !hist || iters < 1) return fail(KB_ERR_ARGUMENT, "bad power-iteration arguments");
+  Work w = layout(op, work);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (op->dtype == KB_F64)
+    return power_t<double>(op, static_cast<double*>(v), static_cast<double*>(wb), w, iters, hist, s);
+  return power_t<float>(op, static_cast<float*>(v), static_cast<float*>(wb), w, iters, hist, s);
+}
+
+int kb_fma_peak(int dtype, float* tflops, void* stream) {
+  if (!tflops) return fail(KB_ERR_ARGUMENT, "null output");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return dtype == KB_F64 ? fma_peak_t<double>(tflops, s) : fma_peak_t<float>(tflops, s);
+}
+
+int kb_time_passes(const kb_op* op, const void* Y, const void* B, void* R, void* X, void* Yio,
+                   void* work, int reps, const double* L, double lam, int* nonfinite,
+                   float* ms4, void* stream) {
+  KB_TRY(check_op(op));
+  if (!Y || !B || !R || !X || !Yio || !work || !L || !nonfinite || !ms4 || reps < 1)
+    return fail(KB_ERR_ARGUMENT, "bad kb_time_passes arguments");
+  Work w = layout(op, work);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<double> host(2 * (size_t)op->batch);
+  for (int b = 0; b < op->batch; ++b) {
+    host[b] = L[b];
+    host[op->batch + b] = L[b] + lam * lam;
+  }
+  KB_CUDA(cudaMemcpyAsync(w.scal, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (op->dtype == KB_F64)
+    return time_passes_t<double>(op, static_cast<const double*>(Y), static_cast<const double*>(B), static_cast<double*>(R), static_cast<double*>(X), static_cast<double*>(Yio), w, reps, ms4, nonfinite, s);
+  return time_passes_t<float>(op, static_cast<const float*>(Y), static_cast<const float*>(B), static_cast<float*>(R), static_cast<float*>(X), static_cast<float*>(Yio), w, reps, ms4, nonfinite, s);
+}
+
+}  // extern "C"

@@ -1,0 +1,360 @@
+"""sFISTA on the B200 behind the reference solver API (kronblur solvers.py).
+
+``sfista(op, B, cfg, X0=None, truth=None, exact_apply=None)`` keeps the reference signature and
+``SolveRun`` result (solvers.py:215-228). Its loop is the reference ``_engine`` (solvers.py:153-199)
+executed by the native runner ``kb_sfista_run``: per iteration one fused forward kernel pair
+(R = A y - B) and one fused adjoint+update pair (x = (L y - A^T R)/(L + lam^2), optional x >= 0
+projection, y = x + beta_k (x - x_prev)). The momentum coefficients beta_k are data independent and
+come from ``momentum_next`` on the host, bit-identical to the reference recurrence.
+
+Extensions (keyword-only, so the reference signature is unchanged): ``options=SolveOptions(...)``
+selects the compute dtype (float64 / float32), the x >= 0 projection that BASELINE's configs ask
+for (the reference has none), and CUDA-graph use.
+
+Semantics kept from the reference:
+  * X0 shape mismatch -> ArgumentError (:155-157); y_1 = X0, t_1 = 1 (:160-161)
+  * non-finite x_k -> NumericError("non-finite iterate at iteration k") (:175-176)
+  * record_history: IterationRecord(k, t_k, Phi_s(x_k), eta, gamma, cumulative ms) (:180-192);
+    record_iterates: a copy of every x_k (:193-194); rel_tol early stop (:197-198)
+  * solve_ms covers only the iteration bodies (:169-174), here timed with CUDA events.
+"""
+
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import ArgumentError, NumericError
+
+LIPSCHITZ_SAFETY = 1.05  # solvers.py:43
+
+
+@dataclass(frozen=True)
+class SolveConfig:
+    """Solver parameters (solvers.py:53-72)."""
+
+    lam: float
+    lipschitz: float
+    max_iter: int = 50
+    rel_tol: float = 0.0
+    record_history: bool = True
+    record_iterates: bool = False
+
+    def __post_init__(self):
+        if not (np.isfinite(self.lam) and self.lam > 0):
+            raise ArgumentError(f"lambda must be positive, got {self.lam}")
+        if not (np.isfinite(self.lipschitz) and self.lipschitz > 0):
+            raise ArgumentError(f"Lipschitz constant must be positive, got {self.lipschitz}")
+        if self.max_iter < 1:
+            raise ArgumentError(f"max_iter must be >= 1, got {self.max_iter}")
+        if self.rel_tol < 0:
+            raise ArgumentError(f"rel_tol must be >= 0, got {self.rel_tol}")
+
+
+@dataclass(frozen=True)
+class IterationRecord:
+    k: int
+    t: float
+    objective: float
+    eta: float | None
+    gamma: float | None
+    ms: float
+
+
+@dataclass
+class SolveRun:
+    x: np.ndarray
+    iterations: int
+    solve_ms: float
+    history: list = field(default_factory=list)
+    iterates: list = field(default_factory=list)
+
+
+@dataclass(frozen=True)
+class SolveOptions:
+    """B200-specific knobs (not part of the reference signature)."""
+
+    dtype: str = "float64"     # compute dtype of the device planes
+    project: bool = False      # x >= 0 after the update (BASELINE configs); reference has none
+    use_graph: bool | None = None  # None: graph when the fast path runs >= 8 iterations
+
+
+def momentum_next(t: float) -> float:
+    """t_{k+1} = (1 + sqrt(1 + 4 t^2)) / 2 (solvers.py:96-101)."""
+    t = float(t)
+    if not (np.isfinite(t) and t >= 1.0):
+        raise ArgumentError(f"momentum parameter must be >= 1, got {t}")
+    return (1.0 + np.sqrt(1.0 + 4.0 * t * t)) / 2.0
+
+
+def momentum_table(iters: int) -> tuple[np.ndarray, np.ndarray]:
+    """(t_k for k=1..iters, beta_k = (t_k - 1)/t_{k+1}) exactly as _engine evaluates them."""
+    ts = np.empty(iters)
+    beta = np.empty(iters)
+    t = 1.0
+    for k in range(iters):
+        tn = momentum_next(t)
+        ts[k] = t
+        beta[k] = (t - 1.0) / tn
+        t = tn
+    return ts, beta
+
+
+def objective(apply, x, b, lam: float) -> float:
+    """Phi(x) = 1/2 ||A x - b||^2 + lam^2/2 ||x||^2 over raveled arrays (solvers.py:133-141)."""
+    r = np.asarray(apply(x) - b)
+    x = np.asarray(x)
+    return 0.5 * float(np.dot(r.ravel(), r.ravel())) + 0.5 * lam**2 * float(np.dot(x.ravel(), x.ravel()))
+
+
+def objective_matrix(op, X, B, lam: float) -> float:
+    """Phi_s(X) with the GPU forward operator (solvers.py:144-146)."""
+    from .kron import kron_apply
+
+    return objective(lambda Z: kron_apply(op, Z), X, B, lam)
+
+
+def _norm(a) -> float:
+    return float(np.linalg.norm(np.asarray(a).ravel()))
+
+
+# --------------------------------------------------------------------------------------------
+# Lipschitz constant
+# --------------------------------------------------------------------------------------------
+def _start_vector(seed: int, m: int, n: int, form: str) -> np.ndarray:
+    from .rand import stream
+
+    if form == "vector":  # restore(): dims = m*n, F-order un-vec (pipeline.py:117-122,169-171)
+        v = stream(seed, "lipschitz").standard_normal((m * n,))
+        nv = np.linalg.norm(v.ravel())
+        if nv == 0:  # pragma: no cover
+            v = np.ones(m * n)
+            nv = np.linalg.norm(v)
+        v = v / nv
+        return v.reshape((m, n), order="F")
+    v = stream(seed, "lipschitz").standard_normal((m, n))
+    nv = np.linalg.norm(v.ravel())
+    if nv == 0:  # pragma: no cover
+        v = np.ones((m, n))
+        nv = np.linalg.norm(v.ravel())
+    return v / nv
+
+
+def _finish_power(hist: np.ndarray) -> float:
+    """Apply solvers.py:123-130 to the device history [iters][2] of (rho, ||w||^2)."""
+    rho = 0.0
+    for k in range(hist.shape[0]):
+        rho = float(hist[k, 0])
+        nw2 = float(hist[k, 1])
+        if nw2 == 0 or rho <= 0 or not np.isfinite(rho):
+            warnings.warn("operator is numerically zero; Lipschitz floor returned")
+            return float(np.finfo(float).eps)
+    return LIPSCHITZ_SAFETY * rho
+
+
+def lipschitz(op, iters: int = 50, seed: int = 0, form: str = "matrix", dtype: str = "float64") -> float:
+    """estimate_lipschitz on the GPU for a KronOperator: same start vector, iteration count and
+    stopping rules as solvers.py:104-130 (matrix form: dims=(m,n); vector form: dims=m*n)."""
+    import torch
+
+    from .device import device_operator
+
+    iters = int(iters)
+    if iters < 1:
+        raise ArgumentError(f"iters must be >= 1, got {iters}")
+    m, n = op.shape
+    dev = device_operator(op, dtype)
+    v0 = _start_vector(seed, m, n, form)
+    v = torch.from_numpy(np.ascontiguousarray(v0)).to(dev.device, dev.tdtype)
+    hist = dev.power_iter(v, iters)
+    return _finish_power(hist[:, :, 0].cpu().numpy())
+
+
+def make_ops(op, form: str = "matrix", dtype: str = "float64"):
+    """(apply, apply_adjoint) closures on the GPU operator, tagged so that ``estimate_lipschitz``
+    runs the fused device power iteration instead of a host loop."""
+    from .kron import kron_apply, kron_apply_adjoint
+    from .psf import unvec, vec
+
+    m, n = op.shape
+    if form == "vector":
+        def apply(v):
+            return vec(kron_apply(op, unvec(v, m, n), dtype=dtype))
+
+        def adjoint(v):
+            return vec(kron_apply_adjoint(op, unvec(v, m, n), dtype=dtype))
+    else:
+        def apply(X):
+            return kron_apply(op, X, dtype=dtype)
+
+        def adjoint(X):
+            return kron_apply_adjoint(op, X, dtype=dtype)
+    apply._kb_power = adjoint._kb_power = (op, form, dtype)
+    return apply, adjoint
+
+
+def estimate_lipschitz(apply, apply_adjoint, dims, iters: int = 50, seed: int = 0) -> float:
+    """lambda_max(A^T A) by power iteration, times 1.05 (solvers.py:104-130).
+
+    Closures from ``make_ops`` run on the device (kb_power_iter). Arbitrary host callables keep
+    the reference's generic loop — the operator is then whatever the caller computes.
+    """
+    tag = getattr(apply, "_kb_power", None)
+    if tag is not None and getattr(apply_adjoint, "_kb_power", None) is tag:
+        op, form, dtype = tag
+        want = op.shape[0] * op.shape[1] if form == "vector" else tuple(op.shape)
+        got = int(dims) if np.isscalar(dims) else tuple(int(d) for d in dims)
+        if got != want:
+            raise ArgumentError(f"dims {dims} do not match the operator ({want})")
+        return lipschitz(op, iters=iters, seed=seed, form=form, dtype=dtype)
+    from .rand import stream
+
+    iters = int(iters)
+    if iters < 1:
+        raise ArgumentError(f"iters must be >= 1, got {iters}")
+    shape = (dims,) if np.isscalar(dims) else tuple(dims)
+    v = stream(seed, "lipschitz").standard_normal(shape)
+    nv = np.linalg.norm(v.ravel())
+    if nv == 0:  # pragma: no cover
+        v = np.ones(shape)
+        nv = np.linalg.norm(v.ravel())
+    v /= nv
+    rho = 0.0
+    for _ in range(iters):
+        w = apply_adjoint(apply(v))
+        rho = float(np.vdot(v.ravel(), w.ravel()))
+        nw = np.linalg.norm(w.ravel())
+        if nw == 0 or rho <= 0:
+            warnings.warn("operator is numerically zero; Lipschitz floor returned")
+            return float(np.finfo(float).eps)
+        v = w / nw
+    return LIPSCHITZ_SAFETY * rho
+
+
+# --------------------------------------------------------------------------------------------
+# sFISTA
+# --------------------------------------------------------------------------------------------
+def _host(t) -> np.ndarray:
+    import torch
+
+    return t.to("cpu", torch.float64).numpy().copy()
+
+
+def sfista(op, B, cfg: SolveConfig, X0=None, truth=None, exact_apply=None, *,
+           options: SolveOptions | None = None) -> SolveRun:
+    """Accelerated solve of the matrix model against a KronOperator, on the B200."""
+    import torch
+
+    from .device import INT_MAX, device_operator
+
+    opts = options or SolveOptions()
+    B = np.asarray(B, dtype=float)
+    if X0 is None:
+        X0 = np.zeros_like(B)
+    X0 = np.array(X0, dtype=float)
+    if X0.shape != B.shape:
+        raise ArgumentError(f"x0 shape {X0.shape} does not match data shape {B.shape}")
+    if B.shape != tuple(op.shape):
+        raise ArgumentError(f"image shape {B.shape} does not match operator shape {tuple(op.shape)}")
+    K = int(cfg.max_iter)
+    L, lam = float(cfg.lipschitz), float(cfg.lam)
+    ts, beta = momentum_table(K)
+    dev = device_operator(op, opts.dtype)
+    fast = not cfg.record_history and not cfg.record_iterates and cfg.rel_tol == 0
+    use_graph = opts.use_graph if opts.use_graph is not None else (fast and K >= 8)
+
+    with dev.lock:
+        stream = torch.cuda.current_stream()
+        hB, hX = dev.staging("host_b", pinned=True), dev.staging("host_x", pinned=True)
+        Bd, Xd, Yd = dev.staging("b"), dev.staging("x"), dev.staging("y")
+        hB.numpy()[...] = B
+        hX.numpy()[...] = X0
+        Bd.copy_(hB, non_blocking=True)
+        Xd.copy_(hX, non_blocking=True)
+        Yd.copy_(Xd)
+        flag = torch.full((1,), INT_MAX, dtype=torch.int32, device=dev.device)
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+        if fast:
+            start.record(stream)
+            dev.sfista_run(Bd, Xd, Yd, beta, 0, K, L, lam, opts.project, flag, use_graph=use_graph)
+            stop.record(stream)
+            hX.copy_(Xd, non_blocking=True)
+            stop.synchronize()
+            torch.cuda.current_stream().synchronize()
+            bad = int(flag.item())
+            if bad <= K:
+                raise NumericError(f"non-finite iterate at iteration {bad}")
+            x = hX.numpy().astype(np.float64, copy=True)
+            return SolveRun(x=x, iterations=K, solve_ms=float(start.elapsed_time(stop)))
+
+        norm_b = _norm(B)
+        norm_truth = _norm(truth) if truth is not None else 0.0
+        norms = torch.zeros((1, 4, 1), dtype=torch.float64, device=dev.device)
+        history, iterates = [], []
+        elapsed = 0.0
+        iterations = 0
+        for k in range(1, K + 1):
+            start.record(stream)
+            dev.sfista_run(Bd, Xd, Yd, beta, k - 1, 1, L, lam, opts.project, flag, norms=norms,
+                           use_graph=False)
+            stop.record(stream)
+            stop.synchronize()
+            elapsed += float(start.elapsed_time(stop))
+            if int(flag.item()) <= k:
+                raise NumericError(f"non-finite iterate at iteration {k}")
+            iterations = k
+            nr = norms[0, :, 0].cpu().numpy()
+            step, base = float(np.sqrt(nr[0])), float(np.sqrt(nr[1]))
+            if cfg.record_history or cfg.record_iterates:
+                x = _host(Xd)
+            if cfg.record_history:
+                Ax = _host(dev.apply(Xd))
+                eta = _norm(x - truth) / norm_truth if truth is not None and norm_truth > 0 else None
+                gamma = (_norm(exact_apply(x) - B) / norm_b
+                         if exact_apply is not None and norm_b > 0 else None)
+                r = Ax - B
+                phi = 0.5 * float(np.dot(r.ravel(), r.ravel())) + 0.5 * lam**2 * float(np.dot(x.ravel(), x.ravel()))
+                history.append(IterationRecord(k=k, t=float(ts[k - 1]), objective=phi, eta=eta,
+                                               gamma=gamma, ms=elapsed))
+            if cfg.record_iterates:
+                iterates.append(x.copy())
+            if cfg.rel_tol > 0 and step < cfg.rel_tol * (base if base > 0 else 1.0):
+                break
+        return SolveRun(x=_host(Xd), iterations=iterations, solve_ms=elapsed, history=history,
+                        iterates=iterates)
+
+
+def sfista_batch(ops, B, lipschitz, lam: float, iters: int, *, options: SolveOptions | None = None,
+                 X0=None):
+    """Batch of independent solves (BASELINE cfg3): one batched operator, per-image L, shared lam
+    and momentum. B: (batch, m, n) numpy or CUDA tensor. Returns (x, solve_ms) with x like B."""
+    import torch
+
+    from .device import INT_MAX, DeviceOperator
+
+    opts = options or SolveOptions()
+    dev = ops if isinstance(ops, DeviceOperator) else DeviceOperator(list(ops), opts.dtype)
+    _, beta = momentum_table(int(iters))
+    on_device = isinstance(B, torch.Tensor) and B.is_cuda
+    Bd = B.to(dev.tdtype).contiguous() if on_device else torch.from_numpy(np.ascontiguousarray(B)).to(dev.device, dev.tdtype)
+    if X0 is None:
+        Xd = torch.zeros_like(Bd)
+    else:
+        Xd = (X0 if isinstance(X0, torch.Tensor) else torch.from_numpy(np.asarray(X0))).to(dev.device, dev.tdtype).contiguous()
+    Yd = Xd.clone()
+    flag = torch.full((1,), INT_MAX, dtype=torch.int32, device=dev.device)
+    stream = torch.cuda.current_stream()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    dev.sfista_run(Bd, Xd, Yd, beta, 0, int(iters), lipschitz, lam, opts.project, flag,
+                   use_graph=bool(opts.use_graph))
+    stop.record(stream)
+    stop.synchronize()
+    bad = int(flag.item())
+    if bad <= iters:
+        raise NumericError(f"non-finite iterate at iteration {bad}")
+    x = Xd if on_device else _host(Xd)
+    return x, float(start.elapsed_time(stop))
