@@ -258,8 +258,9 @@ int stage_a(const kb_op* op, int adjoint, const T* in, const Work& w, const RowB
   KB_TRY(launch_a<T>(op, in, z, static_cast<const T*>(adjoint ? op->ta_corr : op->ta_conv), ga, nw2, s));
   if (adjoint && op->bc_a == KB_BC_REFLECTIVE && op->Ha > 0) {
     const long long z_ps = (long long)op->m * op->n;
-    dim3 grid((op->n + 127) / 128, 2 * op->Ha, op->batch);
-    kb::kb_fold_rows<T><<<grid, 128, 0, s>>>(in, z_ps, z, z_ps, z_ps * op->r, op->r,
+    dim3 grid((op->n + 127) / 128, 2 * op->Ha * op->r, op->batch);
+    constexpr int NU = sizeof(T) == 8 ? 32 : 64;
+    kb::kb_fold_rows<T, NU><<<grid, 128, 0, s>>>(in, z_ps, z, z_ps, z_ps * op->r, op->r,
                                               static_cast<const T*>(op->ta_conv),
                                               (long long)op->r * op->Wpa, ga);
     KB_CUDA(cudaGetLastError());
@@ -273,14 +274,13 @@ int stage_b(const kb_op* op, int adjoint, kb::Epi<T> e, const Work& w, cudaStrea
   const kb::AxisGeom gb = geom_b(op, adjoint);
   if (adjoint && op->bc_b == KB_BC_REFLECTIVE && op->Hb > 0) {
     const int slots = 2 * op->Hb;
-    const int bx = (slots + 31) / 32 * 32;
-    const int by = std::max(1, 256 / bx);
-    dim3 grid((op->m + by - 1) / by, 1, op->batch);
+    const int bx = std::min(128, (slots + 31) / 32 * 32);
+    constexpr int NU = sizeof(T) == 8 ? 32 : 64;
+    dim3 grid((slots + bx - 1) / bx, op->m, op->batch);
     const long long z_ps = (long long)op->m * op->n;
-    kb::kb_fold_cols<T><<<grid, dim3(bx, by), 0, s>>>(z, z_ps, z_ps * op->r, op->r,
-                                                       static_cast<const T*>(op->tb_conv),
-                                                       (long long)op->r * op->Wpb, gb,
-                                                       static_cast<T*>(w.fold));
+    kb::kb_fold_cols<T, NU><<<grid, bx, 0, s>>>(z, z_ps, z_ps * op->r, op->r,
+                                            static_cast<const T*>(op->tb_conv),
+                                            (long long)op->r * op->Wpb, gb, static_cast<T*>(w.fold));
     KB_CUDA(cudaGetLastError());
     e.fold = static_cast<const T*>(w.fold);
     e.foldH = op->Hb;

@@ -139,20 +139,22 @@ kb_pass_a(const T* __restrict__ in, long long in_bs, T* __restrict__ z, long lon
   in += b * in_bs;
   z += b * z_bs;
   tin += b * t_bs;
-  const bool scaled = (nw2 != nullptr);
-  const double nrm = scaled ? sqrt(nw2[b]) : 1.0;
-
+  // Tile fill: rows [p0-H, p0+TP+Wp-1-H) of the input (folded for the reflective forward),
+  // one warp per row, 8-byte cp.async per lane so every row load is in flight at once.
   for (int rr = warp; rr < rows_tile; rr += kNW) {
     int gr = g.g0 + p0 - g.H + rr;
     if (g.fill && (gr < 0 || gr >= g.Mg)) gr = kb_fold(gr, g.Mg);
     const int lr = gr - g.g0;
-    T v = T(0);
-    if (q < ncol && gr >= 0 && gr < g.Mg && lr >= -g.halo_lo && lr < g.len + g.halo_hi) {
-      v = in[(long long)lr * ncol + q];
-      if (scaled) v = (T)((double)v / nrm);
-    }
-    xs[rr * 32 + lane] = v;
+    T* d = xs + rr * 32 + lane;
+    if (q < ncol && gr >= 0 && gr < g.Mg && lr >= -g.halo_lo && lr < g.len + g.halo_hi)
+      cp_async_elem<T>(d, in + (long long)lr * ncol + q);
+    else
+      *d = T(0);
   }
+  cp_async_commit();
+  // power iteration: the pass is linear, so v = w/||w|| is applied to the outputs
+  const T oscale = nw2 ? (T)(1.0 / sqrt(nw2[b])) : T(1);
+  cp_async_wait<0>();
 
   const int s_off = warp * R;
   for (int gb = 0; gb < r; gb += G) {
@@ -193,7 +195,7 @@ kb_pass_a(const T* __restrict__ in, long long in_bs, T* __restrict__ z, long lon
 #pragma unroll
           for (int j = 0; j < R; ++j) {
             const int lr = p0 + s_off + j;
-            if (lr < g.len) zp[(long long)lr * ncol + q] = acc[gg][j];
+            if (lr < g.len) zp[(long long)lr * ncol + q] = nw2 ? acc[gg][j] * oscale : acc[gg][j];
           }
         }
       }
@@ -202,73 +204,85 @@ kb_pass_a(const T* __restrict__ in, long long in_bs, T* __restrict__ z, long lon
 }
 
 // ------------------------------------------------------------------------------------------
-// Adjoint fold along axis 0: for output rows within H of a global domain edge, add the
-// folded-source part sum_{t out of domain} c_{s-t} R[refl(t)] (conv table) to every Z_i.
-// One thread per (edge row slot, column): slot < H is row slot, slot >= H is row Mg-2H+slot.
+// Adjoint fold corrections. For an output index s within H of a reflective domain edge, the
+// transpose adds the folded-source part  sum_{t out of domain} c_{s-t} x[refl(t)]  (conv table,
+// k = t-s+H). With u = refl(t) this is a short Hankel-type sum over the edge samples:
+//   left/top edge   u in [0, min(H-s, M)),   k = H-s-1-u
+//   right/bottom    t in [max(M, s-H), s+H], u = 2M-1-t, k = t-s+H
+// kb_fold_sum loads every edge sample first (all loads in flight), then accumulates.
 // ------------------------------------------------------------------------------------------
-template <typename T>
-__global__ void kb_fold_rows(const T* __restrict__ in, long long in_bs, T* __restrict__ z,
-                             long long z_ps, long long z_bs, int r, const T* __restrict__ tconv,
-                             long long t_bs, AxisGeom g) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  const int slot = blockIdx.y;  // 0..2H-1
-  const int b = blockIdx.z;
-  if (q >= g.other) return;
-  const int s = slot < g.H ? slot : g.Mg - 2 * g.H + slot;  // global output row
-  if (s < 0 || s >= g.Mg) return;
-  if (slot >= g.H && s < g.H) return;  // already covered by a top slot (tiny domains)
-  const int ls = s - g.g0;
-  if (ls < 0 || ls >= g.len) return;   // not on this row block
-  in += b * in_bs;
-  z += b * z_bs;
-  tconv += b * t_bs;
-  for (int i = 0; i < r; ++i) {
-    const T* tc = tconv + (long long)i * g.Wp;
-    T acc = T(0);
-    for (int t = s - g.H; t < 0; ++t) {  // top fold: row u = -1-t
-      const int u = -1 - t;
-      if (u < g.Mg) acc = kb_fma(tc[t - s + g.H], in[(long long)(u - g.g0) * g.other + q], acc);
+template <typename T, int NU>
+__device__ __forceinline__ T kb_fold_sum(const T* __restrict__ tc, const T* __restrict__ src,
+                                         long long stride, int s, int H, int M) {
+  T acc = T(0);
+  const int top = min(H - s, M);
+  const int t0 = max(M, s - H), nb = s + H - t0 + 1;  // bottom sources t0 .. s+H
+  if (top <= NU && nb <= NU) {
+    T v[NU];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) v[u] = (u < top) ? src[(long long)u * stride] : T(0);
+#pragma unroll
+    for (int u = 0; u < NU; ++u)
+      if (u < top) acc = kb_fma(tc[H - s - 1 - u], v[u], acc);
+#pragma unroll
+    for (int d = 0; d < NU; ++d) {
+      const int u = 2 * M - 1 - (t0 + d);
+      v[d] = (d < nb && u >= 0) ? src[(long long)u * stride] : T(0);
     }
-    for (int t = max(g.Mg, s - g.H); t <= s + g.H; ++t) {  // bottom fold: row u = 2Mg-1-t
-      const int u = 2 * g.Mg - 1 - t;
-      if (u >= 0) acc = kb_fma(tc[t - s + g.H], in[(long long)(u - g.g0) * g.other + q], acc);
-    }
-    T* zp = z + (long long)i * z_ps + (long long)ls * g.other + q;
-    *zp = *zp + acc;
+#pragma unroll
+    for (int d = 0; d < NU; ++d)
+      if (d < nb) acc = kb_fma(tc[t0 + d - s + H], v[d], acc);
+    return acc;
   }
+  for (int u = 0; u < top; ++u) acc = kb_fma(tc[H - s - 1 - u], src[(long long)u * stride], acc);
+  for (int t = t0; t <= s + H; ++t) {
+    const int u = 2 * M - 1 - t;
+    if (u >= 0) acc = kb_fma(tc[t - s + H], src[(long long)u * stride], acc);
+  }
+  return acc;
 }
 
-// ------------------------------------------------------------------------------------------
-// Adjoint fold along axis 1: edge corrections for output columns within H of the left / right
-// edge, summed over all terms, into fold[b][p][slot] (slot < H: column slot; slot >= H: column
-// n-2H+slot). Added by pass B's epilogue.
-// ------------------------------------------------------------------------------------------
-template <typename T>
-__global__ void kb_fold_cols(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
-                             const T* __restrict__ tconv, long long t_bs, AxisGeom g,
-                             T* __restrict__ fold) {
-  const int slot = threadIdx.x;          // 0..2H-1 (blockDim.x >= 2H)
-  const int p = blockIdx.x * blockDim.y + threadIdx.y;
+// axis 0: Z_i[s][q] += fold(R[:, q]) for edge rows s. One thread per (edge-row slot, column,
+// term); slot < H is row `slot`, slot >= H is row Mg-2H+slot.
+template <typename T, int NU>
+__global__ void __launch_bounds__(128)
+kb_fold_rows(const T* __restrict__ in, long long in_bs, T* __restrict__ z, long long z_ps,
+             long long z_bs, int r, const T* __restrict__ tconv, long long t_bs, AxisGeom g) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const int slot = blockIdx.y % (2 * g.H);
+  const int i = blockIdx.y / (2 * g.H);
+  const int b = blockIdx.z;
+  if (q >= g.other || i >= r) return;
+  const int H = g.H, M = g.Mg;
+  const int s = slot < H ? slot : M - 2 * H + slot;  // global output row
+  if (s < 0 || s >= M || (slot >= H && s < H)) return;
+  const int ls = s - g.g0;
+  if (ls < 0 || ls >= g.len) return;  // not on this row block
+  const T* tc = tconv + b * t_bs + (long long)i * g.Wp;
+  const T* src = in + b * in_bs + q - (long long)g.g0 * g.other;  // src[u*other] = global row u
+  const T acc = kb_fold_sum<T, NU>(tc, src, g.other, s, H, M);
+  T* zp = z + b * z_bs + (long long)i * z_ps + (long long)ls * g.other + q;
+  *zp = *zp + acc;
+}
+
+// axis 1: fold[b][p][slot] = sum_i fold(Z_i[p, :]) for edge columns (slot < H: column slot;
+// slot >= H: column n-2H+slot); pass B's epilogue adds them. One thread per (row, slot).
+template <typename T, int NU>
+__global__ void __launch_bounds__(128)
+kb_fold_cols(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
+             const T* __restrict__ tconv, long long t_bs, AxisGeom g, T* __restrict__ fold) {
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  const int p = blockIdx.y;
   const int b = blockIdx.z;
   const int n = g.len, H = g.H;
-  if (p >= g.other || slot >= 2 * H) return;
+  if (slot >= 2 * H) return;
   const int s = slot < H ? slot : n - 2 * H + slot;
   T acc = T(0);
   if (s >= 0 && s < n && !(slot >= H && s < H)) {
-    z += b * z_bs + (long long)p * n;
-    tconv += b * t_bs;
-    for (int i = 0; i < r; ++i) {
-      const T* zr = z + (long long)i * z_ps;
-      const T* tc = tconv + (long long)i * g.Wp;
-      for (int t = s - H; t < 0; ++t) {
-        const int u = -1 - t;
-        if (u < n) acc = kb_fma(tc[t - s + H], zr[u], acc);
-      }
-      for (int t = max(n, s - H); t <= s + H; ++t) {
-        const int u = 2 * n - 1 - t;
-        if (u >= 0) acc = kb_fma(tc[t - s + H], zr[u], acc);
-      }
-    }
+    const T* zr = z + b * z_bs + (long long)p * n;
+    const T* tcb = tconv + b * t_bs;
+    for (int i = 0; i < r; ++i)
+      acc += kb_fold_sum<T, NU>(tcb + (long long)i * g.Wp, zr + (long long)i * z_ps, 1, s, H, n);
   }
   fold[((long long)b * g.other + p) * (2 * H) + slot] = acc;
 }
@@ -320,18 +334,21 @@ kb_pass_b(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
   z += b * z_bs;
   tin += b * t_bs;
 
+  // Column sources of the tile (folded for the reflective forward), identical for every row:
+  // computed once per thread for the columns it copies.
   auto load_term = [&](int i, int stage) {
     const T* zp = z + (long long)i * z_ps;
     T* dst = zs + stage * 32 * S;
-    const int total = 32 * cols_tile;
-    for (int idx = tid; idx < total; idx += 32 * kNW) {
-      const int rr = idx / cols_tile, cc = idx - rr * cols_tile;
-      int gq = q0 - g.H + cc;
-      if (g.fill && (gq < 0 || gq >= g.len)) gq = kb_fold(gq, g.len);
+    for (int rr = warp; rr < 32; rr += kNW) {
       const int gp = prow0 + rr;
-      T* d = dst + rr * S + cc;
-      if (gp < nrow && gq >= 0 && gq < g.len) cp_async_elem<T>(d, zp + (long long)gp * g.len + gq);
-      else *d = T(0);
+      const T* src = zp + (long long)gp * g.len;
+      T* drow = dst + rr * S;
+      for (int cc = lane; cc < cols_tile; cc += 32) {
+        int gq = q0 - g.H + cc;
+        if (g.fill && (gq < 0 || gq >= g.len)) gq = kb_fold(gq, g.len);
+        if (gp < nrow && gq >= 0 && gq < g.len) cp_async_elem<T>(drow + cc, src + gq);
+        else drow[cc] = T(0);
+      }
     }
     for (int k = tid; k < g.Wp; k += 32 * kNW) cin[stage * g.Wp + k] = tin[(long long)i * g.Wp + k];
     cp_async_commit();
@@ -385,15 +402,21 @@ kb_pass_b(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
     }
   }
   if constexpr (MODE == EPI_PLAIN || MODE == EPI_RESID) {
+    if constexpr (MODE == EPI_RESID) {
+      T bv[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const int qq = s_first + j;
+        bv[j] = (prow_ok && qq < g.len) ? e.bsub[base + qq] : T(0);
+      }
+#pragma unroll
+      for (int j = 0; j < R; ++j) acc[j] = rn_sub<T>(acc[j], bv[j]);
+    }
     if (prow_ok) {
 #pragma unroll
       for (int j = 0; j < R; ++j) {
         const int qq = s_first + j;
-        if (qq < g.len) {
-          T v = acc[j];
-          if constexpr (MODE == EPI_RESID) v = rn_sub<T>(v, e.bsub[base + qq]);
-          e.out[base + qq] = v;
-        }
+        if (qq < g.len) e.out[base + qq] = acc[j];
       }
     }
   } else if constexpr (MODE == EPI_UPDATE) {
@@ -402,13 +425,21 @@ kb_pass_b(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
     const T bt = (T)e.beta;
     bool bad = false;
     double nrm[3] = {0.0, 0.0, 0.0};
+    T yv_[R], xp_[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {  // issue every operand load before the first use
+      const int qq = s_first + j;
+      const bool ok = prow_ok && qq < g.len;
+      yv_[j] = ok ? e.y[base + qq] : T(0);
+      xp_[j] = ok ? e.x[base + qq] : T(0);
+    }
     if (prow_ok) {
 #pragma unroll
       for (int j = 0; j < R; ++j) {
         const int qq = s_first + j;
         if (qq < g.len) {
-          const T yv = e.y[base + qq];
-          const T xp = e.x[base + qq];
+          const T yv = yv_[j];
+          const T xp = xp_[j];
           T xv = rn_div<T>(rn_sub<T>(rn_mul<T>(Lt, yv), acc[j]), dt);
           if (e.project) xv = (xv > T(0) || xv != xv) ? xv : T(0);
           const T d = rn_sub<T>(xv, xp);
