@@ -53,6 +53,13 @@ int kb_op_create(kb_op** out, int dtype, int m, int n, int r, int batch, int bc_
                  int a_dlo, int a_w, const double* a_taps, int b_dlo, int b_w,
                  const double* b_taps);
 int kb_op_destroy(kb_op* op);
+/*
+ * Layout facts of an operator, info[0..n): {Ha, Wpa, Hb, Wpb, sym_a, sym_b, adjoint pass-A groups,
+ * max group}. sym_* = 1 when every generator on that reflective axis is symmetric or
+ * antisymmetric to 1e-11 relative, so the adjoint folds through sign-reflected tile fills
+ * instead of the exact fold kernels (set KB_EXACT_FOLD=1 to force the exact path).
+ */
+int kb_op_info(const kb_op* op, int* info, int n);
 /* Device workspace (bytes) the calls below need for this operator. */
 size_t kb_workspace_bytes(const kb_op* op);
 

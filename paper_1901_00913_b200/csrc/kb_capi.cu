@@ -9,6 +9,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -41,6 +42,9 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 constexpr int kMaxHalf = 1024;
+constexpr int kGmaxF64 = 4;  // pass A term group (register budget: G*R accumulators)
+constexpr int kGmaxF32 = 8;
+constexpr double kSymTol = 1e-11;  // (anti)symmetry residual allowed for sign-reflected fills
 constexpr int kRA = 8;   // pass A rows per warp
 constexpr int kRB = 16;  // pass B columns per warp
 
@@ -57,7 +61,10 @@ struct GraphCache {
 struct kb_op {
   int dtype, m, n, r, batch, bc_a, bc_b;
   int Ha, Wpa, Hb, Wpb;
-  int G;
+  int gmax;                  // largest term group of pass A
+  int sym_a = 0, sym_b = 0;  // adjoint uses sign-reflected tile fills (no fold kernels)
+  kb::Groups grp_fwd, grp_adj;
+  void* sign_b = nullptr;    // [batch][r] +-1 fill sign of each term on axis 1 (sym_b only)
   void* ta_conv = nullptr;  // [batch][r][Wpa] taps c_{H-k}
   void* ta_corr = nullptr;  // [batch][r][Wpa] taps c_{k-H}
   void* tb_conv = nullptr;
@@ -104,20 +111,18 @@ Work layout(const kb_op* op, void* base) {
   return w;
 }
 
-int pick_group(int r, int gmax) {
-  int best = 1;
-  long best_cost = LONG_MAX;
-  static const int cands[] = {8, 6, 5, 4, 3, 2, 1};
-  for (int G : cands) {
-    if (G > gmax) continue;
-    const long groups = (r + G - 1) / G;
-    const long cost = groups * (G + 2);  // padded term work + per-group tile re-read
-    if (cost < best_cost) {
-      best_cost = cost;
-      best = G;
-    }
+// Split `count` terms starting at `start` into near-equal groups of at most gmax, all with
+// the given tile-fill sign.
+void add_groups(kb::Groups& g, int start, int count, int gmax, int sign) {
+  if (count <= 0) return;
+  const int ng = (count + gmax - 1) / gmax;
+  for (int k = 0; k < ng; ++k) {
+    const int lo = start + (int)((long)count * k / ng), hi = start + (int)((long)count * (k + 1) / ng);
+    g.start[g.n] = lo;
+    g.count[g.n] = hi - lo;
+    g.sign[g.n] = sign;
+    ++g.n;
   }
-  return best;
 }
 
 // Opt a kernel into the full 227 KB of shared memory (minus its static shared memory). Keyed by
@@ -146,50 +151,36 @@ int allow_smem(K kernel, size_t dyn_bytes) {
   return KB_OK;
 }
 
-template <typename T, int G>
-int launch_a_g(const T* in, long long in_bs, T* z, long long z_ps, long long z_bs, int r,
-               const T* tin, long long t_bs, const kb::AxisGeom& g, const double* nw2, int batch,
-               cudaStream_t s) {
+template <typename T, int GMAX>
+int launch_a_g(const T* in, long long in_bs, T* z, long long z_ps, long long z_bs,
+               const T* tin, long long t_bs, const kb::AxisGeom& g, const kb::Groups& grp,
+               const double* nw2, int batch, cudaStream_t s) {
   constexpr int TP = kb::kNW * kRA;
-  const size_t smem = sizeof(T) * ((size_t)(TP + g.Wp - 1) * 32 + (size_t)G * g.Wp);
-  auto kern = kb::kb_pass_a<T, G, kRA>;
+  const size_t smem = sizeof(T) * ((size_t)(TP + g.Wp - 1) * 32 + (size_t)GMAX * g.Wp);
+  auto kern = kb::kb_pass_a<T, GMAX, kRA>;
   KB_TRY(allow_smem(kern, smem));
   dim3 grid((g.other + 31) / 32, (g.len + TP - 1) / TP, batch);
   dim3 block(32, kb::kNW);
-  kern<<<grid, block, smem, s>>>(in, in_bs, z, z_ps, z_bs, r, tin, t_bs, g, nw2);
+  kern<<<grid, block, smem, s>>>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2);
   KB_CUDA(cudaGetLastError());
   return KB_OK;
 }
 
 template <typename T>
 int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeom& g,
-             const double* nw2, cudaStream_t s) {
+             const kb::Groups& grp, const double* nw2, cudaStream_t s) {
   const long long in_bs = (long long)plane_elems(op);
   const long long z_ps = (long long)g.len * g.other;
   const long long z_bs = z_ps * op->r;
   const long long t_bs = (long long)op->r * g.Wp;
-#define KB_A(GG) return launch_a_g<T, GG>(in, in_bs, z, z_ps, z_bs, op->r, tin, t_bs, g, nw2, op->batch, s)
-  switch (op->G) {
-    case 1: KB_A(1);
-    case 2: KB_A(2);
-    case 3: KB_A(3);
-    case 4: KB_A(4);
-    case 5: KB_A(5);
-    default: break;
-  }
-  if constexpr (sizeof(T) == 4) {  // fp32 keeps larger term groups in registers
-    switch (op->G) {
-      case 6: KB_A(6);
-      case 8: KB_A(8);
-      default: break;
-    }
-  }
-#undef KB_A
-  return fail(KB_ERR_ARGUMENT, "unsupported term group size");
+  if constexpr (sizeof(T) == 8)
+    return launch_a_g<T, kGmaxF64>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
+  else
+    return launch_a_g<T, kGmaxF32>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
 }
 
 template <typename T, int MODE>
-int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g,
+int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g, const T* tsign,
              const kb::Epi<T>& e, cudaStream_t s) {
   constexpr int TQ = kb::kNW * kRB;
   const int S = (TQ + g.Wp - 1) | 1;
@@ -201,7 +192,7 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g,
   const long long t_bs = (long long)op->r * g.Wp;
   dim3 grid((g.len + TQ - 1) / TQ, (g.other + 31) / 32, op->batch);
   dim3 block(32, kb::kNW);
-  kern<<<grid, block, smem, s>>>(z, z_ps, z_bs, op->r, tin, t_bs, g, e);
+  kern<<<grid, block, smem, s>>>(z, z_ps, z_bs, op->r, tin, t_bs, g, tsign, e);
   KB_CUDA(cudaGetLastError());
   return KB_OK;
 }
@@ -217,7 +208,7 @@ kb::AxisGeom geom_a(const kb_op* op, int adjoint, const RowBlock& rb) {
   g.other = op->n;
   g.H = op->Ha;
   g.Wp = op->Wpa;
-  g.fill = !adjoint && op->bc_a == KB_BC_REFLECTIVE;
+  g.fill = op->bc_a == KB_BC_REFLECTIVE && (!adjoint || op->sym_a);
   g.g0 = rb.g0;
   g.Mg = rb.mg;
   g.halo_lo = rb.hlo;
@@ -231,7 +222,7 @@ kb::AxisGeom geom_b(const kb_op* op, int adjoint) {
   g.other = op->m;
   g.H = op->Hb;
   g.Wp = op->Wpb;
-  g.fill = !adjoint && op->bc_b == KB_BC_REFLECTIVE;
+  g.fill = op->bc_b == KB_BC_REFLECTIVE && (!adjoint || op->sym_b);
   g.g0 = 0;
   g.Mg = op->n;
   g.halo_lo = 0;
@@ -255,12 +246,12 @@ int stage_a(const kb_op* op, int adjoint, const T* in, const Work& w, const RowB
             const double* nw2, cudaStream_t s) {
   T* z = static_cast<T*>(w.z);
   const kb::AxisGeom ga = geom_a(op, adjoint, rb);
-  KB_TRY(launch_a<T>(op, in, z, static_cast<const T*>(adjoint ? op->ta_corr : op->ta_conv), ga, nw2, s));
-  if (adjoint && op->bc_a == KB_BC_REFLECTIVE && op->Ha > 0) {
+  KB_TRY(launch_a<T>(op, in, z, static_cast<const T*>(adjoint ? op->ta_corr : op->ta_conv), ga,
+                     adjoint ? op->grp_adj : op->grp_fwd, nw2, s));
+  if (adjoint && op->bc_a == KB_BC_REFLECTIVE && !op->sym_a && op->Ha > 0) {
     const long long z_ps = (long long)op->m * op->n;
     dim3 grid((op->n + 127) / 128, 2 * op->Ha * op->r, op->batch);
-    constexpr int NU = sizeof(T) == 8 ? 32 : 64;
-    kb::kb_fold_rows<T, NU><<<grid, 128, 0, s>>>(in, z_ps, z, z_ps, z_ps * op->r, op->r,
+    kb::kb_fold_rows<T><<<grid, 128, 0, s>>>(in, z_ps, z, z_ps, z_ps * op->r, op->r,
                                               static_cast<const T*>(op->ta_conv),
                                               (long long)op->r * op->Wpa, ga);
     KB_CUDA(cudaGetLastError());
@@ -272,20 +263,21 @@ template <typename T, int MODE>
 int stage_b(const kb_op* op, int adjoint, kb::Epi<T> e, const Work& w, cudaStream_t s) {
   const T* z = static_cast<const T*>(w.z);
   const kb::AxisGeom gb = geom_b(op, adjoint);
-  if (adjoint && op->bc_b == KB_BC_REFLECTIVE && op->Hb > 0) {
+  if (adjoint && op->bc_b == KB_BC_REFLECTIVE && !op->sym_b && op->Hb > 0) {
     const int slots = 2 * op->Hb;
     const int bx = std::min(128, (slots + 31) / 32 * 32);
-    constexpr int NU = sizeof(T) == 8 ? 32 : 64;
     dim3 grid((slots + bx - 1) / bx, op->m, op->batch);
     const long long z_ps = (long long)op->m * op->n;
-    kb::kb_fold_cols<T, NU><<<grid, bx, 0, s>>>(z, z_ps, z_ps * op->r, op->r,
+    kb::kb_fold_cols<T><<<grid, bx, 0, s>>>(z, z_ps, z_ps * op->r, op->r,
                                             static_cast<const T*>(op->tb_conv),
                                             (long long)op->r * op->Wpb, gb, static_cast<T*>(w.fold));
     KB_CUDA(cudaGetLastError());
     e.fold = static_cast<const T*>(w.fold);
     e.foldH = op->Hb;
   }
-  return launch_b<T, MODE>(op, z, static_cast<const T*>(adjoint ? op->tb_corr : op->tb_conv), gb, e, s);
+  const T* tsign = (adjoint && op->sym_b) ? static_cast<const T*>(op->sign_b) : nullptr;
+  return launch_b<T, MODE>(op, z, static_cast<const T*>(adjoint ? op->tb_corr : op->tb_conv), gb,
+                           tsign, e, s);
 }
 
 // ---- operator application (one direction) ------------------------------------------------
@@ -389,28 +381,31 @@ int check_op(const kb_op* op) {
   return KB_OK;
 }
 
-// table build: conv[k] = c_{H-k}, corr[k] = c_{k-H}, k in [0, 2H], zero elsewhere
+// table build: conv[k] = c_{H-k}, corr[k] = c_{k-H}, k in [0, 2H], zero elsewhere; row
+// (b, i) of the tables holds host term perm[i] of image b
 template <typename T>
-void build_tables(int dlo, int w, const double* taps, int nrows, int H, int Wp,
-                  std::vector<T>& conv, std::vector<T>& corr) {
-  conv.assign((size_t)nrows * Wp, T(0));
-  corr.assign((size_t)nrows * Wp, T(0));
-  for (int row = 0; row < nrows; ++row) {
-    for (int t = 0; t < w; ++t) {
-      const int d = dlo + t;
-      const double c = taps[(size_t)row * w + t];
-      conv[(size_t)row * Wp + (H - d)] = (T)c;
-      corr[(size_t)row * Wp + (H + d)] = (T)c;
+void build_tables(int dlo, int w, const double* taps, int batch, int r, const std::vector<int>& perm,
+                  int H, int Wp, std::vector<T>& conv, std::vector<T>& corr) {
+  conv.assign((size_t)batch * r * Wp, T(0));
+  corr.assign((size_t)batch * r * Wp, T(0));
+  for (int b = 0; b < batch; ++b)
+    for (int i = 0; i < r; ++i) {
+      const double* src = taps + ((size_t)b * r + perm[i]) * w;
+      T* cv = conv.data() + ((size_t)b * r + i) * Wp;
+      T* cr = corr.data() + ((size_t)b * r + i) * Wp;
+      for (int t = 0; t < w; ++t) {
+        const int d = dlo + t;
+        cv[H - d] = (T)src[t];
+        cr[H + d] = (T)src[t];
+      }
     }
-  }
 }
 
 template <typename T>
-int upload_tables(kb_op* op, int dlo, int w, const double* taps, int H, int Wp, void** conv_d,
-                  void** corr_d) {
+int upload_tables(kb_op* op, int dlo, int w, const double* taps, const std::vector<int>& perm, int H,
+                  int Wp, void** conv_d, void** corr_d) {
   std::vector<T> conv, corr;
-  const int nrows = op->batch * op->r;
-  build_tables<T>(dlo, w, taps, nrows, H, Wp, conv, corr);
+  build_tables<T>(dlo, w, taps, op->batch, op->r, perm, H, Wp, conv, corr);
   const size_t bytes = conv.size() * sizeof(T);
   KB_CUDA(cudaMalloc(conv_d, bytes));
   KB_CUDA(cudaMalloc(corr_d, bytes));
@@ -419,8 +414,34 @@ int upload_tables(kb_op* op, int dlo, int w, const double* taps, int H, int Wp, 
   return KB_OK;
 }
 
+template <typename T>
+int upload_signs(kb_op* op, const std::vector<int>& sign) {
+  std::vector<T> v(sign.begin(), sign.end());
+  KB_CUDA(cudaMalloc(&op->sign_b, v.size() * sizeof(T)));
+  KB_CUDA(cudaMemcpy(op->sign_b, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return KB_OK;
+}
+
+// (Anti)symmetry of a band: sign +1 if c_d ~ c_{-d}, -1 if c_d ~ -c_{-d}; ok when the residual
+// is within kSymTol * max|c|. For such generators the adjoint's folded sources equal the
+// reflect-filled tile times the sign, so F^T needs no separate fold (see kb_kernels.cuh).
+void classify(const double* taps, int dlo, int w, int& sign, bool& ok) {
+  const int H = std::max(std::abs(dlo), std::abs(dlo + w - 1));
+  std::vector<double> full(2 * H + 1, 0.0);
+  for (int t = 0; t < w; ++t) full[dlo + t + H] = taps[t];
+  double mx = 0, rs = 0, ra = 0;
+  for (int k = 0; k <= 2 * H; ++k) {
+    mx = std::max(mx, std::fabs(full[k]));
+    rs = std::max(rs, std::fabs(full[k] - full[2 * H - k]));
+    ra = std::max(ra, std::fabs(full[k] + full[2 * H - k]));
+  }
+  sign = rs <= ra ? 1 : -1;
+  ok = std::min(rs, ra) <= kSymTol * mx;
+}
+
 void free_op(kb_op* op) {
   if (!op) return;
+  cudaFree(op->sign_b);
   cudaFree(op->ta_conv);
   cudaFree(op->ta_corr);
   cudaFree(op->tb_conv);
@@ -548,15 +569,63 @@ int kb_op_create(kb_op** out, int dtype, int m, int n, int r, int batch, int bc_
   op->Hb = Hb;
   op->Wpa = (2 * Ha + 1 + kb::kUB - 1) / kb::kUB * kb::kUB;
   op->Wpb = (2 * Hb + 1 + kb::kUB - 1) / kb::kUB * kb::kUB;
-  op->G = pick_group(r, dtype == KB_F64 ? 5 : 8);
+  op->gmax = dtype == KB_F64 ? kGmaxF64 : kGmaxF32;
+  if ((r + op->gmax - 1) / op->gmax + 1 > kb::kMaxGroups) {
+    delete op;
+    return fail(KB_ERR_ARGUMENT, "too many terms for the pass A group table");
+  }
   op->graph = new GraphCache();
+
+  // Symmetry classes. Axis a: terms are reordered so that the adjoint's pass A groups are
+  // homogeneous in fill sign (same order for every image, else the exact fold path is used).
+  const char* exact_env = std::getenv("KB_EXACT_FOLD");
+  const bool exact = exact_env && exact_env[0] && exact_env[0] != '0';
+  std::vector<int> sa((size_t)batch * r), sb((size_t)batch * r);
+  bool ok_a = bc_a == KB_BC_REFLECTIVE && !exact, ok_b = bc_b == KB_BC_REFLECTIVE && !exact;
+  for (int b = 0; b < batch; ++b)
+    for (int i = 0; i < r; ++i) {
+      bool oka, okb;
+      classify(a_taps + ((size_t)b * r + i) * a_w, a_dlo, a_w, sa[(size_t)b * r + i], oka);
+      classify(b_taps + ((size_t)b * r + i) * b_w, b_dlo, b_w, sb[(size_t)b * r + i], okb);
+      ok_a = ok_a && oka;
+      ok_b = ok_b && okb;
+    }
+  std::vector<int> perm(r);
+  for (int i = 0; i < r; ++i) perm[i] = i;
+  if (ok_a) {
+    std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return sa[x] > sa[y]; });
+    for (int b = 1; b < batch && ok_a; ++b)
+      for (int i = 0; i < r; ++i)
+        if (sa[(size_t)b * r + perm[i]] != sa[perm[i]]) ok_a = false;
+    if (!ok_a)
+      for (int i = 0; i < r; ++i) perm[i] = i;
+  }
+  op->sym_a = ok_a;
+  op->sym_b = ok_b;
+  op->grp_fwd.n = 0;
+  add_groups(op->grp_fwd, 0, r, op->gmax, 1);
+  op->grp_adj.n = 0;
+  if (ok_a) {
+    int nsym = 0;
+    while (nsym < r && sa[perm[nsym]] > 0) ++nsym;
+    add_groups(op->grp_adj, 0, nsym, op->gmax, 1);
+    add_groups(op->grp_adj, nsym, r - nsym, op->gmax, -1);
+  } else {
+    add_groups(op->grp_adj, 0, r, op->gmax, 1);
+  }
+  std::vector<int> sign_b((size_t)batch * r);
+  for (int b = 0; b < batch; ++b)
+    for (int i = 0; i < r; ++i) sign_b[(size_t)b * r + i] = sb[(size_t)b * r + perm[i]];
+
   int rc;
   if (dtype == KB_F64) {
-    rc = upload_tables<double>(op, a_dlo, a_w, a_taps, Ha, op->Wpa, &op->ta_conv, &op->ta_corr);
-    if (rc == KB_OK) rc = upload_tables<double>(op, b_dlo, b_w, b_taps, Hb, op->Wpb, &op->tb_conv, &op->tb_corr);
+    rc = upload_tables<double>(op, a_dlo, a_w, a_taps, perm, Ha, op->Wpa, &op->ta_conv, &op->ta_corr);
+    if (rc == KB_OK) rc = upload_tables<double>(op, b_dlo, b_w, b_taps, perm, Hb, op->Wpb, &op->tb_conv, &op->tb_corr);
+    if (rc == KB_OK && ok_b) rc = upload_signs<double>(op, sign_b);
   } else {
-    rc = upload_tables<float>(op, a_dlo, a_w, a_taps, Ha, op->Wpa, &op->ta_conv, &op->ta_corr);
-    if (rc == KB_OK) rc = upload_tables<float>(op, b_dlo, b_w, b_taps, Hb, op->Wpb, &op->tb_conv, &op->tb_corr);
+    rc = upload_tables<float>(op, a_dlo, a_w, a_taps, perm, Ha, op->Wpa, &op->ta_conv, &op->ta_corr);
+    if (rc == KB_OK) rc = upload_tables<float>(op, b_dlo, b_w, b_taps, perm, Hb, op->Wpb, &op->tb_conv, &op->tb_corr);
+    if (rc == KB_OK && ok_b) rc = upload_signs<float>(op, sign_b);
   }
   if (rc != KB_OK) {
     free_op(op);
@@ -572,6 +641,13 @@ int kb_op_destroy(kb_op* op) {
 }
 
 size_t kb_workspace_bytes(const kb_op* op) { return op ? layout(op, nullptr).bytes : 0; }
+
+int kb_op_info(const kb_op* op, int* info, int n) {
+  KB_TRY(check_op(op));
+  const int v[8] = {op->Ha, op->Wpa, op->Hb, op->Wpb, op->sym_a, op->sym_b, op->grp_adj.n, op->gmax};
+  for (int i = 0; i < n && i < 8; ++i) info[i] = v[i];
+  return KB_OK;
+}
 
 int kb_apply(const kb_op* op, const void* X, void* Y, void* work, void* stream) {
   KB_TRY(check_op(op));

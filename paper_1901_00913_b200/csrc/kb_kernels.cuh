@@ -112,24 +112,73 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N> __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // ------------------------------------------------------------------------------------------
-// pass A: filter along axis 0 (rows) for G terms at a time.
+// pass A: filter along axis 0 (rows), terms processed in groups of up to GMAX.
 //   CTA = 32 lanes (32 columns) x kNW warps; each warp owns R consecutive output rows, so the
 //   CTA tile is (kNW*R) x 32 and the shared tile holds (kNW*R + Wp - 1) input rows.
 // in  : plane (local rows may extend to -halo_lo .. len+halo_hi-1), batch stride in_bs
 // z   : r output planes, plane stride z_ps, batch stride z_bs (same local row indexing as in)
 // tin : taps [batch][r][Wp] (t_bs per image), index k = e + H for source offset e
-// nw2 : optional per-image ||in||^2; loaded values are divided by sqrt(nw2) (power iteration)
+// grp : term groups; with g.fill the out-of-domain tile rows hold sign * x[refl(row)], the sign
+//       being the group's (adjoint of (anti)symmetric generators: see kb_capi.cu, sign_fill)
+// nw2 : optional per-image ||in||^2; outputs are divided by sqrt(nw2) (power iteration)
 // ------------------------------------------------------------------------------------------
+constexpr int kMaxGroups = 16;
+struct Groups {
+  int n;
+  int start[kMaxGroups];
+  int count[kMaxGroups];
+  int sign[kMaxGroups];
+};
+
 template <typename T, int G, int R>
+__device__ __forceinline__ void kb_pass_a_group(const T* __restrict__ xs, const T* __restrict__ cin,
+                                                int Wp, int s_off, int lane, T* __restrict__ z,
+                                                long long z_ps, int gstart, int p0, int len,
+                                                int ncol, int q, bool scaled, T oscale) {
+  T acc[G][R];
+#pragma unroll
+  for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+    for (int j = 0; j < R; ++j) acc[gg][j] = T(0);
+
+  const T* xcol = xs + s_off * 32 + lane;
+  for (int k0 = 0; k0 < Wp; k0 += kU) {
+    T xw[R + kU - 1];
+#pragma unroll
+    for (int i = 0; i < R + kU - 1; ++i) xw[i] = xcol[(k0 + i) * 32];
+#pragma unroll
+    for (int kk = 0; kk < kU; ++kk) {
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) {
+        const T c = cin[gg * Wp + k0 + kk];
+#pragma unroll
+        for (int j = 0; j < R; ++j) acc[gg][j] = kb_fma(c, xw[j + kk], acc[gg][j]);
+      }
+    }
+  }
+  if (q < ncol) {
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+      T* zp = z + (long long)(gstart + gg) * z_ps;
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const int lr = p0 + s_off + j;
+        if (lr < len) zp[(long long)lr * ncol + q] = scaled ? acc[gg][j] * oscale : acc[gg][j];
+      }
+    }
+  }
+}
+
+template <typename T, int GMAX, int R>
 __global__ void __launch_bounds__(32 * kNW, 2)
 kb_pass_a(const T* __restrict__ in, long long in_bs, T* __restrict__ z, long long z_ps,
-          long long z_bs, int r, const T* __restrict__ tin, long long t_bs, AxisGeom g,
+          long long z_bs, const T* __restrict__ tin, long long t_bs, AxisGeom g, Groups grp,
           const double* __restrict__ nw2) {
   extern __shared__ __align__(16) unsigned char kb_smem_a[];
   constexpr int TP = kNW * R;
   const int rows_tile = TP + g.Wp - 1;
   T* xs = reinterpret_cast<T*>(kb_smem_a);   // [rows_tile][32]
-  T* cin = xs + rows_tile * 32;              // [G][Wp]
+  T* cin = xs + rows_tile * 32;              // [GMAX][Wp]
   const int lane = threadIdx.x, warp = threadIdx.y;
   const int tid = warp * 32 + lane;
   const int b = blockIdx.z;
@@ -139,103 +188,78 @@ kb_pass_a(const T* __restrict__ in, long long in_bs, T* __restrict__ z, long lon
   in += b * in_bs;
   z += b * z_bs;
   tin += b * t_bs;
-  // Tile fill: rows [p0-H, p0+TP+Wp-1-H) of the input (folded for the reflective forward),
-  // one warp per row, 8-byte cp.async per lane so every row load is in flight at once.
+  // Tile fill: rows [p0-H, p0+TP+Wp-1-H) of the input (folded when g.fill), one warp per row,
+  // 8-byte cp.async per lane so every row load is in flight at once.
+  const int row_lo = g.g0 + p0 - g.H;               // global row of tile row 0
+  const bool has_out = g.fill && (row_lo < 0 || row_lo + rows_tile > g.Mg);
+  int cur_sign = grp.sign[0];
   for (int rr = warp; rr < rows_tile; rr += kNW) {
-    int gr = g.g0 + p0 - g.H + rr;
-    if (g.fill && (gr < 0 || gr >= g.Mg)) gr = kb_fold(gr, g.Mg);
+    int gr = row_lo + rr;
+    const bool outside = gr < 0 || gr >= g.Mg;
+    if (g.fill && outside) gr = kb_fold(gr, g.Mg);
     const int lr = gr - g.g0;
     T* d = xs + rr * 32 + lane;
-    if (q < ncol && gr >= 0 && gr < g.Mg && lr >= -g.halo_lo && lr < g.len + g.halo_hi)
-      cp_async_elem<T>(d, in + (long long)lr * ncol + q);
-    else
-      *d = T(0);
+    const bool ok = q < ncol && gr >= 0 && gr < g.Mg && lr >= -g.halo_lo && lr < g.len + g.halo_hi;
+    if (ok && !outside) cp_async_elem<T>(d, in + (long long)lr * ncol + q);
+    else *d = ok ? (cur_sign < 0 ? -in[(long long)lr * ncol + q] : in[(long long)lr * ncol + q]) : T(0);
   }
   cp_async_commit();
-  // power iteration: the pass is linear, so v = w/||w|| is applied to the outputs
-  const T oscale = nw2 ? (T)(1.0 / sqrt(nw2[b])) : T(1);
+  const bool scaled = nw2 != nullptr;
+  const T oscale = scaled ? (T)(1.0 / sqrt(nw2[b])) : T(1);
   cp_async_wait<0>();
 
   const int s_off = warp * R;
-  for (int gb = 0; gb < r; gb += G) {
+  for (int gi = 0; gi < grp.n; ++gi) {
+    const int gstart = grp.start[gi], gcount = grp.count[gi];
     __syncthreads();
-    for (int idx = tid; idx < G * g.Wp; idx += 32 * kNW) {
+    if (has_out && grp.sign[gi] != cur_sign) {  // flip the folded rows for this group's sign
+      for (int rr = warp; rr < rows_tile; rr += kNW) {
+        const int gr = row_lo + rr;
+        if (gr < 0 || gr >= g.Mg) xs[rr * 32 + lane] = -xs[rr * 32 + lane];
+      }
+    }
+    cur_sign = grp.sign[gi];
+    for (int idx = tid; idx < gcount * g.Wp; idx += 32 * kNW) {
       const int gg = idx / g.Wp, k = idx - gg * g.Wp;
-      cin[idx] = (gb + gg < r) ? tin[(long long)(gb + gg) * g.Wp + k] : T(0);
+      cin[idx] = tin[(long long)(gstart + gg) * g.Wp + k];
     }
     __syncthreads();
-
-    T acc[G][R];
-#pragma unroll
-    for (int gg = 0; gg < G; ++gg)
-#pragma unroll
-      for (int j = 0; j < R; ++j) acc[gg][j] = T(0);
-
-    const T* xcol = xs + s_off * 32 + lane;
-    for (int k0 = 0; k0 < g.Wp; k0 += kU) {
-      T xw[R + kU - 1];
-#pragma unroll
-      for (int i = 0; i < R + kU - 1; ++i) xw[i] = xcol[(k0 + i) * 32];
-#pragma unroll
-      for (int kk = 0; kk < kU; ++kk) {
-#pragma unroll
-        for (int gg = 0; gg < G; ++gg) {
-          const T c = cin[gg * g.Wp + k0 + kk];
-#pragma unroll
-          for (int j = 0; j < R; ++j) acc[gg][j] = kb_fma(c, xw[j + kk], acc[gg][j]);
-        }
-      }
+#define KB_GROUP(C)                                                                         \
+  case C:                                                                                   \
+    if constexpr (C <= GMAX)                                                                \
+      kb_pass_a_group<T, C, R>(xs, cin, g.Wp, s_off, lane, z, z_ps, gstart, p0, g.len, ncol, \
+                               q, scaled, oscale);                                          \
+    break;
+    switch (gcount) {
+      KB_GROUP(1)
+      KB_GROUP(2)
+      KB_GROUP(3)
+      KB_GROUP(4)
+      KB_GROUP(5)
+      KB_GROUP(6)
+      KB_GROUP(7)
+      KB_GROUP(8)
+      default: break;
     }
-
-    if (q < ncol) {
-#pragma unroll
-      for (int gg = 0; gg < G; ++gg) {
-        if (gb + gg < r) {
-          T* zp = z + (long long)(gb + gg) * z_ps;
-#pragma unroll
-          for (int j = 0; j < R; ++j) {
-            const int lr = p0 + s_off + j;
-            if (lr < g.len) zp[(long long)lr * ncol + q] = nw2 ? acc[gg][j] * oscale : acc[gg][j];
-          }
-        }
-      }
-    }
+#undef KB_GROUP
   }
 }
 
 // ------------------------------------------------------------------------------------------
-// Adjoint fold corrections. For an output index s within H of a reflective domain edge, the
-// transpose adds the folded-source part  sum_{t out of domain} c_{s-t} x[refl(t)]  (conv table,
-// k = t-s+H). With u = refl(t) this is a short Hankel-type sum over the edge samples:
-//   left/top edge   u in [0, min(H-s, M)),   k = H-s-1-u
-//   right/bottom    t in [max(M, s-H), s+H], u = 2M-1-t, k = t-s+H
-// kb_fold_sum loads every edge sample first (all loads in flight), then accumulates.
+// Exact adjoint fold corrections (used when the generators are not (anti)symmetric, so the
+// sign-reflected tile fill does not apply). For an output index s within H of a reflective
+// domain edge, the transpose adds  sum_{t out of domain} c_{s-t} x[refl(t)]  (conv table,
+// k = t-s+H):   left/top edge:  u = -1-t in [0, min(H-s, M)),  k = H-s-1-u
+//               right/bottom:   t in [max(M, s-H), s+H],  u = 2M-1-t,  k = t-s+H
 // ------------------------------------------------------------------------------------------
-template <typename T, int NU>
+template <typename T>
 __device__ __forceinline__ T kb_fold_sum(const T* __restrict__ tc, const T* __restrict__ src,
                                          long long stride, int s, int H, int M) {
   T acc = T(0);
   const int top = min(H - s, M);
-  const int t0 = max(M, s - H), nb = s + H - t0 + 1;  // bottom sources t0 .. s+H
-  if (top <= NU && nb <= NU) {
-    T v[NU];
-#pragma unroll
-    for (int u = 0; u < NU; ++u) v[u] = (u < top) ? src[(long long)u * stride] : T(0);
-#pragma unroll
-    for (int u = 0; u < NU; ++u)
-      if (u < top) acc = kb_fma(tc[H - s - 1 - u], v[u], acc);
-#pragma unroll
-    for (int d = 0; d < NU; ++d) {
-      const int u = 2 * M - 1 - (t0 + d);
-      v[d] = (d < nb && u >= 0) ? src[(long long)u * stride] : T(0);
-    }
-#pragma unroll
-    for (int d = 0; d < NU; ++d)
-      if (d < nb) acc = kb_fma(tc[t0 + d - s + H], v[d], acc);
-    return acc;
-  }
+#pragma unroll 4
   for (int u = 0; u < top; ++u) acc = kb_fma(tc[H - s - 1 - u], src[(long long)u * stride], acc);
-  for (int t = t0; t <= s + H; ++t) {
+  for (int t = max(M, s - H); t <= s + H; ++t) {
     const int u = 2 * M - 1 - t;
     if (u >= 0) acc = kb_fma(tc[t - s + H], src[(long long)u * stride], acc);
   }
@@ -244,7 +268,7 @@ __device__ __forceinline__ T kb_fold_sum(const T* __restrict__ tc, const T* __re
 
 // axis 0: Z_i[s][q] += fold(R[:, q]) for edge rows s. One thread per (edge-row slot, column,
 // term); slot < H is row `slot`, slot >= H is row Mg-2H+slot.
-template <typename T, int NU>
+template <typename T>
 __global__ void __launch_bounds__(128)
 kb_fold_rows(const T* __restrict__ in, long long in_bs, T* __restrict__ z, long long z_ps,
              long long z_bs, int r, const T* __restrict__ tconv, long long t_bs, AxisGeom g) {
@@ -260,14 +284,14 @@ kb_fold_rows(const T* __restrict__ in, long long in_bs, T* __restrict__ z, long 
   if (ls < 0 || ls >= g.len) return;  // not on this row block
   const T* tc = tconv + b * t_bs + (long long)i * g.Wp;
   const T* src = in + b * in_bs + q - (long long)g.g0 * g.other;  // src[u*other] = global row u
-  const T acc = kb_fold_sum<T, NU>(tc, src, g.other, s, H, M);
+  const T acc = kb_fold_sum<T>(tc, src, g.other, s, H, M);
   T* zp = z + b * z_bs + (long long)i * z_ps + (long long)ls * g.other + q;
   *zp = *zp + acc;
 }
 
 // axis 1: fold[b][p][slot] = sum_i fold(Z_i[p, :]) for edge columns (slot < H: column slot;
 // slot >= H: column n-2H+slot); pass B's epilogue adds them. One thread per (row, slot).
-template <typename T, int NU>
+template <typename T>
 __global__ void __launch_bounds__(128)
 kb_fold_cols(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
              const T* __restrict__ tconv, long long t_bs, AxisGeom g, T* __restrict__ fold) {
@@ -282,7 +306,7 @@ kb_fold_cols(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
     const T* zr = z + b * z_bs + (long long)p * n;
     const T* tcb = tconv + b * t_bs;
     for (int i = 0; i < r; ++i)
-      acc += kb_fold_sum<T, NU>(tcb + (long long)i * g.Wp, zr + (long long)i * z_ps, 1, s, H, n);
+      acc += kb_fold_sum<T>(tcb + (long long)i * g.Wp, zr + (long long)i * z_ps, 1, s, H, n);
   }
   fold[((long long)b * g.other + p) * (2 * H) + slot] = acc;
 }
@@ -317,7 +341,8 @@ __device__ __forceinline__ void kb_block_partials(double (&v)[NQ], double* parti
 template <typename T, int R, int MODE>
 __global__ void __launch_bounds__(32 * kNW, 2)
 kb_pass_b(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
-          const T* __restrict__ tin, long long t_bs, AxisGeom g, Epi<T> e) {
+          const T* __restrict__ tin, long long t_bs, AxisGeom g, const T* __restrict__ tsign,
+          Epi<T> e) {
   extern __shared__ __align__(16) unsigned char kb_smem_b[];
   constexpr int TQ = kNW * R;
   const int cols_tile = TQ + g.Wp - 1;
@@ -334,10 +359,12 @@ kb_pass_b(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
   z += b * z_bs;
   tin += b * t_bs;
 
-  // Column sources of the tile (folded for the reflective forward), identical for every row:
-  // computed once per thread for the columns it copies.
+  // One warp per tile row, lanes across columns. With g.fill the out-of-domain columns hold
+  // sign_i * Z_i[p][refl(q)] (sign_i = +1 for the forward; tsign[b][i] for the sign-filled
+  // adjoint), loaded synchronously; in-domain columns go through cp.async.
   auto load_term = [&](int i, int stage) {
     const T* zp = z + (long long)i * z_ps;
+    const T sgn = tsign ? tsign[(long long)b * r + i] : T(1);
     T* dst = zs + stage * 32 * S;
     for (int rr = warp; rr < 32; rr += kNW) {
       const int gp = prow0 + rr;
@@ -345,9 +372,11 @@ kb_pass_b(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
       T* drow = dst + rr * S;
       for (int cc = lane; cc < cols_tile; cc += 32) {
         int gq = q0 - g.H + cc;
-        if (g.fill && (gq < 0 || gq >= g.len)) gq = kb_fold(gq, g.len);
-        if (gp < nrow && gq >= 0 && gq < g.len) cp_async_elem<T>(drow + cc, src + gq);
-        else drow[cc] = T(0);
+        const bool outside = gq < 0 || gq >= g.len;
+        if (g.fill && outside) gq = kb_fold(gq, g.len);
+        const bool ok = gp < nrow && gq >= 0 && gq < g.len;
+        if (ok && !outside) cp_async_elem<T>(drow + cc, src + gq);
+        else drow[cc] = ok ? sgn * src[gq] : T(0);
       }
     }
     for (int k = tid; k < g.Wp; k += 32 * kNW) cin[stage * g.Wp + k] = tin[(long long)i * g.Wp + k];

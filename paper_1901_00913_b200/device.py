@@ -48,6 +48,7 @@ EXPORTS = {
     ),
     "kb_op_destroy": (_c_int, [_vp]),
     "kb_workspace_bytes": (ctypes.c_size_t, [_vp]),
+    "kb_op_info": (_c_int, [_vp, ctypes.POINTER(_c_int), _c_int]),
     "kb_apply": (_c_int, [_vp, _vp, _vp, _vp, _vp]),
     "kb_apply_adjoint": (_c_int, [_vp, _vp, _vp, _vp, _vp]),
     "kb_sfista_run": (
@@ -202,6 +203,13 @@ class DeviceOperator:
         self.work = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self.lock = threading.Lock()
         self._stage = {}
+
+    def info(self) -> dict:
+        """Device layout facts (kb_op_info)."""
+        vals = (_c_int * 8)()
+        _check(load_library().kb_op_info(self._handle, vals, 8), "kb_op_info")
+        keys = ("Ha", "Wpa", "Hb", "Wpb", "sym_a", "sym_b", "adj_groups", "gmax")
+        return dict(zip(keys, (int(v) for v in vals)))
 
     # -- buffers ---------------------------------------------------------------------------
     def plane(self, batched: bool = False):

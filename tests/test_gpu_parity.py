@@ -97,6 +97,31 @@ def test_apply_matches_oracle_fp64(bc, m, size, s, rng):
     assert rel(kb.kron_apply_adjoint(op, X), port.kron_apply_adjoint(pop, X)) <= 1e-12
 
 
+@pytest.mark.parametrize("exact", [False, True])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg5"])
+def test_symmetric_generators_sign_fill(name, exact, monkeypatch):
+    # centrally symmetric BASELINE PSFs give (anti)symmetric generators: the adjoint folds via
+    # sign-reflected tile fills; KB_EXACT_FOLD=1 forces the exact fold kernels instead
+    from paper_1901_00913_b200 import workloads as W
+    from paper_1901_00913_b200.device import DeviceOperator
+
+    cfg = W.CONFIGS[name]
+    m = 3 * cfg.w + 7
+    bc = kb.BoundaryCondition("reflective")  # exercise the fold on every PSF family
+    op = kb.decompose(W.make_psf(cfg), bc, s=cfg.r, shape=(m, m))
+    if exact:
+        monkeypatch.setenv("KB_EXACT_FOLD", "1")
+    info = DeviceOperator([op], "float64").info()
+    assert info["sym_a"] == info["sym_b"] == (0 if exact else 1)
+    dev = DeviceOperator([op], "float64")
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((m, m))
+    t = torch.from_numpy(X).cuda()
+    pop = port.PortOperator(op)
+    assert rel(dev.apply(t, adjoint=True).cpu().numpy(), port.kron_apply_adjoint(pop, X)) <= 1e-12
+    assert rel(dev.apply(t).cpu().numpy(), port.kron_apply(pop, X)) <= 1e-12
+
+
 @pytest.mark.parametrize("bc", [ZERO, REFL])
 def test_adjoint_identity(bc, rng):
     psf = random_psf(rng, 11)
