@@ -87,9 +87,9 @@ struct Work {
   size_t bytes;
 };
 
-int pass_b_blocks(const kb_op* op) {
-  const int TQ = kb::kNW * kRB;
-  return ((op->n + TQ - 1) / TQ) * ((op->m + 31) / 32);
+int pass_b_blocks(const kb_op* op) {  // blocks of the sum pass (one partial each)
+  const int TS = kb::kNW * kRB;
+  return ((op->n + TS - 1) / TS) * ((op->m + 31) / 32);
 }
 
 Work layout(const kb_op* op, void* base) {
@@ -155,11 +155,11 @@ template <typename T, int GMAX>
 int launch_a_g(const T* in, long long in_bs, T* z, long long z_ps, long long z_bs,
                const T* tin, long long t_bs, const kb::AxisGeom& g, const kb::Groups& grp,
                const double* nw2, int batch, cudaStream_t s) {
-  constexpr int TP = kb::kNW * kRA;
-  const size_t smem = sizeof(T) * ((size_t)(TP + g.Wp - 1) * 32 + (size_t)GMAX * g.Wp);
-  auto kern = kb::kb_pass_a<T, GMAX, kRA>;
+  constexpr int TS = kb::kNW * kRA;
+  const size_t smem = sizeof(T) * ((size_t)(TS + g.Wp) * 32 + (size_t)GMAX * g.Wp + 32 * (TS + 1));
+  auto kern = kb::kb_pass_split<T, GMAX, kRA>;
   KB_TRY(allow_smem(kern, smem));
-  dim3 grid((g.other + 31) / 32, (g.len + TP - 1) / TP, batch);
+  dim3 grid((g.other + 31) / 32, (g.len + TS - 1) / TS, batch);
   dim3 block(32, kb::kNW);
   kern<<<grid, block, smem, s>>>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2);
   KB_CUDA(cudaGetLastError());
@@ -182,15 +182,14 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
 template <typename T, int MODE>
 int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g, const T* tsign,
              const kb::Epi<T>& e, cudaStream_t s) {
-  constexpr int TQ = kb::kNW * kRB;
-  const int S = (TQ + g.Wp - 1) | 1;
-  const size_t smem = sizeof(T) * (2 * 32 * (size_t)S + 2 * (size_t)g.Wp);
-  auto kern = kb::kb_pass_b<T, kRB, MODE>;
+  constexpr int TS = kb::kNW * kRB;
+  const size_t smem = sizeof(T) * (2 * (size_t)(TS + g.Wp) * 32 + 2 * (size_t)g.Wp);
+  auto kern = kb::kb_pass_sum<T, kRB, MODE>;
   KB_TRY(allow_smem(kern, smem));
   const long long z_ps = (long long)g.len * g.other;
   const long long z_bs = z_ps * op->r;
   const long long t_bs = (long long)op->r * g.Wp;
-  dim3 grid((g.len + TQ - 1) / TQ, (g.other + 31) / 32, op->batch);
+  dim3 grid((g.other + 31) / 32, (g.len + TS - 1) / TS, op->batch);
   dim3 block(32, kb::kNW);
   kern<<<grid, block, smem, s>>>(z, z_ps, z_bs, op->r, tin, t_bs, g, tsign, e);
   KB_CUDA(cudaGetLastError());
@@ -216,7 +215,7 @@ kb::AxisGeom geom_a(const kb_op* op, int adjoint, const RowBlock& rb) {
   return g;
 }
 
-kb::AxisGeom geom_b(const kb_op* op, int adjoint) {
+kb::AxisGeom geom_b(const kb_op* op, int adjoint) {  // sum pass over Z_i^T [n][m]
   kb::AxisGeom g;
   g.len = op->n;
   g.other = op->m;
@@ -251,9 +250,9 @@ int stage_a(const kb_op* op, int adjoint, const T* in, const Work& w, const RowB
   if (adjoint && op->bc_a == KB_BC_REFLECTIVE && !op->sym_a && op->Ha > 0) {
     const long long z_ps = (long long)op->m * op->n;
     dim3 grid((op->n + 127) / 128, 2 * op->Ha * op->r, op->batch);
-    kb::kb_fold_rows<T><<<grid, 128, 0, s>>>(in, z_ps, z, z_ps, z_ps * op->r, op->r,
-                                              static_cast<const T*>(op->ta_conv),
-                                              (long long)op->r * op->Wpa, ga);
+    kb::kb_fold_split<T><<<grid, 128, 0, s>>>(in, z_ps, z, z_ps, z_ps * op->r, op->r,
+                                               static_cast<const T*>(op->ta_conv),
+                                               (long long)op->r * op->Wpa, ga);
     KB_CUDA(cudaGetLastError());
   }
   return KB_OK;
@@ -264,13 +263,12 @@ int stage_b(const kb_op* op, int adjoint, kb::Epi<T> e, const Work& w, cudaStrea
   const T* z = static_cast<const T*>(w.z);
   const kb::AxisGeom gb = geom_b(op, adjoint);
   if (adjoint && op->bc_b == KB_BC_REFLECTIVE && !op->sym_b && op->Hb > 0) {
-    const int slots = 2 * op->Hb;
-    const int bx = std::min(128, (slots + 31) / 32 * 32);
-    dim3 grid((slots + bx - 1) / bx, op->m, op->batch);
+    dim3 grid((op->m + 127) / 128, 2 * op->Hb, op->batch);
     const long long z_ps = (long long)op->m * op->n;
-    kb::kb_fold_cols<T><<<grid, bx, 0, s>>>(z, z_ps, z_ps * op->r, op->r,
-                                            static_cast<const T*>(op->tb_conv),
-                                            (long long)op->r * op->Wpb, gb, static_cast<T*>(w.fold));
+    kb::kb_fold_sum_pass<T><<<grid, 128, 0, s>>>(z, z_ps, z_ps * op->r, op->r,
+                                                  static_cast<const T*>(op->tb_conv),
+                                                  (long long)op->r * op->Wpb, gb,
+                                                  static_cast<T*>(w.fold));
     KB_CUDA(cudaGetLastError());
     e.fold = static_cast<const T*>(w.fold);
     e.foldH = op->Hb;
@@ -567,7 +565,7 @@ int kb_op_create(kb_op** out, int dtype, int m, int n, int r, int batch, int bc_
   op->bc_b = bc_b;
   op->Ha = Ha;
   op->Hb = Hb;
-  op->Wpa = (2 * Ha + 1 + kb::kUB - 1) / kb::kUB * kb::kUB;
+  op->Wpa = (2 * Ha + 1 + kb::kUB - 1) / kb::kUB * kb::kUB;  // multiple of both passes' R
   op->Wpb = (2 * Hb + 1 + kb::kUB - 1) / kb::kUB * kb::kUB;
   op->gmax = dtype == KB_F64 ? kGmaxF64 : kGmaxF32;
   if ((r + op->gmax - 1) / op->gmax + 1 > kb::kMaxGroups) {

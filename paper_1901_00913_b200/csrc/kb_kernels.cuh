@@ -1,12 +1,16 @@
 // kb_kernels.cuh — sm_100a kernels for the sFISTA hot path (Kronecker-sum blur operator).
 //
 // The operator A_s X = sum_i H_i X K_i^T (kronblur kron.py:218-225) is evaluated as two
-// separable one-dimensional "passes" over row-major (m, n) planes in HBM:
+// separable one-dimensional "passes". Both passes read a row-major plane [S][L], filter along
+// its slow axis S (each thread walks S in registers, the 32 lanes of a warp cover 32
+// consecutive L), and write their result TRANSPOSED, [L][S], through a shared-memory stage —
+// so every global access is a coalesced row segment and the second pass sees its filter axis
+// as the slow axis again:
 //
-//   pass A  (filter along axis 0, lanes along axis 1):  Z_i = F(a_i) X      for a group of
-//           G terms at once, so one shared-memory read of X feeds G*R FMAs per thread.
-//   pass B  (filter along axis 1, lanes along axis 0):  Y = sum_i Z_i F(b_i)^T, summed in
-//           registers over all r terms, followed by a fused epilogue:
+//   pass A "split" (S = m, L = n):  Z_i^T = (F(a_i) X)^T   for a group of G terms at once, so
+//           one shared-memory read of X feeds G*R FMAs per thread; r planes [n][m] out.
+//   pass B "sum"   (S = n, L = m):  Y = sum_i (F(b_i) Z_i^T)^T, summed in registers over all r
+//           terms (double-buffered tiles), written as [m][n] with a fused epilogue:
 //             PLAIN  Y                                 (kron_apply / kron_apply_adjoint)
 //             RESID  R = Y - B                         (forward half of an sFISTA step)
 //             UPDATE x = max0((L y - G)/(L + lam^2)); y' = x + beta (x - x_prev)
@@ -31,18 +35,17 @@
 
 namespace kb {
 
-constexpr int kU = 8;    // taps per unrolled chunk in pass A
-constexpr int kUB = 16;  // taps per unrolled chunk in pass B (tables padded to a multiple of 16)
+constexpr int kUB = 16;  // tap tables are padded to a multiple of 16 (>= both passes' R)
 constexpr int kNW = 8;   // warps per CTA
 
 enum EpiMode { EPI_PLAIN = 0, EPI_RESID = 1, EPI_UPDATE = 2, EPI_POWER = 3 };
 
-// Geometry of the filtered axis. Local index 0 of the plane is global index g0; the plane
-// has `len` local entries along the axis and `halo_lo`/`halo_hi` extra readable entries on
+// Geometry of a pass over an input plane [S][L] (row stride L). Local S index 0 is global
+// index g0; the plane has `len` local rows and `halo_lo`/`halo_hi` extra readable rows on
 // either side (row-block sharding); the domain (for zero-fill / reflection) is [0, Mg).
 struct AxisGeom {
-  int len;      // local extent along the filtered axis
-  int other;    // extent of the other axis
+  int len;      // local extent along S (rows of the input plane, columns of the output plane)
+  int other;    // extent along L (columns of the input plane, rows of the output plane)
   int H;        // half width of the (symmetric, zero padded) tap window
   int Wp;       // padded tap count (multiple of kUB, >= 2H+1)
   int fill;     // 1 = reflect-fill out-of-domain tile entries (forward, reflective kind)
@@ -70,7 +73,7 @@ struct Epi {
   double* partials;    // POWER/UPDATE-with-norms: [batch][gridblocks][4]
   int want_norms;      // UPDATE: accumulate ||x-xp||^2, ||xp||^2, ||x||^2
   long long bstride;   // elements between images for out/bsub/x/y/vin
-  const T* fold;       // adjoint, reflective axis 1: [batch][rows][2*foldH] edge corrections
+  const T* fold;       // adjoint, exact fold on axis 1: [batch][m][2*foldH] edge corrections
   int foldH;           // half width of axis 1 (0: no fold corrections)
 };
 
@@ -112,15 +115,74 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N> __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // ------------------------------------------------------------------------------------------
-// pass A: filter along axis 0 (rows), terms processed in groups of up to GMAX.
-//   CTA = 32 lanes (32 columns) x kNW warps; each warp owns R consecutive output rows, so the
-//   CTA tile is (kNW*R) x 32 and the shared tile holds (kNW*R + Wp - 1) input rows.
-// in  : plane (local rows may extend to -halo_lo .. len+halo_hi-1), batch stride in_bs
-// z   : r output planes, plane stride z_ps, batch stride z_bs (same local row indexing as in)
-// tin : taps [batch][r][Wp] (t_bs per image), index k = e + H for source offset e
-// grp : term groups; with g.fill the out-of-domain tile rows hold sign * x[refl(row)], the sign
-//       being the group's (adjoint of (anti)symmetric generators: see kb_capi.cu, sign_fill)
-// nw2 : optional per-image ||in||^2; outputs are divided by sqrt(nw2) (power iteration)
+// Register-blocked banded dot products along the serial axis of one thread.
+//   acc[g][j] += sum_k c_g[k] * x[(j + k) * 32],   j < R, k < Wp   (Wp a multiple of R)
+// x is a column of a [rows][32] shared-memory tile. The window slides R taps at a time through
+// two register arrays whose roles alternate, so each tap costs one new load and the loads of
+// the next block overlap the FMAs of the current one.
+// ------------------------------------------------------------------------------------------
+template <typename T, int G, int R>
+__device__ __forceinline__ void kb_taps(T (&acc)[G][R], const T* __restrict__ x,
+                                        const T* __restrict__ coef, int cstride, int Wp) {
+  T A[R], B[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) A[j] = x[j * 32];
+  for (int k0 = 0; k0 < Wp; k0 += 2 * R) {
+#pragma unroll
+    for (int j = 0; j < R; ++j) B[j] = x[(k0 + R + j) * 32];
+#pragma unroll
+    for (int kk = 0; kk < R; ++kk) {
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) {
+        const T c = coef[gg * cstride + k0 + kk];
+#pragma unroll
+        for (int j = 0; j < R; ++j) acc[gg][j] = kb_fma(c, (j + kk < R) ? A[j + kk] : B[j + kk - R], acc[gg][j]);
+      }
+    }
+    if (k0 + R >= Wp) break;
+#pragma unroll
+    for (int j = 0; j < R; ++j) A[j] = x[(k0 + 2 * R + j) * 32];
+#pragma unroll
+    for (int kk = 0; kk < R; ++kk) {
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) {
+        const T c = coef[gg * cstride + k0 + R + kk];
+#pragma unroll
+        for (int j = 0; j < R; ++j) acc[gg][j] = kb_fma(c, (j + kk < R) ? B[j + kk] : A[j + kk - R], acc[gg][j]);
+      }
+    }
+  }
+}
+
+// Fill rows [0, rows) of a [rows][32] tile with input rows S = row_lo + rr (global), lanes
+// over L = l0 + lane. In-domain rows stream in with cp.async; out-of-domain rows are folded
+// (times `sign`) when g.fill, else zero.
+template <typename T>
+__device__ __forceinline__ void kb_fill_tile(T* __restrict__ xs, const T* __restrict__ in,
+                                             const AxisGeom& g, int row_lo, int rows, int l,
+                                             int warp, int lane, int sign) {
+  for (int rr = warp; rr < rows; rr += kNW) {
+    int gr = row_lo + rr;
+    const bool outside = gr < 0 || gr >= g.Mg;
+    if (g.fill && outside) gr = kb_fold(gr, g.Mg);
+    const int lr = gr - g.g0;
+    T* d = xs + rr * 32 + lane;
+    const bool ok = l < g.other && gr >= 0 && gr < g.Mg && lr >= -g.halo_lo && lr < g.len + g.halo_hi;
+    if (ok && !outside) cp_async_elem<T>(d, in + (long long)lr * g.other + l);
+    else *d = ok ? (sign < 0 ? -in[(long long)lr * g.other + l] : in[(long long)lr * g.other + l]) : T(0);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// pass A (split): Z_i^T[l][s] = sum_k c_i[k] X[s - H + k][l] for every term of a group.
+//   CTA = 32 lanes (L) x kNW warps; each warp owns R consecutive outputs along S, so the CTA
+//   tile is TS = kNW*R along S by 32 along L; the input tile holds TS + Wp rows.
+// in   : input plane [S][L] (local rows may extend to -halo_lo .. len+halo_hi-1)
+// z    : r output planes [L][S] (z_ps per plane, z_bs per image)
+// tin  : taps [batch][r][Wp], index k = e + H for source offset e
+// grp  : term groups; with g.fill the out-of-domain tile rows hold sign * x[refl(row)] with the
+//        group's sign (adjoint of (anti)symmetric generators: see kb_capi.cu)
+// nw2  : optional per-image ||in||^2; outputs are divided by sqrt(nw2) (power iteration)
 // ------------------------------------------------------------------------------------------
 constexpr int kMaxGroups = 16;
 struct Groups {
@@ -131,81 +193,60 @@ struct Groups {
 };
 
 template <typename T, int G, int R>
-__device__ __forceinline__ void kb_pass_a_group(const T* __restrict__ xs, const T* __restrict__ cin,
-                                                int Wp, int s_off, int lane, T* __restrict__ z,
-                                                long long z_ps, int gstart, int p0, int len,
-                                                int ncol, int q, bool scaled, T oscale) {
+__device__ __forceinline__ void kb_split_group(const T* __restrict__ xs, const T* __restrict__ cin,
+                                               T* __restrict__ ot, const AxisGeom& g, int s_off,
+                                               int lane, int warp, T* __restrict__ z,
+                                               long long z_ps, int gstart, int s0, int l0,
+                                               T oscale) {
+  constexpr int TS = kNW * R;
   T acc[G][R];
 #pragma unroll
   for (int gg = 0; gg < G; ++gg)
 #pragma unroll
     for (int j = 0; j < R; ++j) acc[gg][j] = T(0);
-
-  const T* xcol = xs + s_off * 32 + lane;
-  for (int k0 = 0; k0 < Wp; k0 += kU) {
-    T xw[R + kU - 1];
+  kb_taps<T, G, R>(acc, xs + s_off * 32 + lane, cin, g.Wp, g.Wp);
 #pragma unroll
-    for (int i = 0; i < R + kU - 1; ++i) xw[i] = xcol[(k0 + i) * 32];
+  for (int gg = 0; gg < G; ++gg) {
 #pragma unroll
-    for (int kk = 0; kk < kU; ++kk) {
+    for (int j = 0; j < R; ++j) ot[lane * (TS + 1) + s_off + j] = acc[gg][j] * oscale;
+    __syncthreads();
+    T* zp = z + (long long)(gstart + gg) * z_ps;
+    for (int l = warp; l < 32; l += kNW) {
+      if (l0 + l >= g.other) break;
+      T* zrow = zp + (long long)(l0 + l) * g.len + s0;
 #pragma unroll
-      for (int gg = 0; gg < G; ++gg) {
-        const T c = cin[gg * Wp + k0 + kk];
-#pragma unroll
-        for (int j = 0; j < R; ++j) acc[gg][j] = kb_fma(c, xw[j + kk], acc[gg][j]);
-      }
+      for (int s = lane; s < TS; s += 32)
+        if (s0 + s < g.len) zrow[s] = ot[l * (TS + 1) + s];
     }
-  }
-  if (q < ncol) {
-#pragma unroll
-    for (int gg = 0; gg < G; ++gg) {
-      T* zp = z + (long long)(gstart + gg) * z_ps;
-#pragma unroll
-      for (int j = 0; j < R; ++j) {
-        const int lr = p0 + s_off + j;
-        if (lr < len) zp[(long long)lr * ncol + q] = scaled ? acc[gg][j] * oscale : acc[gg][j];
-      }
-    }
+    __syncthreads();
   }
 }
 
 template <typename T, int GMAX, int R>
 __global__ void __launch_bounds__(32 * kNW, 2)
-kb_pass_a(const T* __restrict__ in, long long in_bs, T* __restrict__ z, long long z_ps,
-          long long z_bs, const T* __restrict__ tin, long long t_bs, AxisGeom g, Groups grp,
-          const double* __restrict__ nw2) {
+kb_pass_split(const T* __restrict__ in, long long in_bs, T* __restrict__ z, long long z_ps,
+              long long z_bs, const T* __restrict__ tin, long long t_bs, AxisGeom g, Groups grp,
+              const double* __restrict__ nw2) {
   extern __shared__ __align__(16) unsigned char kb_smem_a[];
-  constexpr int TP = kNW * R;
-  const int rows_tile = TP + g.Wp - 1;
-  T* xs = reinterpret_cast<T*>(kb_smem_a);   // [rows_tile][32]
-  T* cin = xs + rows_tile * 32;              // [GMAX][Wp]
+  constexpr int TS = kNW * R;
+  const int rows_tile = TS + g.Wp;               // window reads reach s_off + Wp + R - 1
+  T* xs = reinterpret_cast<T*>(kb_smem_a);       // [rows_tile][32]
+  T* cin = xs + rows_tile * 32;                  // [GMAX][Wp]
+  T* ot = cin + GMAX * g.Wp;                     // [32][TS + 1] transpose stage
   const int lane = threadIdx.x, warp = threadIdx.y;
   const int tid = warp * 32 + lane;
   const int b = blockIdx.z;
-  const int p0 = blockIdx.y * TP;
-  const int q = blockIdx.x * 32 + lane;
-  const int ncol = g.other;
+  const int s0 = blockIdx.y * TS;
+  const int l0 = blockIdx.x * 32;
   in += b * in_bs;
   z += b * z_bs;
   tin += b * t_bs;
-  // Tile fill: rows [p0-H, p0+TP+Wp-1-H) of the input (folded when g.fill), one warp per row,
-  // 8-byte cp.async per lane so every row load is in flight at once.
-  const int row_lo = g.g0 + p0 - g.H;               // global row of tile row 0
+  const int row_lo = g.g0 + s0 - g.H;            // global S index of tile row 0
   const bool has_out = g.fill && (row_lo < 0 || row_lo + rows_tile > g.Mg);
   int cur_sign = grp.sign[0];
-  for (int rr = warp; rr < rows_tile; rr += kNW) {
-    int gr = row_lo + rr;
-    const bool outside = gr < 0 || gr >= g.Mg;
-    if (g.fill && outside) gr = kb_fold(gr, g.Mg);
-    const int lr = gr - g.g0;
-    T* d = xs + rr * 32 + lane;
-    const bool ok = q < ncol && gr >= 0 && gr < g.Mg && lr >= -g.halo_lo && lr < g.len + g.halo_hi;
-    if (ok && !outside) cp_async_elem<T>(d, in + (long long)lr * ncol + q);
-    else *d = ok ? (cur_sign < 0 ? -in[(long long)lr * ncol + q] : in[(long long)lr * ncol + q]) : T(0);
-  }
+  kb_fill_tile<T>(xs, in, g, row_lo, rows_tile, l0 + lane, warp, lane, cur_sign);
   cp_async_commit();
-  const bool scaled = nw2 != nullptr;
-  const T oscale = scaled ? (T)(1.0 / sqrt(nw2[b])) : T(1);
+  const T oscale = nw2 ? (T)(1.0 / sqrt(nw2[b])) : T(1);
   cp_async_wait<0>();
 
   const int s_off = warp * R;
@@ -219,16 +260,12 @@ kb_pass_a(const T* __restrict__ in, long long in_bs, T* __restrict__ z, long lon
       }
     }
     cur_sign = grp.sign[gi];
-    for (int idx = tid; idx < gcount * g.Wp; idx += 32 * kNW) {
-      const int gg = idx / g.Wp, k = idx - gg * g.Wp;
-      cin[idx] = tin[(long long)(gstart + gg) * g.Wp + k];
-    }
+    for (int idx = tid; idx < gcount * g.Wp; idx += 32 * kNW) cin[idx] = tin[(long long)gstart * g.Wp + idx];
     __syncthreads();
-#define KB_GROUP(C)                                                                         \
-  case C:                                                                                   \
-    if constexpr (C <= GMAX)                                                                \
-      kb_pass_a_group<T, C, R>(xs, cin, g.Wp, s_off, lane, z, z_ps, gstart, p0, g.len, ncol, \
-                               q, scaled, oscale);                                          \
+#define KB_GROUP(C)                                                                           \
+  case C:                                                                                     \
+    if constexpr (C <= GMAX)                                                                  \
+      kb_split_group<T, C, R>(xs, cin, ot, g, s_off, lane, warp, z, z_ps, gstart, s0, l0, oscale); \
     break;
     switch (gcount) {
       KB_GROUP(1)
@@ -266,49 +303,50 @@ __device__ __forceinline__ T kb_fold_sum(const T* __restrict__ tc, const T* __re
   return acc;
 }
 
-// axis 0: Z_i[s][q] += fold(R[:, q]) for edge rows s. One thread per (edge-row slot, column,
-// term); slot < H is row `slot`, slot >= H is row Mg-2H+slot.
+// split-pass fold: Z_i^T[l][s] += fold over S of in[:, l], for edge S positions s. One thread
+// per (L index, edge slot, term); slot < H is S = slot, slot >= H is S = Mg-2H+slot.
 template <typename T>
 __global__ void __launch_bounds__(128)
-kb_fold_rows(const T* __restrict__ in, long long in_bs, T* __restrict__ z, long long z_ps,
-             long long z_bs, int r, const T* __restrict__ tconv, long long t_bs, AxisGeom g) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+kb_fold_split(const T* __restrict__ in, long long in_bs, T* __restrict__ z, long long z_ps,
+              long long z_bs, int r, const T* __restrict__ tconv, long long t_bs, AxisGeom g) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
   const int slot = blockIdx.y % (2 * g.H);
   const int i = blockIdx.y / (2 * g.H);
   const int b = blockIdx.z;
-  if (q >= g.other || i >= r) return;
+  if (l >= g.other || i >= r) return;
   const int H = g.H, M = g.Mg;
-  const int s = slot < H ? slot : M - 2 * H + slot;  // global output row
+  const int s = slot < H ? slot : M - 2 * H + slot;  // global S index
   if (s < 0 || s >= M || (slot >= H && s < H)) return;
   const int ls = s - g.g0;
   if (ls < 0 || ls >= g.len) return;  // not on this row block
   const T* tc = tconv + b * t_bs + (long long)i * g.Wp;
-  const T* src = in + b * in_bs + q - (long long)g.g0 * g.other;  // src[u*other] = global row u
+  const T* src = in + b * in_bs + l - (long long)g.g0 * g.other;  // src[u*other] = global row u
   const T acc = kb_fold_sum<T>(tc, src, g.other, s, H, M);
-  T* zp = z + b * z_bs + (long long)i * z_ps + (long long)ls * g.other + q;
+  T* zp = z + b * z_bs + (long long)i * z_ps + (long long)l * g.len + ls;
   *zp = *zp + acc;
 }
 
-// axis 1: fold[b][p][slot] = sum_i fold(Z_i[p, :]) for edge columns (slot < H: column slot;
-// slot >= H: column n-2H+slot); pass B's epilogue adds them. One thread per (row, slot).
+// sum-pass fold: fold[b][l][slot] = sum_i fold over S of Z_i^T[:, l] for edge S positions
+// (slot < H: S = slot; slot >= H: S = n-2H+slot), added by the sum pass epilogue. One thread
+// per (L index, slot); lanes run along L so every source row is read coalesced.
 template <typename T>
 __global__ void __launch_bounds__(128)
-kb_fold_cols(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
-             const T* __restrict__ tconv, long long t_bs, AxisGeom g, T* __restrict__ fold) {
-  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
-  const int p = blockIdx.y;
+kb_fold_sum_pass(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
+                 const T* __restrict__ tconv, long long t_bs, AxisGeom g, T* __restrict__ fold) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  const int slot = blockIdx.y;
   const int b = blockIdx.z;
   const int n = g.len, H = g.H;
-  if (slot >= 2 * H) return;
+  if (l >= g.other) return;
   const int s = slot < H ? slot : n - 2 * H + slot;
   T acc = T(0);
   if (s >= 0 && s < n && !(slot >= H && s < H)) {
-    const T* zr = z + b * z_bs + (long long)p * n;
+    const T* zl = z + b * z_bs + l;
     const T* tcb = tconv + b * t_bs;
     for (int i = 0; i < r; ++i)
-      acc += kb_fold_sum<T>(tcb + (long long)i * g.Wp, zr + (long long)i * z_ps, 1, s, H, n);
+      acc += kb_fold_sum<T>(tcb + (long long)i * g.Wp, zl + (long long)i * z_ps, g.other, s, H, n);
   }
-  fold[((long long)b * g.other + p) * (2 * H) + slot] = acc;
+  fold[((long long)b * g.other + l) * (2 * H) + slot] = acc;
 }
 
 // block reduction of NQ doubles into partials[b][block][0..NQ-1] (deterministic order)
@@ -333,62 +371,42 @@ __device__ __forceinline__ void kb_block_partials(double (&v)[NQ], double* parti
 }
 
 // ------------------------------------------------------------------------------------------
-// pass B: filter along axis 1 (columns), summing all r terms in registers, fused epilogue.
-//   CTA = 32 lanes (32 rows) x kNW warps; each warp owns R consecutive output columns, so the
-//   CTA tile is 32 x (kNW*R). Term tiles are double buffered in shared memory with cp.async;
-//   the tile row stride S is odd so the column-wise register windows are bank-conflict free.
+// pass B (sum): Y[l][s] = sum_i sum_k c_i[k] Z_i^T[s - H + k][l], with the fused epilogue.
+//   Same CTA geometry as the split pass (TS = kNW*R along S, 32 along L); term tiles are double
+//   buffered with cp.async; the result is transposed through shared memory so the epilogue
+//   reads and writes [L][S] = [m][n] rows coalesced.
 // ------------------------------------------------------------------------------------------
 template <typename T, int R, int MODE>
 __global__ void __launch_bounds__(32 * kNW, 2)
-kb_pass_b(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
-          const T* __restrict__ tin, long long t_bs, AxisGeom g, const T* __restrict__ tsign,
-          Epi<T> e) {
+kb_pass_sum(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
+            const T* __restrict__ tin, long long t_bs, AxisGeom g, const T* __restrict__ tsign,
+            Epi<T> e) {
   extern __shared__ __align__(16) unsigned char kb_smem_b[];
-  constexpr int TQ = kNW * R;
-  const int cols_tile = TQ + g.Wp - 1;
-  const int S = cols_tile | 1;  // odd stride
-  T* zs = reinterpret_cast<T*>(kb_smem_b);  // [2][32][S]
-  T* cin = zs + 2 * 32 * S;                   // [2][Wp]
+  constexpr int TS = kNW * R;
+  const int rows_tile = TS + g.Wp;
+  T* xs = reinterpret_cast<T*>(kb_smem_b);   // [2][rows_tile][32]; reused as [32][TS+1] at the end
+  T* cin = xs + 2 * rows_tile * 32;          // [2][Wp]
   const int lane = threadIdx.x, warp = threadIdx.y;
   const int tid = warp * 32 + lane;
   const int b = blockIdx.z;
-  const int nrow = g.other;                   // rows of the plane (axis 0 extent)
-  const int q0 = blockIdx.x * TQ;
-  const int prow0 = blockIdx.y * 32;
-  const int p = prow0 + lane;
+  const int s0 = blockIdx.y * TS;
+  const int l0 = blockIdx.x * 32;
   z += b * z_bs;
   tin += b * t_bs;
+  const int row_lo = g.g0 + s0 - g.H;
 
-  // One warp per tile row, lanes across columns. With g.fill the out-of-domain columns hold
-  // sign_i * Z_i[p][refl(q)] (sign_i = +1 for the forward; tsign[b][i] for the sign-filled
-  // adjoint), loaded synchronously; in-domain columns go through cp.async.
   auto load_term = [&](int i, int stage) {
-    const T* zp = z + (long long)i * z_ps;
-    const T sgn = tsign ? tsign[(long long)b * r + i] : T(1);
-    T* dst = zs + stage * 32 * S;
-    for (int rr = warp; rr < 32; rr += kNW) {
-      const int gp = prow0 + rr;
-      const T* src = zp + (long long)gp * g.len;
-      T* drow = dst + rr * S;
-      for (int cc = lane; cc < cols_tile; cc += 32) {
-        int gq = q0 - g.H + cc;
-        const bool outside = gq < 0 || gq >= g.len;
-        if (g.fill && outside) gq = kb_fold(gq, g.len);
-        const bool ok = gp < nrow && gq >= 0 && gq < g.len;
-        if (ok && !outside) cp_async_elem<T>(drow + cc, src + gq);
-        else drow[cc] = ok ? sgn * src[gq] : T(0);
-      }
-    }
+    const int sgn = tsign ? (tsign[(long long)b * r + i] < T(0) ? -1 : 1) : 1;
+    kb_fill_tile<T>(xs + stage * rows_tile * 32, z + (long long)i * z_ps, g, row_lo, rows_tile,
+                    l0 + lane, warp, lane, sgn);
     for (int k = tid; k < g.Wp; k += 32 * kNW) cin[stage * g.Wp + k] = tin[(long long)i * g.Wp + k];
     cp_async_commit();
   };
 
-  T acc[R];
+  T acc[1][R];
 #pragma unroll
-  for (int j = 0; j < R; ++j) acc[j] = T(0);
-
-  const int c_off = warp * R;
-  const int s_first = q0 + c_off;  // first output column of this warp (columns are global)
+  for (int j = 0; j < R; ++j) acc[0][j] = T(0);
+  const int s_off = warp * R;
 
   load_term(0, 0);
   for (int i = 0; i < r; ++i) {
@@ -400,114 +418,108 @@ kb_pass_b(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
       cp_async_wait<0>();
     }
     __syncthreads();
-    const T* zrow = zs + st * 32 * S + lane * S + c_off;
-    const T* ci = cin + st * g.Wp;
-    for (int k0 = 0; k0 < g.Wp; k0 += kUB) {
-      T xw[R + kUB - 1];
-#pragma unroll
-      for (int t = 0; t < R + kUB - 1; ++t) xw[t] = zrow[k0 + t];
-#pragma unroll
-      for (int kk = 0; kk < kUB; ++kk) {
-        const T c = ci[k0 + kk];
-#pragma unroll
-        for (int j = 0; j < R; ++j) acc[j] = kb_fma(c, xw[j + kk], acc[j]);
-      }
-    }
+    kb_taps<T, 1, R>(acc, xs + st * rows_tile * 32 + s_off * 32 + lane, cin + st * g.Wp, 0, g.Wp);
     __syncthreads();
   }
 
+  // transpose stage: ot[l][s]
+  T* ot = xs;
+#pragma unroll
+  for (int j = 0; j < R; ++j) ot[lane * (TS + 1) + s_off + j] = acc[0][j];
+  __syncthreads();
+
   // ---------------------------------- epilogue ----------------------------------
-  const long long base = (long long)b * e.bstride + (long long)p * g.len;
-  const bool prow_ok = p < nrow;
-  if (e.foldH > 0 && prow_ok) {  // adjoint fold corrections near the left / right edges
-    const int FH = e.foldH;
-    const int right0 = g.len - 2 * FH;  // column of slot 0 in the right-edge numbering
-    const T* fr = e.fold + ((long long)b * nrow + p) * (2 * FH);
+  // warp w handles output rows l = w, w+kNW, ..; lanes walk the row's TS outputs.
+  constexpr int NS = TS / 32;  // outputs per lane per row
+  double nrm[3] = {0.0, 0.0, 0.0};
+  bool bad = false;
+  const double vs = (MODE == EPI_POWER && e.vnw2) ? sqrt(e.vnw2[b]) : 1.0;
+  const int n = g.len;
+  for (int l = warp; l < 32; l += kNW) {
+    const int p = l0 + l;
+    if (p >= g.other) break;
+    const long long base = (long long)b * e.bstride + (long long)p * n + s0;
+    T v[NS];
 #pragma unroll
-    for (int j = 0; j < R; ++j) {
-      const int qq = s_first + j;
-      if (qq < FH) acc[j] += fr[qq];
-      else if (qq - right0 >= FH && qq < g.len) acc[j] += fr[qq - right0];
-    }
-  }
-  if constexpr (MODE == EPI_PLAIN || MODE == EPI_RESID) {
-    if constexpr (MODE == EPI_RESID) {
-      T bv[R];
-#pragma unroll
-      for (int j = 0; j < R; ++j) {
-        const int qq = s_first + j;
-        bv[j] = (prow_ok && qq < g.len) ? e.bsub[base + qq] : T(0);
-      }
-#pragma unroll
-      for (int j = 0; j < R; ++j) acc[j] = rn_sub<T>(acc[j], bv[j]);
-    }
-    if (prow_ok) {
-#pragma unroll
-      for (int j = 0; j < R; ++j) {
-        const int qq = s_first + j;
-        if (qq < g.len) e.out[base + qq] = acc[j];
+    for (int k = 0; k < NS; ++k) {
+      const int s = lane + 32 * k;
+      v[k] = ot[l * (TS + 1) + s];
+      if (e.foldH > 0) {  // exact-fold corrections near the left / right edges
+        const int q = s0 + s, FH = e.foldH;
+        const T* fr = e.fold + ((long long)b * g.other + p) * (2 * FH);
+        if (q < FH) v[k] += fr[q];
+        else if (q >= n - FH && q < n) v[k] += fr[q - (n - 2 * FH)];
       }
     }
-  } else if constexpr (MODE == EPI_UPDATE) {
-    const T Lt = (T)e.L[b];
-    const T dt = (T)e.denom[b];
-    const T bt = (T)e.beta;
-    bool bad = false;
-    double nrm[3] = {0.0, 0.0, 0.0};
-    T yv_[R], xp_[R];
+    if constexpr (MODE == EPI_PLAIN || MODE == EPI_RESID) {
+      T bv[NS];
 #pragma unroll
-    for (int j = 0; j < R; ++j) {  // issue every operand load before the first use
-      const int qq = s_first + j;
-      const bool ok = prow_ok && qq < g.len;
-      yv_[j] = ok ? e.y[base + qq] : T(0);
-      xp_[j] = ok ? e.x[base + qq] : T(0);
-    }
-    if (prow_ok) {
+      for (int k = 0; k < NS; ++k) {
+        const int s = lane + 32 * k;
+        bv[k] = (MODE == EPI_RESID && s0 + s < n) ? e.bsub[base + s] : T(0);
+      }
 #pragma unroll
-      for (int j = 0; j < R; ++j) {
-        const int qq = s_first + j;
-        if (qq < g.len) {
-          const T yv = yv_[j];
-          const T xp = xp_[j];
-          T xv = rn_div<T>(rn_sub<T>(rn_mul<T>(Lt, yv), acc[j]), dt);
+      for (int k = 0; k < NS; ++k) {
+        const int s = lane + 32 * k;
+        if (s0 + s < n) e.out[base + s] = (MODE == EPI_RESID) ? rn_sub<T>(v[k], bv[k]) : v[k];
+      }
+    } else if constexpr (MODE == EPI_UPDATE) {
+      const T Lt = (T)e.L[b], dt = (T)e.denom[b], bt = (T)e.beta;
+      T yv[NS], xp[NS];
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const int s = lane + 32 * k;
+        const bool ok = s0 + s < n;
+        yv[k] = ok ? e.y[base + s] : T(0);
+        xp[k] = ok ? e.x[base + s] : T(0);
+      }
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const int s = lane + 32 * k;
+        if (s0 + s < n) {
+          T xv = rn_div<T>(rn_sub<T>(rn_mul<T>(Lt, yv[k]), v[k]), dt);
           if (e.project) xv = (xv > T(0) || xv != xv) ? xv : T(0);
-          const T d = rn_sub<T>(xv, xp);
-          const T yn = rn_add<T>(xv, rn_mul<T>(bt, d));
-          e.x[base + qq] = xv;
-          e.y[base + qq] = yn;
+          const T d = rn_sub<T>(xv, xp[k]);
+          e.x[base + s] = xv;
+          e.y[base + s] = rn_add<T>(xv, rn_mul<T>(bt, d));
           bad |= !isfinite((double)xv);
           if (e.want_norms) {
             nrm[0] += (double)d * (double)d;
-            nrm[1] += (double)xp * (double)xp;
+            nrm[1] += (double)xp[k] * (double)xp[k];
             nrm[2] += (double)xv * (double)xv;
           }
         }
       }
-    }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(e.nonfinite, e.k);
-    if (e.want_norms) {
-      const int nblk = gridDim.x * gridDim.y;
-      kb_block_partials<3>(nrm, e.partials, b, nblk, blockIdx.y * gridDim.x + blockIdx.x);
-    }
-  } else {  // EPI_POWER
-    const double vs = e.vnw2 ? sqrt(e.vnw2[b]) : 1.0;
-    double pr[2] = {0.0, 0.0};
-    if (prow_ok) {
+    } else {  // EPI_POWER
+      T vi[NS];
 #pragma unroll
-      for (int j = 0; j < R; ++j) {
-        const int qq = s_first + j;
-        if (qq < g.len) {
-          const T w = acc[j];
-          T v = e.vin[base + qq];
-          if (e.vnw2) v = (T)((double)v / vs);
-          e.out[base + qq] = w;
-          pr[0] += (double)v * (double)w;
-          pr[1] += (double)w * (double)w;
+      for (int k = 0; k < NS; ++k) {
+        const int s = lane + 32 * k;
+        vi[k] = (s0 + s < n) ? e.vin[base + s] : T(0);
+      }
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const int s = lane + 32 * k;
+        if (s0 + s < n) {
+          const T w = v[k];
+          T vv = vi[k];
+          if (e.vnw2) vv = (T)((double)vv / vs);
+          e.out[base + s] = w;
+          nrm[0] += (double)vv * (double)w;
+          nrm[1] += (double)w * (double)w;
         }
       }
     }
-    const int nblk = gridDim.x * gridDim.y;
-    kb_block_partials<2>(pr, e.partials, b, nblk, blockIdx.y * gridDim.x + blockIdx.x);
+  }
+  if constexpr (MODE == EPI_UPDATE) {
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(e.nonfinite, e.k);
+    if (e.want_norms) {
+      double v3[3] = {nrm[0], nrm[1], nrm[2]};
+      kb_block_partials<3>(v3, e.partials, b, gridDim.x * gridDim.y, blockIdx.y * gridDim.x + blockIdx.x);
+    }
+  } else if constexpr (MODE == EPI_POWER) {
+    double v2[2] = {nrm[0], nrm[1]};
+    kb_block_partials<2>(v2, e.partials, b, gridDim.x * gridDim.y, blockIdx.y * gridDim.x + blockIdx.x);
   }
 }
 
