@@ -1,0 +1,169 @@
+"""Pin the CPU oracle (oracle/kronblur_port.py) to the reference's golden vectors.
+
+Fixtures in tests/golden/ were produced by running the reference package itself
+(tests/golden/make_golden.py). These tests need no GPU.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, hankel_loop, toeplitz_loop
+
+import paper_1901_00913_b200 as kb
+from oracle import kronblur_port as port
+
+
+def load(name):
+    return np.load(os.path.join(GOLDEN, name), allow_pickle=False)
+
+
+class F:  # minimal factor object for the port
+    def __init__(self, kind, c, j):
+        self.kind, self.c, self.j, self.n = kind, np.asarray(c, float), int(j), len(c)
+
+
+# ------------------------------------------------------------------ structured.py
+def test_worked_examples_exact():
+    g = load("structured.npz")
+    c = np.arange(1.0, 8.0)
+    assert np.array_equal(port.dense_toeplitz(c, 4), g["toep_c1to7_j4"])
+    assert np.array_equal(port.dense_hankel(c, 3), g["hank_c1to7_j3"])
+    assert g["toep_c1to7_j4"][0].tolist() == [4, 3, 2, 1, 0, 0, 0]
+    assert g["hank_c1to7_j3"][-1].tolist() == [0, 0, 0, 0, 0, 1, 2]
+
+
+def test_dense_layouts_match_reference_bit_exact():
+    g = load("structured.npz")
+    for i in range(12):
+        n, j = g[f"rand{i}_n_j"]
+        c = g[f"rand{i}_c"]
+        assert np.array_equal(port.dense_toeplitz(c, j), g[f"rand{i}_T"])
+        assert np.array_equal(port.dense_hankel(c, j), g[f"rand{i}_H"])
+        assert np.array_equal(port.dense_factor(F("toeplitz_plus_hankel", c, j)), g[f"rand{i}_TH"])
+        # and the package's own materialisation (host helper) agrees
+        assert np.array_equal(kb.factor_to_dense(kb.toep_plus_hank(c, j)), g[f"rand{i}_TH"])
+        assert np.array_equal(port.dense_toeplitz(c, j), toeplitz_loop(c, j))
+        assert np.array_equal(port.dense_hankel(c, j), hankel_loop(c, j))
+
+
+@pytest.mark.parametrize("kind", ["T", "H", "TH"])
+def test_fft_apply_matches_reference(kind):
+    g = load("structured.npz")
+    names = {"T": "toeplitz", "H": "hankel", "TH": "toeplitz_plus_hankel"}
+    for i in range(3):
+        n, j = g[f"fft{i}_n_j"]
+        plan = port.FactorPlan(F(names[kind], g[f"fft{i}_c"], j))
+        X = g[f"fft{i}_X"]
+        # same algorithm (circulant rfft embedding), same library: identical to rounding
+        np.testing.assert_allclose(port.factor_apply(plan, X), g[f"fft{i}_{kind}_FX"], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(port.factor_apply(plan, X, True), g[f"fft{i}_{kind}_FtX"], rtol=0, atol=1e-12)
+
+
+# ------------------------------------------------------------------ momentum
+def test_momentum_against_reference_and_60_digit_values():
+    g = load("momentum.npz")
+    t = 1.0
+    for k in range(300):
+        t = port.momentum_next(t)
+        assert t == g["t_ref"][k]
+        assert abs(t - g["t_decimal"][k]) <= 1e-13 * t
+    ts, beta = kb.momentum_table(300)
+    assert np.array_equal(ts[1:], g["t_ref"][:-1])
+    with pytest.raises(ValueError):
+        port.momentum_next(0.5)
+
+
+# ------------------------------------------------------------------ operator / solver
+def small_cases():
+    g = load("kron_small.npz")
+    ids = sorted({k.split("_")[0] for k in g.files})
+    return g, ids
+
+
+def op_from(g, pre):
+    make = kb.toep if str(g[pre + "kind"]) == "toeplitz" else kb.toep_plus_hank
+    terms = tuple(kb.KronTerm(sigma=float(s), H=make(a, int(g[pre + "H_j"])), K=make(b, int(g[pre + "K_j"])))
+                  for s, a, b in zip(g[pre + "sigma"], g[pre + "H_c"], g[pre + "K_c"]))
+    m = int(g[pre + "m_s"][0])
+    bc = kb.BoundaryCondition(str(g[pre + "bc"]))
+    return kb.KronOperator(terms=terms, shape=(m, m), bc=bc, sigma=g[pre + "sigma"], s=len(terms),
+                           rank=int(g[pre + "rank"]), eps=0.0)
+
+
+def test_port_apply_reproduces_reference_bit_for_bit():
+    g, ids = small_cases()
+    for cid in ids:
+        pre = cid + "_"
+        pop = port.PortOperator(op_from(g, pre))
+        assert np.array_equal(port.kron_apply(pop, g[pre + "X"]), g[pre + "AX"])
+        assert np.array_equal(port.kron_apply_adjoint(pop, g[pre + "X"]), g[pre + "AtX"])
+
+
+def test_port_lipschitz_and_solver_reproduce_reference():
+    g, ids = small_cases()
+    for cid in ids:
+        pre = cid + "_"
+        op = op_from(g, pre)
+        pop = port.PortOperator(op)
+        m = op.shape[0]
+        seed = int(cid[1:])
+        L = port.estimate_lipschitz(lambda V: port.kron_apply(pop, V),
+                                    lambda V: port.kron_apply_adjoint(pop, V), (m, m), 50, seed)
+        assert L == float(g[pre + "L_mat"])
+        Lv = port.estimate_lipschitz(
+            lambda v: kb.vec(port.kron_apply(pop, kb.unvec(v, m, m))),
+            lambda v: kb.vec(port.kron_apply_adjoint(pop, kb.unvec(v, m, m))), m * m, 50, seed)
+        assert Lv == float(g[pre + "L_vec"])
+        x, _ = port.sfista(pop, g[pre + "B"], float(g[pre + "L_mat"]), 0.05, 40, project=False)
+        assert np.array_equal(x, g[pre + "x_sfista"])
+        xp, _ = port.sfista(pop, g[pre + "B"], float(g[pre + "L_mat"]), 0.05, 40, project=True)
+        assert np.array_equal(xp, g[pre + "x_proj"])
+        assert np.all(xp >= 0)
+
+
+def test_untruncated_reference_apply_is_direct_blur():
+    g, ids = small_cases()
+    for cid in ids:
+        pre = cid + "_"
+        if pre + "blur" in g.files:
+            np.testing.assert_allclose(g[pre + "Afull_X"], g[pre + "blur"], rtol=0,
+                                       atol=1e-10 * np.abs(g[pre + "blur"]).max())
+
+
+def test_cfg1_golden_solution_reproduced_by_port():
+    g = load("cfg1.npz")
+    op = kb.KronOperator(
+        terms=tuple(kb.KronTerm(sigma=float(s), H=kb.toep(a, int(g["H_j"])), K=kb.toep(b, int(g["K_j"])))
+                    for s, a, b in zip(g["sigma"], g["H_c"], g["K_c"])),
+        shape=(256, 256), bc=kb.BoundaryCondition.ZERO, sigma=g["sigma"], s=3, rank=int(g["rank"]), eps=0.0)
+    x, _ = port.sfista(op, g["B"], float(g["L"]), 0.02, 100, project=True)
+    assert np.array_equal(x, g["x_proj"])
+
+
+# ------------------------------------------------------------------ host setup (decompose)
+@pytest.mark.parametrize("cid", ["c0", "c1", "c2", "c3", "c4", "c5"])
+def test_support_block_decompose_matches_reference(cid):
+    g = load("kron_small.npz")
+    pre = cid + "_"
+    m, s = (int(v) for v in g[pre + "m_s"])
+    psf = kb.Psf(g[pre + "psf"], tuple(int(v) for v in g[pre + "center"]))
+    op = kb.decompose(psf, kb.BoundaryCondition(str(g[pre + "bc"])), s=s, shape=(m, m))
+    sig = g[pre + "sigma"]
+    np.testing.assert_allclose(op.sigma[:s], sig[:s], rtol=0, atol=1e-13 * sig[0])
+    assert op.rank == int(g[pre + "rank"])
+    for i, t in enumerate(op.terms):
+        a, b = g[pre + "H_c"][i], g[pre + "K_c"][i]
+        mag = np.abs(a)
+        sgn = np.sign(a[np.argmax(mag > 1e-3 * mag.max())])  # SURVEY F11 sign rule
+        assert t.H.j == int(g[pre + "H_j"]) and t.K.j == int(g[pre + "K_j"])
+        np.testing.assert_allclose(t.H.c, sgn * a, rtol=0, atol=1e-10 * mag.max())
+        np.testing.assert_allclose(t.K.c, sgn * b, rtol=0, atol=1e-10 * np.abs(b).max())
+    # the operator (outer products) matches even where individual signs could differ
+    pop_ref = port.PortOperator(op_from(g, pre))
+    pop = port.PortOperator(op)
+    X = g[pre + "X"]
+    np.testing.assert_allclose(port.kron_apply(pop, X), g[pre + "AX"], rtol=0,
+                               atol=1e-11 * np.abs(g[pre + "AX"]).max())
+    assert np.array_equal(port.kron_apply(pop_ref, X), g[pre + "AX"])
