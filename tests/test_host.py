@@ -222,3 +222,19 @@ def test_blur_exact_matches_loop_oracle(rng):
     for bc in ("zero", "reflective"):
         got = workloads.blur_exact(torch.from_numpy(X), psf, bc).numpy()
         np.testing.assert_allclose(got, blur_loop(psf.values, psf.center, X, bc), rtol=0, atol=1e-12)
+
+
+def test_install_patches_every_by_name_binding(monkeypatch):
+    kronblur = pytest.importorskip("kronblur")  # the reference, when importable (build container)
+    from kronblur import pipeline, solvers
+
+    orig = (solvers.sfista, pipeline.sfista, pipeline.estimate_lipschitz, pipeline.kron_apply)
+    undo = kb.install(kronblur)
+    try:
+        assert solvers.sfista is not orig[0] and pipeline.sfista is solvers.sfista
+        assert pipeline.estimate_lipschitz is kb.estimate_lipschitz
+        assert pipeline.kron_apply is kb.kron_apply and solvers.kron_apply is kb.kron_apply
+        assert kronblur.kron_apply_adjoint is kb.kron_apply_adjoint
+    finally:
+        undo()
+    assert (solvers.sfista, pipeline.sfista, pipeline.estimate_lipschitz, pipeline.kron_apply) == orig
