@@ -18,6 +18,7 @@
 
 #include "../../include/kronblur_b200.h"
 #include "kb_kernels.cuh"
+#include "kb_dmma.cuh"
 
 namespace {
 
@@ -173,15 +174,37 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
   const long long z_ps = (long long)g.len * g.other;
   const long long z_bs = z_ps * op->r;
   const long long t_bs = (long long)op->r * g.Wp;
-  if constexpr (sizeof(T) == 8)
-    return launch_a_g<T, kGmaxF64>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
-  else
+  if constexpr (sizeof(T) == 8) {
+    constexpr int TS = kb::kNW * 8;
+    const size_t smem = sizeof(double) * ((size_t)kb::dmma_rows(TS, g.Wp) * kb::kXS +
+                                          (size_t)kGmaxF64 * kb::dmma_cstride_split(g.Wp) + 32 * (TS + 1));
+    auto kern = kb::kb_pass_split_dmma<kGmaxF64>;
+    KB_TRY(allow_smem(kern, smem));
+    dim3 grid((g.other + 31) / 32, (g.len + TS - 1) / TS, op->batch);
+    kern<<<grid, dim3(32, kb::kNW), smem, s>>>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2);
+    KB_CUDA(cudaGetLastError());
+    return KB_OK;
+  } else {
     return launch_a_g<T, kGmaxF32>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
+  }
 }
 
 template <typename T, int MODE>
 int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g, const T* tsign,
              const kb::Epi<T>& e, cudaStream_t s) {
+  if constexpr (sizeof(T) == 8) {
+    constexpr int TS = kb::kNW * 16;
+    const size_t smem = sizeof(double) * (2 * (size_t)kb::dmma_rows(TS, g.Wp) * kb::kXS +
+                                          2 * (size_t)kb::dmma_cstride_sum(g.Wp));
+    auto kern = kb::kb_pass_sum_dmma<MODE>;
+    KB_TRY(allow_smem(kern, smem));
+    const long long z_ps = (long long)g.len * g.other;
+    dim3 grid((g.other + 31) / 32, (g.len + TS - 1) / TS, op->batch);
+    kern<<<grid, dim3(32, kb::kNW), smem, s>>>(z, z_ps, z_ps * op->r, op->r, tin,
+                                               (long long)op->r * g.Wp, g, tsign, e);
+    KB_CUDA(cudaGetLastError());
+    return KB_OK;
+  }
   constexpr int TS = kb::kNW * kRB;
   const size_t smem = sizeof(T) * (2 * (size_t)(TS + g.Wp) * 32 + 2 * (size_t)g.Wp);
   auto kern = kb::kb_pass_sum<T, kRB, MODE>;

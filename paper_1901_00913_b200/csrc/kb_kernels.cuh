@@ -157,7 +157,7 @@ __device__ __forceinline__ void kb_taps(T (&acc)[G][R], const T* __restrict__ x,
 // Fill rows [0, rows) of a [rows][32] tile with input rows S = row_lo + rr (global), lanes
 // over L = l0 + lane. In-domain rows stream in with cp.async; out-of-domain rows are folded
 // (times `sign`) when g.fill, else zero.
-template <typename T>
+template <typename T, int XS = 32>
 __device__ __forceinline__ void kb_fill_tile(T* __restrict__ xs, const T* __restrict__ in,
                                              const AxisGeom& g, int row_lo, int rows, int l,
                                              int warp, int lane, int sign) {
@@ -166,7 +166,7 @@ __device__ __forceinline__ void kb_fill_tile(T* __restrict__ xs, const T* __rest
     const bool outside = gr < 0 || gr >= g.Mg;
     if (g.fill && outside) gr = kb_fold(gr, g.Mg);
     const int lr = gr - g.g0;
-    T* d = xs + rr * 32 + lane;
+    T* d = xs + rr * XS + lane;
     const bool ok = l < g.other && gr >= 0 && gr < g.Mg && lr >= -g.halo_lo && lr < g.len + g.halo_hi;
     if (ok && !outside) cp_async_elem<T>(d, in + (long long)lr * g.other + l);
     else *d = ok ? (sign < 0 ? -in[(long long)lr * g.other + l] : in[(long long)lr * g.other + l]) : T(0);
@@ -370,65 +370,11 @@ __device__ __forceinline__ void kb_block_partials(double (&v)[NQ], double* parti
   }
 }
 
-// ------------------------------------------------------------------------------------------
-// pass B (sum): Y[l][s] = sum_i sum_k c_i[k] Z_i^T[s - H + k][l], with the fused epilogue.
-//   Same CTA geometry as the split pass (TS = kNW*R along S, 32 along L); term tiles are double
-//   buffered with cp.async; the result is transposed through shared memory so the epilogue
-//   reads and writes [L][S] = [m][n] rows coalesced.
-// ------------------------------------------------------------------------------------------
-template <typename T, int R, int MODE>
-__global__ void __launch_bounds__(32 * kNW, 2)
-kb_pass_sum(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
-            const T* __restrict__ tin, long long t_bs, AxisGeom g, const T* __restrict__ tsign,
-            Epi<T> e) {
-  extern __shared__ __align__(16) unsigned char kb_smem_b[];
-  constexpr int TS = kNW * R;
-  const int rows_tile = TS + g.Wp;
-  T* xs = reinterpret_cast<T*>(kb_smem_b);   // [2][rows_tile][32]; reused as [32][TS+1] at the end
-  T* cin = xs + 2 * rows_tile * 32;          // [2][Wp]
-  const int lane = threadIdx.x, warp = threadIdx.y;
-  const int tid = warp * 32 + lane;
-  const int b = blockIdx.z;
-  const int s0 = blockIdx.y * TS;
-  const int l0 = blockIdx.x * 32;
-  z += b * z_bs;
-  tin += b * t_bs;
-  const int row_lo = g.g0 + s0 - g.H;
-
-  auto load_term = [&](int i, int stage) {
-    const int sgn = tsign ? (tsign[(long long)b * r + i] < T(0) ? -1 : 1) : 1;
-    kb_fill_tile<T>(xs + stage * rows_tile * 32, z + (long long)i * z_ps, g, row_lo, rows_tile,
-                    l0 + lane, warp, lane, sgn);
-    for (int k = tid; k < g.Wp; k += 32 * kNW) cin[stage * g.Wp + k] = tin[(long long)i * g.Wp + k];
-    cp_async_commit();
-  };
-
-  T acc[1][R];
-#pragma unroll
-  for (int j = 0; j < R; ++j) acc[0][j] = T(0);
-  const int s_off = warp * R;
-
-  load_term(0, 0);
-  for (int i = 0; i < r; ++i) {
-    const int st = i & 1;
-    if (i + 1 < r) {
-      load_term(i + 1, st ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    kb_taps<T, 1, R>(acc, xs + st * rows_tile * 32 + s_off * 32 + lane, cin + st * g.Wp, 0, g.Wp);
-    __syncthreads();
-  }
-
-  // transpose stage: ot[l][s]
-  T* ot = xs;
-#pragma unroll
-  for (int j = 0; j < R; ++j) ot[lane * (TS + 1) + s_off + j] = acc[0][j];
-  __syncthreads();
-
-  // ---------------------------------- epilogue ----------------------------------
+// Fused epilogue of the sum pass: ot[l*(TS+1) + s] holds the block's [32 L][TS S] results.
+template <typename T, int MODE, int TS>
+__device__ __forceinline__ void kb_sum_epilogue(const T* __restrict__ ot, const AxisGeom& g,
+                                                const Epi<T>& e, int b, int s0, int l0, int warp,
+                                                int lane) {
   // warp w handles output rows l = w, w+kNW, ..; lanes walk the row's TS outputs.
   constexpr int NS = TS / 32;  // outputs per lane per row
   double nrm[3] = {0.0, 0.0, 0.0};
@@ -521,6 +467,68 @@ kb_pass_sum(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
     double v2[2] = {nrm[0], nrm[1]};
     kb_block_partials<2>(v2, e.partials, b, gridDim.x * gridDim.y, blockIdx.y * gridDim.x + blockIdx.x);
   }
+}
+
+// ------------------------------------------------------------------------------------------
+// pass B (sum): Y[l][s] = sum_i sum_k c_i[k] Z_i^T[s - H + k][l], with the fused epilogue.
+//   Same CTA geometry as the split pass (TS = kNW*R along S, 32 along L); term tiles are double
+//   buffered with cp.async; the result is transposed through shared memory so the epilogue
+//   reads and writes [L][S] = [m][n] rows coalesced.
+// ------------------------------------------------------------------------------------------
+template <typename T, int R, int MODE>
+__global__ void __launch_bounds__(32 * kNW, 2)
+kb_pass_sum(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
+            const T* __restrict__ tin, long long t_bs, AxisGeom g, const T* __restrict__ tsign,
+            Epi<T> e) {
+  extern __shared__ __align__(16) unsigned char kb_smem_b[];
+  constexpr int TS = kNW * R;
+  const int rows_tile = TS + g.Wp;
+  T* xs = reinterpret_cast<T*>(kb_smem_b);   // [2][rows_tile][32]; reused as [32][TS+1] at the end
+  T* cin = xs + 2 * rows_tile * 32;          // [2][Wp]
+  const int lane = threadIdx.x, warp = threadIdx.y;
+  const int tid = warp * 32 + lane;
+  const int b = blockIdx.z;
+  const int s0 = blockIdx.y * TS;
+  const int l0 = blockIdx.x * 32;
+  z += b * z_bs;
+  tin += b * t_bs;
+  const int row_lo = g.g0 + s0 - g.H;
+
+  auto load_term = [&](int i, int stage) {
+    const int sgn = tsign ? (tsign[(long long)b * r + i] < T(0) ? -1 : 1) : 1;
+    kb_fill_tile<T>(xs + stage * rows_tile * 32, z + (long long)i * z_ps, g, row_lo, rows_tile,
+                    l0 + lane, warp, lane, sgn);
+    for (int k = tid; k < g.Wp; k += 32 * kNW) cin[stage * g.Wp + k] = tin[(long long)i * g.Wp + k];
+    cp_async_commit();
+  };
+
+  T acc[1][R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) acc[0][j] = T(0);
+  const int s_off = warp * R;
+
+  load_term(0, 0);
+  for (int i = 0; i < r; ++i) {
+    const int st = i & 1;
+    if (i + 1 < r) {
+      load_term(i + 1, st ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    kb_taps<T, 1, R>(acc, xs + st * rows_tile * 32 + s_off * 32 + lane, cin + st * g.Wp, 0, g.Wp);
+    __syncthreads();
+  }
+
+  // transpose stage: ot[l][s]
+  T* ot = xs;
+#pragma unroll
+  for (int j = 0; j < R; ++j) ot[lane * (TS + 1) + s_off + j] = acc[0][j];
+  __syncthreads();
+
+  // ---------------------------------- epilogue ----------------------------------
+  kb_sum_epilogue<T, MODE, TS>(ot, g, e, b, s0, l0, warp, lane);
 }
 
 // final deterministic reduction: out[q*qstride + b*bstride] = sum_blk partials[b][blk][q]
