@@ -88,7 +88,24 @@ struct Work {
   size_t bytes;
 };
 
-int pass_b_blocks(const kb_op* op) {  // blocks of the sum pass (one partial each)
+// Resident blocks for the persistent fp64 kernels: two per SM.
+int persistent_blocks() {
+  static int nb = 0;
+  if (!nb) {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    nb = 2 * sms;
+  }
+  return nb;
+}
+
+// Blocks of the sum pass (one norm partial per block and image).
+int sum_blocks(const kb_op* op) {
+  if (op->dtype == KB_F64) {
+    int parts, nb;
+    kb::plan_items(op->n, (op->m + 31) / 32, op->batch, persistent_blocks(), parts, nb);
+    return nb;
+  }
   const int TS = kb::kNW * kRB;
   return ((op->n + TS - 1) / TS) * ((op->m + 31) / 32);
 }
@@ -105,7 +122,7 @@ Work layout(const kb_op* op, void* base) {
   w.fold = b ? b + off : nullptr;
   off = align_up(off + elem(op) * (size_t)op->batch * op->m * 2 * std::max(op->Hb, 1), 256);
   w.partials = b ? reinterpret_cast<double*>(b + off) : nullptr;
-  off = align_up(off + sizeof(double) * 4 * (size_t)op->batch * pass_b_blocks(op), 256);
+  off = align_up(off + sizeof(double) * 4 * (size_t)op->batch * sum_blocks(op), 256);
   w.scal = b ? reinterpret_cast<double*>(b + off) : nullptr;
   off = align_up(off + sizeof(double) * 4 * (size_t)op->batch, 256);
   w.bytes = off;
@@ -176,12 +193,14 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
   const long long t_bs = (long long)op->r * g.Wp;
   if constexpr (sizeof(T) == 8) {
     constexpr int TS = kb::kNW * 8;
-    const size_t smem = sizeof(double) * ((size_t)kb::dmma_rows(TS, g.Wp) * kb::kXS +
-                                          (size_t)kGmaxF64 * kb::dmma_cstride_split(g.Wp) + 32 * (TS + 1));
+    const size_t smem = sizeof(double) * (2 * (size_t)kb::dmma_rows(TS, g.Wp) * kb::kXS +
+                                          (size_t)op->r * kb::dmma_cstride_split(g.Wp) + 32 * (TS + 1));
     auto kern = kb::kb_pass_split_dmma<kGmaxF64>;
     KB_TRY(allow_smem(kern, smem));
-    dim3 grid((g.other + 31) / 32, (g.len + TS - 1) / TS, op->batch);
-    kern<<<grid, dim3(32, kb::kNW), smem, s>>>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2);
+    int parts, nb;
+    kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
+    kern<<<nb, dim3(32, kb::kNW), smem, s>>>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2,
+                                             op->r, op->batch, parts);
     KB_CUDA(cudaGetLastError());
     return KB_OK;
   } else {
@@ -193,15 +212,17 @@ template <typename T, int MODE>
 int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g, const T* tsign,
              const kb::Epi<T>& e, cudaStream_t s) {
   if constexpr (sizeof(T) == 8) {
-    constexpr int TS = kb::kNW * 16;
-    const size_t smem = sizeof(double) * (2 * (size_t)kb::dmma_rows(TS, g.Wp) * kb::kXS +
+    const size_t smem = sizeof(double) * (2 * (size_t)kb::dmma_rows(kb::kNW * 16, g.Wp) * kb::kXS +
                                           2 * (size_t)kb::dmma_cstride_sum(g.Wp));
     auto kern = kb::kb_pass_sum_dmma<MODE>;
     KB_TRY(allow_smem(kern, smem));
     const long long z_ps = (long long)g.len * g.other;
-    dim3 grid((g.other + 31) / 32, (g.len + TS - 1) / TS, op->batch);
-    kern<<<grid, dim3(32, kb::kNW), smem, s>>>(z, z_ps, z_ps * op->r, op->r, tin,
-                                               (long long)op->r * g.Wp, g, tsign, e);
+    int parts, nb;
+    kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
+    if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // blocks skip untouched images
+      KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb, s));
+    kern<<<nb, dim3(32, kb::kNW), smem, s>>>(z, z_ps, z_ps * op->r, op->r, tin,
+                                             (long long)op->r * g.Wp, g, tsign, e, op->batch, parts);
     KB_CUDA(cudaGetLastError());
     return KB_OK;
   }
@@ -347,7 +368,7 @@ int update_t(const kb_op* op, const T* R, T* X, T* Y, const Work& w, const RowBl
   KB_TRY((stage_b<T, kb::EPI_UPDATE>(op, 1, update_epi<T>(op, X, Y, w, beta, k, Ldev, ddev, project,
                                                           nonfinite, norms_out != nullptr), w, s)));
   if (norms_out) {
-    kb::kb_reduce_partials<<<op->batch, 256, 0, s>>>(w.partials, pass_b_blocks(op), 3, norms_out,
+    kb::kb_reduce_partials<<<op->batch, 256, 0, s>>>(w.partials, sum_blocks(op), 3, norms_out,
                                                       op->batch, 1);
     KB_CUDA(cudaGetLastError());
   }
@@ -389,7 +410,7 @@ int power_t(const kb_op* op, T* v, T* wbuf, const Work& w, int iters, double* hi
     e2.vnw2 = nw2;
     e2.partials = w.partials;
     KB_TRY((stage_b<T, kb::EPI_POWER>(op, 1, e2, w, s)));
-    kb::kb_reduce_partials<<<op->batch, 256, 0, s>>>(w.partials, pass_b_blocks(op), 2,
+    kb::kb_reduce_partials<<<op->batch, 256, 0, s>>>(w.partials, sum_blocks(op), 2,
                                                       hist + (size_t)k * 2 * op->batch,
                                                       op->batch, 1);
     KB_CUDA(cudaGetLastError());

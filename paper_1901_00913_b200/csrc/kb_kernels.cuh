@@ -371,30 +371,30 @@ __device__ __forceinline__ void kb_block_partials(double (&v)[NQ], double* parti
 }
 
 // Fused epilogue of the sum pass: ot[l*(TS+1) + s] holds the block's [32 L][TS S] results.
+// Outputs with S index in [s0, s_end) are written; per-thread norm partials and the
+// non-finite flag accumulate in nrm / bad (reduced by kb_sum_finish).
 template <typename T, int MODE, int TS>
 __device__ __forceinline__ void kb_sum_epilogue(const T* __restrict__ ot, const AxisGeom& g,
-                                                const Epi<T>& e, int b, int s0, int l0, int warp,
-                                                int lane) {
+                                                const Epi<T>& e, int b, int s0, int s_end, int l0,
+                                                int warp, int lane, double (&nrm)[3], bool& bad) {
   // warp w handles output rows l = w, w+kNW, ..; lanes walk the row's TS outputs.
   constexpr int NS = TS / 32;  // outputs per lane per row
-  double nrm[3] = {0.0, 0.0, 0.0};
-  bool bad = false;
   const double vs = (MODE == EPI_POWER && e.vnw2) ? sqrt(e.vnw2[b]) : 1.0;
-  const int n = g.len;
+  const int n = s_end;
   for (int l = warp; l < 32; l += kNW) {
     const int p = l0 + l;
     if (p >= g.other) break;
-    const long long base = (long long)b * e.bstride + (long long)p * n + s0;
+    const long long base = (long long)b * e.bstride + (long long)p * g.len + s0;
     T v[NS];
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
       const int s = lane + 32 * k;
       v[k] = ot[l * (TS + 1) + s];
       if (e.foldH > 0) {  // exact-fold corrections near the left / right edges
-        const int q = s0 + s, FH = e.foldH;
+        const int q = s0 + s, FH = e.foldH, N = g.len;
         const T* fr = e.fold + ((long long)b * g.other + p) * (2 * FH);
         if (q < FH) v[k] += fr[q];
-        else if (q >= n - FH && q < n) v[k] += fr[q - (n - 2 * FH)];
+        else if (q >= N - FH && q < N) v[k] += fr[q - (N - 2 * FH)];
       }
     }
     if constexpr (MODE == EPI_PLAIN || MODE == EPI_RESID) {
@@ -457,15 +457,18 @@ __device__ __forceinline__ void kb_sum_epilogue(const T* __restrict__ ot, const 
       }
     }
   }
+}
+
+// Block-level end of the sum pass: non-finite flag and deterministic norm partials.
+template <typename T, int MODE>
+__device__ __forceinline__ void kb_sum_finish(const Epi<T>& e, double (&nrm)[3], bool bad, int b,
+                                              int nblk, int blk, int lane) {
   if constexpr (MODE == EPI_UPDATE) {
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(e.nonfinite, e.k);
-    if (e.want_norms) {
-      double v3[3] = {nrm[0], nrm[1], nrm[2]};
-      kb_block_partials<3>(v3, e.partials, b, gridDim.x * gridDim.y, blockIdx.y * gridDim.x + blockIdx.x);
-    }
+    if (e.want_norms) kb_block_partials<3>(nrm, e.partials, b, nblk, blk);
   } else if constexpr (MODE == EPI_POWER) {
     double v2[2] = {nrm[0], nrm[1]};
-    kb_block_partials<2>(v2, e.partials, b, gridDim.x * gridDim.y, blockIdx.y * gridDim.x + blockIdx.x);
+    kb_block_partials<2>(v2, e.partials, b, nblk, blk);
   }
 }
 
@@ -528,7 +531,10 @@ kb_pass_sum(const T* __restrict__ z, long long z_ps, long long z_bs, int r,
   __syncthreads();
 
   // ---------------------------------- epilogue ----------------------------------
-  kb_sum_epilogue<T, MODE, TS>(ot, g, e, b, s0, l0, warp, lane);
+  double nrm[3] = {0.0, 0.0, 0.0};
+  bool bad = false;
+  kb_sum_epilogue<T, MODE, TS>(ot, g, e, b, s0, g.len, l0, warp, lane, nrm, bad);
+  kb_sum_finish<T, MODE>(e, nrm, bad, b, gridDim.x * gridDim.y, blockIdx.y * gridDim.x + blockIdx.x, lane);
 }
 
 // final deterministic reduction: out[q*qstride + b*bstride] = sum_blk partials[b][blk][q]

@@ -52,6 +52,97 @@ __global__ void dmma_k(double* out, int iters) {
   if (s == -1.2345) out[0] = s;
 }
 
+// DMMA with distinct A/B registers per MMA (8 accumulators, 4 A x 2 B operands)
+__global__ void dmma2_k(double* out, int iters) {
+  double a[4], b[2];
+  for (int i = 0; i < 4; ++i) a[i] = threadIdx.x * 1e-3 + i;
+  for (int i = 0; i < 2; ++i) b[i] = threadIdx.x * 2e-3 - i;
+  double c[8][2];
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a[i & 3]), "d"(b[i >> 2]));
+  }
+  double s = 0;
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == -1.2345) out[0] = s;
+}
+
+// DMMA fed from shared memory every iteration (the banded-pass pattern)
+__global__ void dmma_smem_k(double* out, int iters) {
+  __shared__ double sm[64 * 36];
+  for (int i = threadIdx.x; i < 64 * 36; i += blockDim.x) sm[i] = i * 1e-4;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  double c[16][2];
+  for (int i = 0; i < 16; ++i) c[i][0] = c[i][1] = 0;
+  for (int it = 0; it < iters; ++it) {
+    const int base = (it & 7) * 4;
+    double A[4], B[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) A[g] = sm[(base + g) * 36 + (lane & 3)];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) B[j] = sm[(base + (lane & 3)) * 36 + 8 * j + (lane >> 2)];
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[g * 4 + j][0]), "+d"(c[g * 4 + j][1]) : "d"(A[g]), "d"(B[j]));
+  }
+  double s = 0;
+  for (int i = 0; i < 16; ++i) s += c[i][0] + c[i][1];
+  if (s == -1.2345) out[0] = s;
+}
+
+// DFMA with 3 distinct registers and changing multiplicands
+__global__ void dfma3_k(double* out, int iters, double a) {
+  double x[8], y[8];
+  for (int i = 0; i < 8; ++i) { x[i] = threadIdx.x + i; y[i] = a + i * 1e-3; }
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = fma(y[i], x[(i + 1) & 7], x[i]);
+  double s = 0;
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == -1.2345) out[0] = s;
+}
+
+// the split-pass inner loop alone: tile [128][36] in smem, G=4 terms x 4 n-tiles, 18 chunks
+__global__ void __launch_bounds__(256, 2) dmma_split_k(double* out, int reps) {
+  __shared__ double xs[136 * 36];
+  __shared__ double cp[4 * 96];
+  for (int i = threadIdx.x; i < 136 * 36; i += 256) xs[i] = i * 1e-5;
+  for (int i = threadIdx.x; i < 4 * 96; i += 256) cp[i] = i * 1e-3;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ar = lane >> 2, ac = lane & 3;
+  double D[4][4][2] = {};
+  const double* xb = xs + (warp * 8 + ac) * 36 + ar;
+  const double* cb = cp + 8 + ac - ar;
+  for (int rep = 0; rep < reps; ++rep) {
+#pragma unroll 2
+    for (int c = 0; c < 18; ++c) {
+      double A[4], B[4];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) A[g] = cb[g * 96 + 4 * c];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) B[j] = xb[4 * c * 36 + 8 * j];
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(D[g][j][0]), "+d"(D[g][j][1]) : "d"(A[g]), "d"(B[j]));
+    }
+  }
+  double s = 0;
+  for (int g = 0; g < 4; ++g)
+    for (int j = 0; j < 4; ++j) s += D[g][j][0] + D[g][j][1];
+  if (s == -1.2345) out[0] = s;
+}
+
 template <typename K, typename... A>
 float timeit(K k, int blocks, int threads, A... a) {
   cudaEvent_t e0, e1;
@@ -85,6 +176,17 @@ int main() {
     ms = timeit(dmma_k, blocks, tpb, dout, it / 4);
     // per warp per mma: 8*8*4 = 256 FMA
     printf("DMMA  tpb=%d  %.2f TFLOP/s\n", tpb, 2.0 * 256 * 4 * (it / 4) * (double)blocks * (tpb / 32) / ms / 1e9);
+    ms = timeit(dmma2_k, blocks, tpb, dout, it / 8);
+    printf("DMMA2 tpb=%d  %.2f TFLOP/s\n", tpb, 2.0 * 256 * 8 * (it / 8) * (double)blocks * (tpb / 32) / ms / 1e9);
+    ms = timeit(dmma_smem_k, blocks, tpb, dout, it / 16);
+    printf("DMMAs tpb=%d  %.2f TFLOP/s\n", tpb, 2.0 * 256 * 16 * (it / 16) * (double)blocks * (tpb / 32) / ms / 1e9);
+    ms = timeit(dfma3_k, blocks, tpb, dout, it, 0.999);
+    printf("DFMA3 tpb=%d  %.2f TFLOP/s\n", tpb, 2.0 * 8 * it * (double)blocks * tpb / ms / 1e9);
+  }
+  {
+    const int reps = 200;
+    float ms = timeit(dmma_split_k, sms * 2, 256, dout, reps);
+    printf("DMMA split-loop 16 warps/SM  %.2f TFLOP/s\n", 2.0 * 256 * 16 * 18 * reps * (double)sms * 2 * 8 / ms / 1e9);
   }
   return 0;
 }
