@@ -99,12 +99,13 @@ int persistent_blocks() {
   return nb;
 }
 
-// Blocks of the sum pass (one norm partial per block and image).
+// Norm partial slots of the sum pass per image: one per warp (fp64 persistent kernel) or
+// one per block (fp32).
 int sum_blocks(const kb_op* op) {
   if (op->dtype == KB_F64) {
     int parts, nb;
     kb::plan_items(op->n, (op->m + 31) / 32, op->batch, persistent_blocks(), parts, nb);
-    return nb;
+    return nb * kb::kNW;
   }
   const int TS = kb::kNW * kRB;
   return ((op->n + TS - 1) / TS) * ((op->m + 31) / 32);
@@ -193,8 +194,8 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
   const long long t_bs = (long long)op->r * g.Wp;
   if constexpr (sizeof(T) == 8) {
     constexpr int TS = kb::kNW * 8;
-    const size_t smem = sizeof(double) * (2 * (size_t)kb::dmma_rows(TS, g.Wp) * kb::kXS +
-                                          (size_t)op->r * kb::dmma_cstride_split(g.Wp) + 32 * (TS + 1));
+    const size_t smem = sizeof(double) * ((size_t)kb::kStages * kb::dmma_rows(TS, g.Wp) * kb::kXS +
+                                          (size_t)op->r * kb::dmma_cstride_split(g.Wp));
     auto kern = kb::kb_pass_split_dmma<kGmaxF64>;
     KB_TRY(allow_smem(kern, smem));
     int parts, nb;
@@ -212,15 +213,15 @@ template <typename T, int MODE>
 int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g, const T* tsign,
              const kb::Epi<T>& e, cudaStream_t s) {
   if constexpr (sizeof(T) == 8) {
-    const size_t smem = sizeof(double) * (2 * (size_t)kb::dmma_rows(kb::kNW * 16, g.Wp) * kb::kXS +
-                                          2 * (size_t)kb::dmma_cstride_sum(g.Wp));
+    const size_t smem = sizeof(double) * ((size_t)kb::kStages * kb::dmma_rows(kb::kNW * 16, g.Wp) * kb::kXS +
+                                          (size_t)op->r * kb::dmma_cstride_sum(g.Wp));
     auto kern = kb::kb_pass_sum_dmma<MODE>;
     KB_TRY(allow_smem(kern, smem));
     const long long z_ps = (long long)g.len * g.other;
     int parts, nb;
     kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
-    if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // blocks skip untouched images
-      KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb, s));
+    if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // warps skip untouched images
+      KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kNW, s));
     kern<<<nb, dim3(32, kb::kNW), smem, s>>>(z, z_ps, z_ps * op->r, op->r, tin,
                                              (long long)op->r * g.Wp, g, tsign, e, op->batch, parts);
     KB_CUDA(cudaGetLastError());

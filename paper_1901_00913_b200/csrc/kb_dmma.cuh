@@ -2,8 +2,7 @@
 //
 // sm_100a has no f64 kind of tcgen05.mma; its FP64 tensor path is the warp-level
 // DMMA, measured at 37 TF/s on the box (DFMA: 34 TF/s, tools/microbench.cu). One DMMA is 256
-// FMAs and its operands are single registers, so the issue and register budget that limit the
-// DFMA loops (kb_taps) mostly disappear.
+// FMAs and its operands are single registers.
 //
 // A banded pass out[s] = sum_k c[k] x[s + k] over an 8-row output block is the product
 //     Out(8 x 8 cols) = T(8 x (Wp+7)) * X((Wp+7) x 8 cols),   T[s][t] = c[t - s],
@@ -11,6 +10,16 @@
 // (read from a zero-guarded copy of the taps), the B fragment is 4 input rows of the tile.
 // The structural overhead is (Wp+7)/Wp (11% at Wp = 64). Fragment layouts (m8n8k4.f64):
 //   A: lane holds A[lane/4][lane%4];  B: B[lane%4][lane/4];  C: C[lane/4][2*(lane%4) + i].
+//
+// Both kernels are persistent (balanced (image, L-tile, S-part) work items, one block per
+// SM slot) and stream their input tiles through a shared-memory ring synchronised with
+// mbarriers, not block barriers: every thread issues its share of a tile as cp.async and arms
+// the stage's "full" barrier with cp.async.mbarrier.arrive; every warp releases a stage on its
+// "empty" barrier once its MMAs have read it. Warps therefore drift within the ring, and one
+// warp's epilogue (straight from its accumulators to global memory) overlaps the other warps'
+// MMAs. Out-of-domain tile rows are cp.async'd from their folded source row (or zero-filled);
+// the (anti)symmetric adjoint's fill sign is applied to the A fragment of those rows, so tiles
+// are never rewritten in shared memory.
 #pragma once
 #include "kb_kernels.cuh"
 
@@ -19,6 +28,7 @@ namespace kb {
 constexpr int kXS = 36;    // tile row stride (doubles): the 16 B-fragment addresses of a
                            // half-warp, rows r0..r0+3 x cols c0..c0+3, hit 16 distinct bank pairs
 constexpr int kCG = 8;     // zero guard on each side of the tap copies
+constexpr int kStages = 2; // tile ring depth
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -26,9 +36,35 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
                : "d"(a), "d"(b));
 }
 
+// ---- mbarrier / cp.async helpers ---------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// arrive on `bar` once every cp.async this thread issued so far has landed
+__device__ __forceinline__ void cp_async_arrive(unsigned long long* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+// 8-byte cp.async; src_bytes = 0 zero-fills the destination
+__device__ __forceinline__ void cp_async_8z(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(src_bytes)
+               : "memory");
+}
+
 // K-chunk count covering t in [0, Wp + 7) for one 8-row output block
 __host__ __device__ __forceinline__ int dmma_chunks(int Wp) { return (Wp + 7 + 3) / 4; }
-
 // rows of the input tile the DMMA kernels read for TS outputs
 __host__ __device__ __forceinline__ int dmma_rows(int TS, int Wp) { return TS - 8 + 4 * dmma_chunks(Wp); }
 // zero-guarded tap copies: every A-fragment index of the chunk loops stays inside
@@ -36,19 +72,15 @@ __host__ __device__ __forceinline__ int dmma_cstride_split(int Wp) { return 4 * 
 __host__ __device__ __forceinline__ int dmma_cstride_sum(int Wp) { return 4 * dmma_chunks(Wp) + 32; }
 
 // ------------------------------------------------------------------------------------------
-// Persistent work split. The units of a pass are (image b, L-tile lt, S row s), linearised as
-// u = (b*LT + lt)*S + s. Block k of NB owns [k*U/NB, (k+1)*U/NB) and walks it in chunks of at
-// most TS rows that never cross an (image, L-tile) boundary, so every SM gets the same number
-// of output rows (+- one chunk remainder) whatever the image size, and the next chunk's input
-// tile streams in (cp.async, double buffered) while the current one is multiplied.
+// Persistent work split. Work items are (image b, L-tile lt, S-part) with `parts` equal S
+// ranges per L-tile; block k of NB owns items [k*I/NB, (k+1)*I/NB) and walks each item's S
+// range in chunks of at most TS rows.
 // ------------------------------------------------------------------------------------------
 struct Chunk {
   int b, lt, s0, cnt;
 };
 
 struct ChunkWalk {
-  // work items: (image, L-tile, S-part) with `parts` equal S ranges per L-tile; block k owns
-  // items [k*I/NB, (k+1)*I/NB) and walks each item's S range in chunks of <= TS rows
   long long it, it_end;
   int S, LT, parts;
   int b = 0, lt = 0, s = 0, s_end = 0;
@@ -104,63 +136,75 @@ inline void plan_items(int S, int LT, int batch, int max_blocks, int& parts, int
   nb = (int)(items < max_blocks ? items : max_blocks);
 }
 
+// Issue this thread's share of one [rows][kXS] tile (rows warp, warp+kNW, ..; lane = L col)
+// as cp.async, then arm `full` with the completion of this thread's copies.
+__device__ __forceinline__ void kb_fill_async(double* __restrict__ xs, const double* __restrict__ in,
+                                              const AxisGeom& g, int row_lo, int rows, int l,
+                                              int warp, int lane, unsigned long long* full) {
+  const bool lok = l < g.other;
+  for (int rr = warp; rr < rows; rr += kNW) {
+    int gr = row_lo + rr;
+    if (g.fill && (gr < 0 || gr >= g.Mg)) gr = kb_fold(gr, g.Mg);
+    const int lr = gr - g.g0;
+    const bool ok = lok && gr >= 0 && gr < g.Mg && lr >= -g.halo_lo && lr < g.len + g.halo_hi;
+    cp_async_8z(xs + rr * kXS + lane, ok ? in + (long long)lr * g.other + l : in, ok ? 8 : 0);
+  }
+  cp_async_arrive(full);
+}
+
 // ------------------------------------------------------------------------------------------
-// split pass (fp64, DMMA, persistent): warp w owns S rows [8w, 8w+8) of a chunk x 32 L (four
-// n-tiles) for the G terms of a group: 4G accumulator tiles (8G registers).
+// split pass (fp64, DMMA): warp w owns S rows [8w, 8w+8) of a chunk x 32 L (four n-tiles)
+// for the G terms of a group: 4G accumulator tiles (8G registers). Results go straight from the
+// accumulators to Z_i^T (8 consecutive S values = 64 B per output row and store).
 // ------------------------------------------------------------------------------------------
 template <int G>
 __device__ __forceinline__ void kb_split_group_dmma(const double* __restrict__ xs,
                                                     const double* __restrict__ cb, int cstride,
-                                                    double* __restrict__ ot, const AxisGeom& g,
-                                                    int s_off, int lane, int warp,
+                                                    const AxisGeom& g, int s_off, int lane,
                                                     double* __restrict__ z, long long z_ps,
-                                                    int gstart, const Chunk& ch, double oscale) {
-  constexpr int TS = kNW * 8;
+                                                    int gstart, const Chunk& ch, double oscale,
+                                                    int row_lo, int sign) {
   const int ar = lane >> 2, ac = lane & 3;
   double D[G][4][2];
 #pragma unroll
   for (int gg = 0; gg < G; ++gg)
 #pragma unroll
     for (int j = 0; j < 4; ++j) D[gg][j][0] = D[gg][j][1] = 0.0;
-  if (s_off < ch.cnt) {  // warp-uniform: warps past the chunk's rows idle
-    const int nch = dmma_chunks(g.Wp);
-    const double* xb = xs + (s_off + ac) * kXS + ar;
-    const double* ca = cb + kCG + ac - ar;
+  const int nch = dmma_chunks(g.Wp);
+  const double* xb = xs + (s_off + ac) * kXS + ar;
+  const double* ca = cb + kCG + ac - ar;
+  // global S index of this lane's B row in chunk c is row_lo + s_off + 4c + ac
+  const int grow0 = row_lo + s_off + ac;
+  const bool flip = sign < 0 && g.fill;
 #pragma unroll 2
-    for (int c = 0; c < nch; ++c) {
-      double A[G], B[4];
+  for (int c = 0; c < nch; ++c) {
+    double A[G], B[4];
+    const bool neg = flip && (unsigned)(grow0 + 4 * c) >= (unsigned)g.Mg;
 #pragma unroll
-      for (int gg = 0; gg < G; ++gg) A[gg] = ca[gg * cstride + 4 * c];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) B[j] = xb[4 * c * kXS + 8 * j];
-#pragma unroll
-      for (int gg = 0; gg < G; ++gg)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_884(D[gg][j][0], D[gg][j][1], A[gg], B[j]);
+    for (int gg = 0; gg < G; ++gg) {
+      const double a = ca[gg * cstride + 4 * c];
+      A[gg] = neg ? -a : a;
     }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) B[j] = xb[4 * c * kXS + 8 * j];
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_884(D[gg][j][0], D[gg][j][1], A[gg], B[j]);
   }
-  // one term at a time through the [32][TS+1] transpose stage, then coalesced row stores
+  const int s = s_off + ar;
+  if (s >= ch.cnt) return;
   const int l0 = ch.lt * 32;
 #pragma unroll
   for (int gg = 0; gg < G; ++gg) {
-    if (s_off < ch.cnt) {
+    double* zp = z + (long long)(gstart + gg) * z_ps + ch.s0 + s;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
-          ot[(8 * j + 2 * ac + i) * (TS + 1) + s_off + ar] = D[gg][j][i] * oscale;
-    }
-    __syncthreads();
-    double* zp = z + (long long)(gstart + gg) * z_ps;
-    for (int l = warp; l < 32; l += kNW) {
-      if (l0 + l >= g.other) break;
-      double* zrow = zp + (long long)(l0 + l) * g.len + ch.s0;
-      const double* orow = ot + l * (TS + 1);
-#pragma unroll
-      for (int s = lane; s < TS; s += 32)
-        if (s < ch.cnt) zrow[s] = orow[s];
-    }
-    __syncthreads();
+      for (int i = 0; i < 2; ++i) {
+        const int l = l0 + 8 * j + 2 * ac + i;
+        if (l < g.other) zp[(long long)l * g.len] = D[gg][j][i] * oscale;
+      }
   }
 }
 
@@ -171,92 +215,184 @@ kb_pass_split_dmma(const double* __restrict__ in, long long in_bs, double* __res
                    AxisGeom g, Groups grp, const double* __restrict__ nw2, int r, int batch,
                    int parts) {
   extern __shared__ __align__(16) unsigned char kb_smem_d[];
+  __shared__ unsigned long long full[kStages], empty[kStages];
   constexpr int TS = kNW * 8;
   const int rows_tile = dmma_rows(TS, g.Wp);
   const int cstride = dmma_cstride_split(g.Wp);
-  double* xs = reinterpret_cast<double*>(kb_smem_d);  // [2][rows_tile][kXS]
-  double* cpad = xs + 2 * rows_tile * kXS;             // [r][cstride], taps at offset kCG
-  double* ot = cpad + r * cstride;                     // [32][TS + 1]
+  double* xs = reinterpret_cast<double*>(kb_smem_d);  // [kStages][rows_tile][kXS]
+  double* cpad = xs + kStages * rows_tile * kXS;       // [r][cstride], taps at offset kCG
   const int lane = threadIdx.x, warp = threadIdx.y;
   const int tid = warp * 32 + lane;
   const int LT = (g.other + 31) / 32;
-  ChunkWalk walk(g.len, LT, parts, batch);
+  const int s_off = warp * 8;
 
-  auto fill = [&](const Chunk& c, int buf) {
-    kb_fill_tile<double, kXS>(xs + buf * rows_tile * kXS, in + c.b * in_bs, g, g.g0 + c.s0 - g.H,
-                              rows_tile, c.lt * 32 + lane, warp, lane, grp.sign[0]);
-    cp_async_commit();
-  };
-
-  Chunk cur, nxt;
-  if (!walk.next(cur, TS)) return;
-  fill(cur, 0);
-  // batch-uniform taps: all images of a batched operator share the term layout; per-image taps
-  // are reloaded when a chunk starts a new image
-  int taps_b = -1;
-  int buf = 0;
-  bool more = true;
-  while (more) {
-    more = walk.next(nxt, TS);
-    if (more) {
-      fill(nxt, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+  if (tid == 0) {
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(&full[st], 32 * kNW);
+      mbar_init(&empty[st], kNW);
     }
-    if (cur.b != taps_b) {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  // this block's chunk list, walked once by the filling side and once by the consuming side
+  ChunkWalk fill_walk(g.len, LT, parts, batch), use_walk(g.len, LT, parts, batch);
+  Chunk fc, ch;
+  int nfill = 0;
+  auto issue = [&]() {
+    if (!fill_walk.next(fc, TS)) return;
+    const int st = nfill % kStages;
+    if (nfill >= kStages) mbar_wait(&empty[st], ((nfill / kStages) - 1) & 1);
+    kb_fill_async(xs + st * rows_tile * kXS, in + fc.b * in_bs, g, g.g0 + fc.s0 - g.H, rows_tile,
+                  fc.lt * 32 + lane, warp, lane, &full[st]);
+    ++nfill;
+  };
+  for (int k = 0; k < kStages - 1; ++k) issue();
+
+  int taps_b = -1;
+  for (int t = 0; use_walk.next(ch, TS); ++t) {
+    if (ch.b != taps_b) {  // per-image taps (uniform across the block: block-level reload)
       __syncthreads();
-      const double* tb = tin + cur.b * t_bs;
+      const double* tb = tin + ch.b * t_bs;
       for (int idx = tid; idx < r * cstride; idx += 32 * kNW) {
         const int i = idx / cstride, k = idx - i * cstride - kCG;
         cpad[idx] = (k >= 0 && k < g.Wp) ? tb[(long long)i * g.Wp + k] : 0.0;
       }
-      taps_b = cur.b;
+      __syncthreads();
+      taps_b = ch.b;
     }
-    __syncthreads();
-    double* xt = xs + buf * rows_tile * kXS;
-    const int row_lo = g.g0 + cur.s0 - g.H;
-    const bool has_out = g.fill && (row_lo < 0 || row_lo + rows_tile > g.Mg);
-    const double oscale = nw2 ? 1.0 / sqrt(nw2[cur.b]) : 1.0;
-    double* zb = z + cur.b * z_bs;
-    int cur_sign = grp.sign[0];
-    for (int gi = 0; gi < grp.n; ++gi) {
-      const int gstart = grp.start[gi], gcount = grp.count[gi];
-      if (has_out && grp.sign[gi] != cur_sign) {  // flip the folded rows for this group's sign
-        for (int rr = warp; rr < rows_tile; rr += kNW) {
-          const int gr = row_lo + rr;
-          if (gr < 0 || gr >= g.Mg) xt[rr * kXS + lane] = -xt[rr * kXS + lane];
-        }
-        __syncthreads();
-      }
-      cur_sign = grp.sign[gi];
-      const double* cb = cpad + gstart * cstride;
-#define KB_DGROUP(C)                                                                                 \
-  case C:                                                                                            \
-    if constexpr (C <= GMAX)                                                                         \
-      kb_split_group_dmma<C>(xt, cb, cstride, ot, g, warp * 8, lane, warp, zb, z_ps, gstart, cur, oscale); \
+    issue();  // keep kStages-1 tiles in flight ahead of the one consumed now
+    const int st = t % kStages;
+    mbar_wait(&full[st], (t / kStages) & 1);
+    const double* xt = xs + st * rows_tile * kXS;
+    const int row_lo = g.g0 + ch.s0 - g.H;
+    const double oscale = nw2 ? 1.0 / sqrt(nw2[ch.b]) : 1.0;
+    double* zb = z + ch.b * z_bs;
+    if (s_off < ch.cnt) {  // warp-uniform: warps past the chunk's rows idle
+      for (int gi = 0; gi < grp.n; ++gi) {
+        const int gstart = grp.start[gi];
+        const double* cb = cpad + gstart * cstride;
+#define KB_DGROUP(C)                                                                                  \
+  case C:                                                                                             \
+    if constexpr (C <= GMAX)                                                                          \
+      kb_split_group_dmma<C>(xt, cb, cstride, g, s_off, lane, zb, z_ps, gstart, ch, oscale, row_lo,   \
+                             grp.sign[gi]);                                                           \
     break;
-      switch (gcount) {
-        KB_DGROUP(1)
-        KB_DGROUP(2)
-        KB_DGROUP(3)
-        KB_DGROUP(4)
-        KB_DGROUP(5)
-        KB_DGROUP(6)
-        default: break;
-      }
+        switch (grp.count[gi]) {
+          KB_DGROUP(1)
+          KB_DGROUP(2)
+          KB_DGROUP(3)
+          KB_DGROUP(4)
+          KB_DGROUP(5)
+          KB_DGROUP(6)
+          default: break;
+        }
 #undef KB_DGROUP
+      }
     }
-    cur = nxt;
-    buf ^= 1;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+// ------------------------------------------------------------------------------------------
+// Fused epilogue straight from the sum pass accumulators: lane (ar, ac) of warp s_off holds
+// output S = s0+s_off+8mt+ar (n index) for L = l0+8j+2ac+i (m index), i.e. per store 8
+// consecutive n values (64 B) of 4 image rows. One m-tile at a time, operand loads first.
+// ------------------------------------------------------------------------------------------
+template <int MODE>
+__device__ __forceinline__ void kb_sum_epilogue_regs(const double (&D)[2][4][2], const AxisGeom& g,
+                                                     const Epi<double>& e, const Chunk& ch,
+                                                     int s_off, int ar, int ac, double (&nrm)[3],
+                                                     bool& bad) {
+  const int n = g.len;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const int sl = s_off + 8 * mt + ar;  // row within the chunk
+    const int q = ch.s0 + sl;            // n index
+    if (sl >= ch.cnt || q >= n) continue;
+    const long long rowbase = (long long)ch.b * e.bstride + q;
+    double u[4][2], w[4][2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int p = ch.lt * 32 + 8 * j + 2 * ac + i;
+        const long long at = rowbase + (long long)p * n;
+        const bool ok = p < g.other;
+        if constexpr (MODE == EPI_RESID) u[j][i] = ok ? e.bsub[at] : 0.0;
+        if constexpr (MODE == EPI_UPDATE) {
+          u[j][i] = ok ? e.y[at] : 0.0;
+          w[j][i] = ok ? e.x[at] : 0.0;
+        }
+        if constexpr (MODE == EPI_POWER) u[j][i] = ok ? e.vin[at] : 0.0;
+      }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int p = ch.lt * 32 + 8 * j + 2 * ac + i;
+        if (p >= g.other) continue;
+        const long long at = rowbase + (long long)p * n;
+        double val = D[mt][j][i];
+        if (e.foldH > 0) {
+          const int FH = e.foldH;
+          const double* f = e.fold + ((long long)ch.b * g.other + p) * (2 * FH);
+          if (q < FH) val += f[q];
+          else if (q >= n - FH) val += f[q - (n - 2 * FH)];
+        }
+        if constexpr (MODE == EPI_PLAIN) {
+          e.out[at] = val;
+        } else if constexpr (MODE == EPI_RESID) {
+          e.out[at] = __dsub_rn(val, u[j][i]);
+        } else if constexpr (MODE == EPI_UPDATE) {
+          double xv = __ddiv_rn(__dsub_rn(__dmul_rn(e.L[ch.b], u[j][i]), val), e.denom[ch.b]);
+          if (e.project) xv = (xv > 0.0 || xv != xv) ? xv : 0.0;
+          const double d = __dsub_rn(xv, w[j][i]);
+          e.x[at] = xv;
+          e.y[at] = __dadd_rn(xv, __dmul_rn(e.beta, d));
+          bad |= !isfinite(xv);
+          if (e.want_norms) {
+            nrm[0] += d * d;
+            nrm[1] += w[j][i] * w[j][i];
+            nrm[2] += xv * xv;
+          }
+        } else {  // EPI_POWER
+          const double vv = e.vnw2 ? u[j][i] / sqrt(e.vnw2[ch.b]) : u[j][i];
+          e.out[at] = val;
+          nrm[0] += vv * val;
+          nrm[1] += val * val;
+        }
+      }
+  }
+}
+
+// per-warp end of an image's epilogues: non-finite flag and this warp's norm partials
+template <int MODE>
+__device__ __forceinline__ void kb_warp_finish(const Epi<double>& e, double (&nrm)[3], bool bad,
+                                               int b, int nslots, int slot, int lane) {
+  if constexpr (MODE == EPI_UPDATE) {
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(e.nonfinite, e.k);
+  }
+  if constexpr (MODE == EPI_UPDATE || MODE == EPI_POWER) {
+    if (MODE == EPI_POWER || e.want_norms) {
+#pragma unroll
+      for (int qq = 0; qq < 3; ++qq) {
+        double v = nrm[qq];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) e.partials[((long long)b * nslots + slot) * 4 + qq] = v;
+      }
+    }
   }
 }
 
 // ------------------------------------------------------------------------------------------
-// sum pass (fp64, DMMA, persistent): warp w owns S rows [16w, 16w+16) (two m-tiles) x 32 L;
-// the (chunk, term) tiles stream through two buffers; m-tile 1 reuses the B fragment of chunk
-// t0 with the A fragment of t0 - 8. After a chunk's last term the result is transposed through
-// the buffer just consumed and the fused epilogue runs on coalesced [m][n] rows.
+// sum pass (fp64, DMMA): warp w owns S rows [16w, 16w+16) (two m-tiles) x 32 L of a chunk;
+// the (chunk, term) tiles stream through the mbarrier ring; m-tile 1 reuses the B fragment of
+// chunk t0 with the A fragment of t0 - 8. After a chunk's last term each warp runs the fused
+// epilogue from its registers. Norm partials are per warp: partials[b][block*kNW + warp].
 // ------------------------------------------------------------------------------------------
 template <int MODE>
 __global__ void __launch_bounds__(32 * kNW, 2)
@@ -264,113 +400,117 @@ kb_pass_sum_dmma(const double* __restrict__ z, long long z_ps, long long z_bs, i
                  const double* __restrict__ tin, long long t_bs, AxisGeom g,
                  const double* __restrict__ tsign, Epi<double> e, int batch, int parts) {
   extern __shared__ __align__(16) unsigned char kb_smem_d[];
+  __shared__ unsigned long long full[kStages], empty[kStages];
   constexpr int TS = kNW * 16;
   const int rows_tile = dmma_rows(TS, g.Wp);
   const int cstride = dmma_cstride_sum(g.Wp);  // taps at offset kCG + 8 (m-tile 1 reads t0 - 8)
-  double* xs = reinterpret_cast<double*>(kb_smem_d);  // [2][rows_tile][kXS]
-  double* cpad = xs + 2 * rows_tile * kXS;             // [2][cstride] (taps of each buffered tile)
+  double* xs = reinterpret_cast<double*>(kb_smem_d);  // [kStages][rows_tile][kXS]
+  double* cpad = xs + kStages * rows_tile * kXS;       // [r][cstride]
   const int lane = threadIdx.x, warp = threadIdx.y;
   const int tid = warp * 32 + lane;
   const int LT = (g.other + 31) / 32;
-  ChunkWalk walk(g.len, LT, parts, batch);
   const int ar = lane >> 2, ac = lane & 3;
   const int s_off = warp * 16;
   const int nch = dmma_chunks(g.Wp);
+  const int nslots = gridDim.x * kNW, slot = blockIdx.x * kNW + warp;
 
-  auto fill = [&](const Chunk& c, int term, int buf) {
-    const int sgn = tsign ? (tsign[(long long)c.b * r + term] < 0.0 ? -1 : 1) : 1;
-    kb_fill_tile<double, kXS>(xs + buf * rows_tile * kXS, z + c.b * z_bs + (long long)term * z_ps,
-                              g, g.g0 + c.s0 - g.H, rows_tile, c.lt * 32 + lane, warp, lane, sgn);
-    const double* tb = tin + c.b * t_bs + (long long)term * g.Wp;
-    for (int idx = tid; idx < cstride; idx += 32 * kNW) {
-      const int k = idx - kCG - 8;
-      cpad[buf * cstride + idx] = (k >= 0 && k < g.Wp) ? tb[k] : 0.0;
+  if (tid == 0) {
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(&full[st], 32 * kNW);
+      mbar_init(&empty[st], kNW);
     }
-    cp_async_commit();
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  // tile sequence: (chunk, term) for every chunk of this block
+  ChunkWalk fill_walk(g.len, LT, parts, batch), use_walk(g.len, LT, parts, batch);
+  Chunk fc;
+  int fterm = r;  // forces fetching the first chunk
+  bool fmore = true;
+  int nfill = 0;
+  auto issue = [&]() {
+    if (!fmore) return;
+    if (fterm == r) {
+      if (!fill_walk.next(fc, TS)) {
+        fmore = false;
+        return;
+      }
+      fterm = 0;
+    }
+    const int st = nfill % kStages;
+    if (nfill >= kStages) mbar_wait(&empty[st], ((nfill / kStages) - 1) & 1);
+    kb_fill_async(xs + st * rows_tile * kXS, z + fc.b * z_bs + (long long)fterm * z_ps, g,
+                  g.g0 + fc.s0 - g.H, rows_tile, fc.lt * 32 + lane, warp, lane, &full[st]);
+    ++fterm;
+    ++nfill;
   };
+  for (int k = 0; k < kStages - 1; ++k) issue();
 
   double nrm[3] = {0.0, 0.0, 0.0};
   bool bad = false;
-  const int nblk = gridDim.x, blk = blockIdx.x;
-
-  Chunk cur, nxt;
-  if (!walk.next(cur, TS)) {
-    if (MODE == EPI_UPDATE || MODE == EPI_POWER) kb_sum_finish<double, MODE>(e, nrm, bad, 0, nblk, blk, lane);
-    return;
-  }
-  bool have_next = walk.next(nxt, TS);
-  fill(cur, 0, 0);
-  int buf = 0, term = 0, norm_b = cur.b;
+  int norm_b = -1, taps_b = -1;
   double D[2][4][2];
-  while (true) {
-    __syncthreads();  // the buffer about to be refilled has been consumed by every warp
-    // prefetch the next (chunk, term) tile
-    const bool last_term = term + 1 == r;
-    const bool prefetch = !last_term || have_next;
-    if (prefetch) {
-      if (!last_term) fill(cur, term + 1, buf ^ 1);
-      else fill(nxt, 0, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+  Chunk ch;
+  int t = 0;
+  while (use_walk.next(ch, TS)) {
+    if (ch.b != taps_b) {  // per-image taps (uniform across the block)
+      __syncthreads();
+      const double* tb = tin + ch.b * t_bs;
+      for (int idx = tid; idx < r * cstride; idx += 32 * kNW) {
+        const int i = idx / cstride, k = idx - i * cstride - kCG - 8;
+        cpad[idx] = (k >= 0 && k < g.Wp) ? tb[(long long)i * g.Wp + k] : 0.0;
+      }
+      __syncthreads();
+      taps_b = ch.b;
     }
-    __syncthreads();
-    if (term == 0) {
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) D[mt][j][0] = D[mt][j][1] = 0.0;
+    if (ch.b != norm_b) {
+      if (norm_b >= 0) kb_warp_finish<MODE>(e, nrm, bad, norm_b, nslots, slot, lane);
+      nrm[0] = nrm[1] = nrm[2] = 0.0;
+      bad = false;
+      norm_b = ch.b;
     }
-    if (s_off < cur.cnt) {  // warp-uniform
-      const double* xb = xs + buf * rows_tile * kXS + (s_off + ac) * kXS + ar;
-      const double* cb = cpad + buf * cstride + kCG + 8 + ac - ar;
-      const bool two = s_off + 8 < cur.cnt;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) D[mt][j][0] = D[mt][j][1] = 0.0;
+    const int row_lo = g.g0 + ch.s0 - g.H;
+    const int grow0 = row_lo + s_off + ac;
+    const bool active = s_off < ch.cnt;  // warp-uniform
+    const bool two = s_off + 8 < ch.cnt;
+    for (int term = 0; term < r; ++term, ++t) {
+      issue();
+      const int st = t % kStages;
+      mbar_wait(&full[st], (t / kStages) & 1);
+      if (active) {
+        const double* xb = xs + st * rows_tile * kXS + (s_off + ac) * kXS + ar;
+        const double* cb = cpad + term * cstride + kCG + 8 + ac - ar;
+        const bool flip = g.fill && tsign && tsign[(long long)ch.b * r + term] < 0.0;
 #pragma unroll 2
-      for (int c = 0; c < nch + 2; ++c) {
-        double B[4];
+        for (int c = 0; c < nch + 2; ++c) {
+          double B[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) B[j] = xb[4 * c * kXS + 8 * j];
-        const double a0 = cb[4 * c];      // zero beyond the band
-        const double a1 = cb[4 * c - 8];  // zero for c < 2 (guard)
+          for (int j = 0; j < 4; ++j) B[j] = xb[4 * c * kXS + 8 * j];
+          double a0 = cb[4 * c];      // zero beyond the band
+          double a1 = cb[4 * c - 8];  // zero for c < 2 (guard)
+          if (flip && (unsigned)(grow0 + 4 * c) >= (unsigned)g.Mg) {
+            a0 = -a0;
+            a1 = -a1;
+          }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          dmma_884(D[0][j][0], D[0][j][1], a0, B[j]);
-          if (two) dmma_884(D[1][j][0], D[1][j][1], a1, B[j]);
+          for (int j = 0; j < 4; ++j) {
+            dmma_884(D[0][j][0], D[0][j][1], a0, B[j]);
+            if (two) dmma_884(D[1][j][0], D[1][j][1], a1, B[j]);
+          }
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
     }
-    if (last_term) {
-      __syncthreads();  // everyone is done reading this buffer: reuse it as the transpose stage
-      double* ot = xs + buf * rows_tile * kXS;
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-          for (int ii = 0; ii < 2; ++ii)
-            ot[(8 * j + 2 * ac + ii) * (TS + 1) + s_off + 8 * mt + ar] = D[mt][j][ii];
-      __syncthreads();
-      if (MODE == EPI_UPDATE || MODE == EPI_POWER) {
-        if (cur.b != norm_b) {  // this block's partials of the previous image are complete
-          kb_sum_finish<double, MODE>(e, nrm, bad, norm_b, nblk, blk, lane);
-          nrm[0] = nrm[1] = nrm[2] = 0.0;
-          bad = false;
-          norm_b = cur.b;
-        }
-      }
-      kb_sum_epilogue<double, MODE, TS>(ot, g, e, cur.b, cur.s0, min(g.len, cur.s0 + cur.cnt),
-                                        cur.lt * 32, warp, lane, nrm, bad);
-      __syncthreads();
-      if (!have_next) break;
-      cur = nxt;
-      have_next = walk.next(nxt, TS);
-      term = 0;
-    } else {
-      ++term;
-    }
-    buf ^= 1;
+    if (active) kb_sum_epilogue_regs<MODE>(D, g, e, ch, s_off, ar, ac, nrm, bad);
   }
-  if (MODE == EPI_UPDATE || MODE == EPI_POWER) kb_sum_finish<double, MODE>(e, nrm, bad, norm_b, nblk, blk, lane);
+  if (norm_b >= 0) kb_warp_finish<MODE>(e, nrm, bad, norm_b, nslots, slot, lane);
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
 }  // namespace kb
