@@ -3,6 +3,8 @@
 // Owns the device tap tables of an operator, the workspace layout, and the native iteration
 // loop of the sFISTA engine (kronblur solvers.py:168-174) including optional CUDA-graph
 // capture of the whole launch sequence. No torch types cross this boundary.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -43,7 +45,7 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 constexpr int kMaxHalf = 1024;
-constexpr int kGmaxF64 = 4;  // pass A term group (register budget: G*R accumulators)
+constexpr int kGmaxF64 = 3;  // pass A term group (register budget: G*R accumulators)
 constexpr int kGmaxF32 = 8;
 constexpr double kSymTol = 1e-11;  // (anti)symmetry residual allowed for sign-reflected fills
 constexpr int kRA = 8;   // pass A rows per warp
@@ -99,10 +101,39 @@ int persistent_blocks() {
   return nb;
 }
 
+// TMA descriptor of a 3-D [planes][rows][cols] fp64 array (cols contiguous) with a
+// {36 cols x box_rows} box; false when TMA's alignment rules rule it out (caller falls back).
+bool make_tmap(CUtensorMap* map, const void* base, long long cols, long long rows, long long planes,
+               long long row_stride, long long plane_stride, int box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  if (!encode) return false;
+  if (reinterpret_cast<uintptr_t>(base) % 16 || (row_stride * 8) % 16 || (plane_stride * 8) % 16) return false;
+  if (box_rows < 1 || box_rows > 256) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)planes};
+  const cuuint64_t strides[2] = {(cuuint64_t)row_stride * 8, (cuuint64_t)plane_stride * 8};
+  const cuuint32_t box[3] = {36, (cuuint32_t)box_rows, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// fp64 runs on the TMA + DMMA kernels when both image extents are even (16-byte row strides)
+bool use_dmma(const kb_op* op) { return op->dtype == KB_F64 && op->m % 2 == 0 && op->n % 2 == 0; }
+
 // Norm partial slots of the sum pass per image: one per warp (fp64 persistent kernel) or
 // one per block (fp32).
 int sum_blocks(const kb_op* op) {
-  if (op->dtype == KB_F64) {
+  if (use_dmma(op)) {  // per-warp slots
     int parts, nb;
     kb::plan_items(op->n, (op->m + 31) / 32, op->batch, persistent_blocks(), parts, nb);
     return nb * kb::kNW;
@@ -194,16 +225,24 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
   const long long t_bs = (long long)op->r * g.Wp;
   if constexpr (sizeof(T) == 8) {
     constexpr int TS = kb::kNW * 8;
-    const size_t smem = sizeof(double) * ((size_t)kb::kStages * kb::dmma_rows(TS, g.Wp) * kb::kXS +
-                                          (size_t)op->r * kb::dmma_cstride_split(g.Wp));
-    auto kern = kb::kb_pass_split_dmma<kGmaxF64>;
-    KB_TRY(allow_smem(kern, smem));
-    int parts, nb;
-    kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
-    kern<<<nb, dim3(32, kb::kNW), smem, s>>>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2,
-                                             op->r, op->batch, parts);
-    KB_CUDA(cudaGetLastError());
-    return KB_OK;
+    const kb::TileBoxes tb = kb::tile_boxes(kb::dmma_rows(TS, g.Wp));
+    CUtensorMap map;
+    if (use_dmma(op)) {
+      if (!make_tmap(&map, in - (long long)g.halo_lo * g.other, g.other, g.len + g.halo_lo + g.halo_hi,
+                     op->batch, g.other, in_bs, tb.box_rows))
+        return fail(KB_ERR_ARGUMENT, "input plane not 16-byte aligned for TMA");
+      const size_t smem = sizeof(double) * ((size_t)kb::kStages * tb.stage_elems +
+                                            (size_t)op->r * kb::dmma_cstride_split(g.Wp));
+      auto kern = kb::kb_pass_split_dmma<kGmaxF64>;
+      KB_TRY(allow_smem(kern, smem));
+      int parts, nb;
+      kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
+      kern<<<nb, dim3(32, kb::kNW), smem, s>>>(map, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r,
+                                               op->batch, parts);
+      KB_CUDA(cudaGetLastError());
+      return KB_OK;
+    }
+    return launch_a_g<T, kGmaxF64>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
   } else {
     return launch_a_g<T, kGmaxF32>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
   }
@@ -213,19 +252,25 @@ template <typename T, int MODE>
 int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g, const T* tsign,
              const kb::Epi<T>& e, cudaStream_t s) {
   if constexpr (sizeof(T) == 8) {
-    const size_t smem = sizeof(double) * ((size_t)kb::kStages * kb::dmma_rows(kb::kNW * 16, g.Wp) * kb::kXS +
-                                          (size_t)op->r * kb::dmma_cstride_sum(g.Wp));
-    auto kern = kb::kb_pass_sum_dmma<MODE>;
-    KB_TRY(allow_smem(kern, smem));
+    const kb::TileBoxes tb = kb::tile_boxes(kb::dmma_rows(kb::kNW * 16, g.Wp));
     const long long z_ps = (long long)g.len * g.other;
-    int parts, nb;
-    kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
-    if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // warps skip untouched images
-      KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kNW, s));
-    kern<<<nb, dim3(32, kb::kNW), smem, s>>>(z, z_ps, z_ps * op->r, op->r, tin,
-                                             (long long)op->r * g.Wp, g, tsign, e, op->batch, parts);
-    KB_CUDA(cudaGetLastError());
-    return KB_OK;
+    CUtensorMap map;
+    if (use_dmma(op)) {
+      if (!make_tmap(&map, z, g.other, g.len, (long long)op->batch * op->r, g.other, z_ps, tb.box_rows))
+        return fail(KB_ERR_ARGUMENT, "intermediate planes not 16-byte aligned for TMA");
+      const size_t smem = sizeof(double) * ((size_t)kb::kStages * tb.stage_elems +
+                                            (size_t)op->r * kb::dmma_cstride_sum(g.Wp));
+      auto kern = kb::kb_pass_sum_dmma<MODE>;
+      KB_TRY(allow_smem(kern, smem));
+      int parts, nb;
+      kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
+      if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // warps skip untouched images
+        KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kNW, s));
+      kern<<<nb, dim3(32, kb::kNW), smem, s>>>(map, op->r, tin, (long long)op->r * g.Wp, g, tsign, e,
+                                               op->batch, parts);
+      KB_CUDA(cudaGetLastError());
+      return KB_OK;
+    }
   }
   constexpr int TS = kb::kNW * kRB;
   const size_t smem = sizeof(T) * (2 * (size_t)(TS + g.Wp) * 32 + 2 * (size_t)g.Wp);
@@ -246,8 +291,18 @@ struct RowBlock {
   int g0, mg, hlo, hhi;
 };
 
+int debug_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* v = std::getenv("KB_DEBUG_MODE");
+    mode = v ? std::atoi(v) : 0;
+  }
+  return mode;
+}
+
 kb::AxisGeom geom_a(const kb_op* op, int adjoint, const RowBlock& rb) {
   kb::AxisGeom g;
+  g.dbg = debug_mode();
   g.len = op->m;
   g.other = op->n;
   g.H = op->Ha;
@@ -262,6 +317,7 @@ kb::AxisGeom geom_a(const kb_op* op, int adjoint, const RowBlock& rb) {
 
 kb::AxisGeom geom_b(const kb_op* op, int adjoint) {  // sum pass over Z_i^T [n][m]
   kb::AxisGeom g;
+  g.dbg = debug_mode();
   g.len = op->n;
   g.other = op->m;
   g.H = op->Hb;

@@ -21,6 +21,8 @@
 // the (anti)symmetric adjoint's fill sign is applied to the A fragment of those rows, so tiles
 // are never rewritten in shared memory.
 #pragma once
+#include <cuda.h>  // CUtensorMap
+
 #include "kb_kernels.cuh"
 
 namespace kb {
@@ -61,6 +63,53 @@ __device__ __forceinline__ void cp_async_8z(void* smem, const void* gmem, int sr
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
                "r"(src_bytes)
                : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// TMA: 3-D box of `map` at (c0 = column, c1 = row, c2 = plane) -> shared memory, completion
+// counted in bytes on `bar`; out-of-range coordinates are zero-filled by the hardware
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// TMA tile geometry: a tile of `rows` rows is fetched as nbox boxes of box_rows (<= 256) rows;
+// each stage buffer is padded to a 128-byte multiple.
+struct TileBoxes {
+  int nbox, box_rows, stage_elems;
+};
+__host__ __device__ __forceinline__ TileBoxes tile_boxes(int rows) {
+  TileBoxes t;
+  t.nbox = (rows + 255) / 256;
+  t.box_rows = (rows + t.nbox - 1) / t.nbox;
+  t.stage_elems = ((t.nbox * t.box_rows * 36 + 15) / 16) * 16;
+  return t;
+}
+
+// Tile row whose data stands in for tile row tr of a reflect-filled pass: rows outside the
+// domain read their folded partner inside the tile scaled by `sign` (at a domain edge the TMA
+// box contains every partner an in-chunk output needs). A fold leaving the domain or the tile
+// keeps the (zero-filled, out-of-range) row itself with weight 0: DMMA multiplies every B row by
+// the whole A column, so even zero-weighted rows must hold finite values.
+__device__ __forceinline__ int kb_src_row(int tr, int row_lo, int Mg, int rows, int sign, double& mul) {
+  const int gr = row_lo + tr;
+  mul = 1.0;
+  if (gr >= 0 && gr < Mg) return tr;
+  const int f = kb_fold(gr, Mg);
+  const int u = f - row_lo;
+  if (f < 0 || u < 0 || u >= rows) {
+    mul = 0.0;
+    return tr;
+  }
+  mul = (double)sign;
+  return u;
 }
 
 // K-chunk count covering t in [0, Wp + 7) for one 8-row output block
@@ -136,64 +185,55 @@ inline void plan_items(int S, int LT, int batch, int max_blocks, int& parts, int
   nb = (int)(items < max_blocks ? items : max_blocks);
 }
 
-// Issue this thread's share of one [rows][kXS] tile (rows warp, warp+kNW, ..; lane = L col)
-// as cp.async, then arm `full` with the completion of this thread's copies.
-__device__ __forceinline__ void kb_fill_async(double* __restrict__ xs, const double* __restrict__ in,
-                                              const AxisGeom& g, int row_lo, int rows, int l,
-                                              int warp, int lane, unsigned long long* full) {
-  const bool lok = l < g.other;
-  for (int rr = warp; rr < rows; rr += kNW) {
-    int gr = row_lo + rr;
-    if (g.fill && (gr < 0 || gr >= g.Mg)) gr = kb_fold(gr, g.Mg);
-    const int lr = gr - g.g0;
-    const bool ok = lok && gr >= 0 && gr < g.Mg && lr >= -g.halo_lo && lr < g.len + g.halo_hi;
-    cp_async_8z(xs + rr * kXS + lane, ok ? in + (long long)lr * g.other + l : in, ok ? 8 : 0);
-  }
-  cp_async_arrive(full);
-}
-
 // ------------------------------------------------------------------------------------------
 // split pass (fp64, DMMA): warp w owns S rows [8w, 8w+8) of a chunk x 32 L (four n-tiles)
 // for the G terms of a group: 4G accumulator tiles (8G registers). Results go straight from the
 // accumulators to Z_i^T (8 consecutive S values = 64 B per output row and store).
 // ------------------------------------------------------------------------------------------
+// MMA loop of one group: EDGE tiles (reflect-filled pass at a domain edge) read folded rows.
+template <int G, bool EDGE>
+__device__ __forceinline__ void kb_split_mma(double (&D)[G][4][2], const double* __restrict__ xs,
+                                             const double* __restrict__ ca, int cstride, int nch,
+                                             int s_off, int ar, int ac, int row_lo, int Mg,
+                                             int rows, int sign) {
+  const double* xb = xs + (s_off + ac) * kXS + ar;
+#pragma unroll 2
+  for (int c = 0; c < nch; ++c) {
+    double A[G], B[4];
+    double mul = 1.0;
+    const double* xr = xb + 4 * c * kXS;
+    if constexpr (EDGE) xr = xs + kb_src_row(s_off + 4 * c + ac, row_lo, Mg, rows, sign, mul) * kXS + ar;
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) A[gg] = EDGE ? ca[gg * cstride + 4 * c] * mul : ca[gg * cstride + 4 * c];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) B[j] = xr[8 * j];
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_884(D[gg][j][0], D[gg][j][1], A[gg], B[j]);
+  }
+}
+
 template <int G>
 __device__ __forceinline__ void kb_split_group_dmma(const double* __restrict__ xs,
                                                     const double* __restrict__ cb, int cstride,
                                                     const AxisGeom& g, int s_off, int lane,
                                                     double* __restrict__ z, long long z_ps,
                                                     int gstart, const Chunk& ch, double oscale,
-                                                    int row_lo, int sign) {
+                                                    bool scaled, int row_lo, bool edge, int sign) {
   const int ar = lane >> 2, ac = lane & 3;
   double D[G][4][2];
 #pragma unroll
   for (int gg = 0; gg < G; ++gg)
 #pragma unroll
     for (int j = 0; j < 4; ++j) D[gg][j][0] = D[gg][j][1] = 0.0;
-  const int nch = dmma_chunks(g.Wp);
-  const double* xb = xs + (s_off + ac) * kXS + ar;
+  const int nch = (g.dbg & 1) ? 0 : dmma_chunks(g.Wp);
   const double* ca = cb + kCG + ac - ar;
-  // global S index of this lane's B row in chunk c is row_lo + s_off + 4c + ac
-  const int grow0 = row_lo + s_off + ac;
-  const bool flip = sign < 0 && g.fill;
-#pragma unroll 2
-  for (int c = 0; c < nch; ++c) {
-    double A[G], B[4];
-    const bool neg = flip && (unsigned)(grow0 + 4 * c) >= (unsigned)g.Mg;
-#pragma unroll
-    for (int gg = 0; gg < G; ++gg) {
-      const double a = ca[gg * cstride + 4 * c];
-      A[gg] = neg ? -a : a;
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) B[j] = xb[4 * c * kXS + 8 * j];
-#pragma unroll
-    for (int gg = 0; gg < G; ++gg)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dmma_884(D[gg][j][0], D[gg][j][1], A[gg], B[j]);
-  }
+  const int rows = dmma_rows(kNW * 8, g.Wp);
+  if (edge) kb_split_mma<G, true>(D, xs, ca, cstride, nch, s_off, ar, ac, row_lo, g.Mg, rows, sign);
+  else kb_split_mma<G, false>(D, xs, ca, cstride, nch, s_off, ar, ac, row_lo, g.Mg, rows, sign);
   const int s = s_off + ar;
-  if (s >= ch.cnt) return;
+  if (s >= ch.cnt || (g.dbg & 2)) return;
   const int l0 = ch.lt * 32;
 #pragma unroll
   for (int gg = 0; gg < G; ++gg) {
@@ -203,24 +243,25 @@ __device__ __forceinline__ void kb_split_group_dmma(const double* __restrict__ x
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const int l = l0 + 8 * j + 2 * ac + i;
-        if (l < g.other) zp[(long long)l * g.len] = D[gg][j][i] * oscale;
+        if (l < g.other) zp[(long long)l * g.len] = scaled ? D[gg][j][i] * oscale : D[gg][j][i];
       }
   }
 }
 
 template <int GMAX>
 __global__ void __launch_bounds__(32 * kNW, 2)
-kb_pass_split_dmma(const double* __restrict__ in, long long in_bs, double* __restrict__ z,
+kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict__ z,
                    long long z_ps, long long z_bs, const double* __restrict__ tin, long long t_bs,
                    AxisGeom g, Groups grp, const double* __restrict__ nw2, int r, int batch,
                    int parts) {
-  extern __shared__ __align__(16) unsigned char kb_smem_d[];
+  extern __shared__ __align__(128) unsigned char kb_smem_d[];
   __shared__ unsigned long long full[kStages], empty[kStages];
   constexpr int TS = kNW * 8;
   const int rows_tile = dmma_rows(TS, g.Wp);
+  const TileBoxes tb = tile_boxes(rows_tile);
   const int cstride = dmma_cstride_split(g.Wp);
-  double* xs = reinterpret_cast<double*>(kb_smem_d);  // [kStages][rows_tile][kXS]
-  double* cpad = xs + kStages * rows_tile * kXS;       // [r][cstride], taps at offset kCG
+  double* xs = reinterpret_cast<double*>(kb_smem_d);  // [kStages][stage_elems]
+  double* cpad = xs + kStages * tb.stage_elems;        // [r][cstride], taps at offset kCG
   const int lane = threadIdx.x, warp = threadIdx.y;
   const int tid = warp * 32 + lane;
   const int LT = (g.other + 31) / 32;
@@ -228,23 +269,27 @@ kb_pass_split_dmma(const double* __restrict__ in, long long in_bs, double* __res
 
   if (tid == 0) {
     for (int st = 0; st < kStages; ++st) {
-      mbar_init(&full[st], 32 * kNW);
+      mbar_init(&full[st], 1);
       mbar_init(&empty[st], kNW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
-  // this block's chunk list, walked once by the filling side and once by the consuming side
+  // thread 0 walks this block's chunk list ahead of the consumers and issues one TMA box per
+  // (<= 256-row) part of each tile; the map covers the local plane including its halo rows
   ChunkWalk fill_walk(g.len, LT, parts, batch), use_walk(g.len, LT, parts, batch);
   Chunk fc, ch;
   int nfill = 0;
   auto issue = [&]() {
-    if (!fill_walk.next(fc, TS)) return;
+    if (tid != 0 || !fill_walk.next(fc, TS)) return;
     const int st = nfill % kStages;
     if (nfill >= kStages) mbar_wait(&empty[st], ((nfill / kStages) - 1) & 1);
-    kb_fill_async(xs + st * rows_tile * kXS, in + fc.b * in_bs, g, g.g0 + fc.s0 - g.H, rows_tile,
-                  fc.lt * 32 + lane, warp, lane, &full[st]);
+    mbar_arrive_expect_tx(&full[st], (unsigned)(tb.nbox * tb.box_rows * 36 * sizeof(double)));
+    const int row0 = fc.s0 - g.H + g.halo_lo;  // map row of tile row 0
+    for (int k = 0; k < tb.nbox; ++k)
+      tma_load_3d(xs + st * tb.stage_elems + k * tb.box_rows * kXS, &tmap, fc.lt * 32,
+                  row0 + k * tb.box_rows, fc.b, &full[st]);
     ++nfill;
   };
   for (int k = 0; k < kStages - 1; ++k) issue();
@@ -253,10 +298,10 @@ kb_pass_split_dmma(const double* __restrict__ in, long long in_bs, double* __res
   for (int t = 0; use_walk.next(ch, TS); ++t) {
     if (ch.b != taps_b) {  // per-image taps (uniform across the block: block-level reload)
       __syncthreads();
-      const double* tb = tin + ch.b * t_bs;
+      const double* tbp = tin + ch.b * t_bs;
       for (int idx = tid; idx < r * cstride; idx += 32 * kNW) {
         const int i = idx / cstride, k = idx - i * cstride - kCG;
-        cpad[idx] = (k >= 0 && k < g.Wp) ? tb[(long long)i * g.Wp + k] : 0.0;
+        cpad[idx] = (k >= 0 && k < g.Wp) ? tbp[(long long)i * g.Wp + k] : 0.0;
       }
       __syncthreads();
       taps_b = ch.b;
@@ -264,8 +309,9 @@ kb_pass_split_dmma(const double* __restrict__ in, long long in_bs, double* __res
     issue();  // keep kStages-1 tiles in flight ahead of the one consumed now
     const int st = t % kStages;
     mbar_wait(&full[st], (t / kStages) & 1);
-    const double* xt = xs + st * rows_tile * kXS;
+    const double* xt = xs + st * tb.stage_elems;
     const int row_lo = g.g0 + ch.s0 - g.H;
+    const bool edge = g.fill && (row_lo < 0 || row_lo + rows_tile > g.Mg);
     const double oscale = nw2 ? 1.0 / sqrt(nw2[ch.b]) : 1.0;
     double* zb = z + ch.b * z_bs;
     if (s_off < ch.cnt) {  // warp-uniform: warps past the chunk's rows idle
@@ -275,8 +321,8 @@ kb_pass_split_dmma(const double* __restrict__ in, long long in_bs, double* __res
 #define KB_DGROUP(C)                                                                                  \
   case C:                                                                                             \
     if constexpr (C <= GMAX)                                                                          \
-      kb_split_group_dmma<C>(xt, cb, cstride, g, s_off, lane, zb, z_ps, gstart, ch, oscale, row_lo,   \
-                             grp.sign[gi]);                                                           \
+      kb_split_group_dmma<C>(xt, cb, cstride, g, s_off, lane, zb, z_ps, gstart, ch, oscale,           \
+                             nw2 != nullptr, row_lo, edge, grp.sign[gi]);                             \
     break;
         switch (grp.count[gi]) {
           KB_DGROUP(1)
@@ -293,7 +339,6 @@ kb_pass_split_dmma(const double* __restrict__ in, long long in_bs, double* __res
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
 // ------------------------------------------------------------------------------------------
@@ -388,6 +433,35 @@ __device__ __forceinline__ void kb_warp_finish(const Epi<double>& e, double (&nr
   }
 }
 
+// MMA loop of one (chunk, term) tile of the sum pass (two m-tiles sharing the B fragment).
+template <bool EDGE>
+__device__ __forceinline__ void kb_sum_mma(double (&D)[2][4][2], const double* __restrict__ xs,
+                                           const double* __restrict__ cb, int nchr, int s_off,
+                                           int ar, int ac, int row_lo, int Mg, int rows, int sign,
+                                           bool two) {
+  const double* xb = xs + (s_off + ac) * kXS + ar;
+#pragma unroll 2
+  for (int c = 0; c < nchr; ++c) {
+    double mul = 1.0;
+    const double* xr = xb + 4 * c * kXS;
+    if constexpr (EDGE) xr = xs + kb_src_row(s_off + 4 * c + ac, row_lo, Mg, rows, sign, mul) * kXS + ar;
+    double B[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) B[j] = xr[8 * j];
+    double a0 = cb[4 * c];      // zero beyond the band
+    double a1 = cb[4 * c - 8];  // zero for c < 2 (guard)
+    if constexpr (EDGE) {
+      a0 *= mul;
+      a1 *= mul;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      dmma_884(D[0][j][0], D[0][j][1], a0, B[j]);
+      if (two) dmma_884(D[1][j][0], D[1][j][1], a1, B[j]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // sum pass (fp64, DMMA): warp w owns S rows [16w, 16w+16) (two m-tiles) x 32 L of a chunk;
 // the (chunk, term) tiles stream through the mbarrier ring; m-tile 1 reuses the B fragment of
@@ -396,16 +470,17 @@ __device__ __forceinline__ void kb_warp_finish(const Epi<double>& e, double (&nr
 // ------------------------------------------------------------------------------------------
 template <int MODE>
 __global__ void __launch_bounds__(32 * kNW, 2)
-kb_pass_sum_dmma(const double* __restrict__ z, long long z_ps, long long z_bs, int r,
-                 const double* __restrict__ tin, long long t_bs, AxisGeom g,
-                 const double* __restrict__ tsign, Epi<double> e, int batch, int parts) {
-  extern __shared__ __align__(16) unsigned char kb_smem_d[];
+kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* __restrict__ tin,
+                 long long t_bs, AxisGeom g, const double* __restrict__ tsign, Epi<double> e,
+                 int batch, int parts) {
+  extern __shared__ __align__(128) unsigned char kb_smem_d[];
   __shared__ unsigned long long full[kStages], empty[kStages];
   constexpr int TS = kNW * 16;
   const int rows_tile = dmma_rows(TS, g.Wp);
+  const TileBoxes tb = tile_boxes(rows_tile);
   const int cstride = dmma_cstride_sum(g.Wp);  // taps at offset kCG + 8 (m-tile 1 reads t0 - 8)
-  double* xs = reinterpret_cast<double*>(kb_smem_d);  // [kStages][rows_tile][kXS]
-  double* cpad = xs + kStages * rows_tile * kXS;       // [r][cstride]
+  double* xs = reinterpret_cast<double*>(kb_smem_d);  // [kStages][stage_elems]
+  double* cpad = xs + kStages * tb.stage_elems;        // [r][cstride]
   const int lane = threadIdx.x, warp = threadIdx.y;
   const int tid = warp * 32 + lane;
   const int LT = (g.other + 31) / 32;
@@ -416,21 +491,21 @@ kb_pass_sum_dmma(const double* __restrict__ z, long long z_ps, long long z_bs, i
 
   if (tid == 0) {
     for (int st = 0; st < kStages; ++st) {
-      mbar_init(&full[st], 32 * kNW);
+      mbar_init(&full[st], 1);
       mbar_init(&empty[st], kNW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
-  // tile sequence: (chunk, term) for every chunk of this block
+  // tile sequence: (chunk, term) for every chunk of this block; thread 0 issues the TMA boxes
   ChunkWalk fill_walk(g.len, LT, parts, batch), use_walk(g.len, LT, parts, batch);
   Chunk fc;
   int fterm = r;  // forces fetching the first chunk
   bool fmore = true;
   int nfill = 0;
   auto issue = [&]() {
-    if (!fmore) return;
+    if (tid != 0 || !fmore) return;
     if (fterm == r) {
       if (!fill_walk.next(fc, TS)) {
         fmore = false;
@@ -440,8 +515,11 @@ kb_pass_sum_dmma(const double* __restrict__ z, long long z_ps, long long z_bs, i
     }
     const int st = nfill % kStages;
     if (nfill >= kStages) mbar_wait(&empty[st], ((nfill / kStages) - 1) & 1);
-    kb_fill_async(xs + st * rows_tile * kXS, z + fc.b * z_bs + (long long)fterm * z_ps, g,
-                  g.g0 + fc.s0 - g.H, rows_tile, fc.lt * 32 + lane, warp, lane, &full[st]);
+    mbar_arrive_expect_tx(&full[st], (unsigned)(tb.nbox * tb.box_rows * 36 * sizeof(double)));
+    const int row0 = fc.s0 - g.H;  // Z^T planes are not row sharded
+    for (int k = 0; k < tb.nbox; ++k)
+      tma_load_3d(xs + st * tb.stage_elems + k * tb.box_rows * kXS, &tmap, fc.lt * 32,
+                  row0 + k * tb.box_rows, fc.b * r + fterm, &full[st]);
     ++fterm;
     ++nfill;
   };
@@ -475,7 +553,7 @@ kb_pass_sum_dmma(const double* __restrict__ z, long long z_ps, long long z_bs, i
 #pragma unroll
       for (int j = 0; j < 4; ++j) D[mt][j][0] = D[mt][j][1] = 0.0;
     const int row_lo = g.g0 + ch.s0 - g.H;
-    const int grow0 = row_lo + s_off + ac;
+    const bool edge = g.fill && (row_lo < 0 || row_lo + rows_tile > g.Mg);
     const bool active = s_off < ch.cnt;  // warp-uniform
     const bool two = s_off + 8 < ch.cnt;
     for (int term = 0; term < r; ++term, ++t) {
@@ -483,34 +561,19 @@ kb_pass_sum_dmma(const double* __restrict__ z, long long z_ps, long long z_bs, i
       const int st = t % kStages;
       mbar_wait(&full[st], (t / kStages) & 1);
       if (active) {
-        const double* xb = xs + st * rows_tile * kXS + (s_off + ac) * kXS + ar;
+        const double* xt = xs + st * tb.stage_elems;
         const double* cb = cpad + term * cstride + kCG + 8 + ac - ar;
-        const bool flip = g.fill && tsign && tsign[(long long)ch.b * r + term] < 0.0;
-#pragma unroll 2
-        for (int c = 0; c < nch + 2; ++c) {
-          double B[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) B[j] = xb[4 * c * kXS + 8 * j];
-          double a0 = cb[4 * c];      // zero beyond the band
-          double a1 = cb[4 * c - 8];  // zero for c < 2 (guard)
-          if (flip && (unsigned)(grow0 + 4 * c) >= (unsigned)g.Mg) {
-            a0 = -a0;
-            a1 = -a1;
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            dmma_884(D[0][j][0], D[0][j][1], a0, B[j]);
-            if (two) dmma_884(D[1][j][0], D[1][j][1], a1, B[j]);
-          }
-        }
+        const int sgn = (tsign && tsign[(long long)ch.b * r + term] < 0.0) ? -1 : 1;
+        const int nchr = (g.dbg & 1) ? 0 : nch + 2;
+        if (edge) kb_sum_mma<true>(D, xt, cb, nchr, s_off, ar, ac, row_lo, g.Mg, rows_tile, sgn, two);
+        else kb_sum_mma<false>(D, xt, cb, nchr, s_off, ar, ac, row_lo, g.Mg, rows_tile, sgn, two);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
-    if (active) kb_sum_epilogue_regs<MODE>(D, g, e, ch, s_off, ar, ac, nrm, bad);
+    if (active && !(g.dbg & 2)) kb_sum_epilogue_regs<MODE>(D, g, e, ch, s_off, ar, ac, nrm, bad);
   }
   if (norm_b >= 0) kb_warp_finish<MODE>(e, nrm, bad, norm_b, nslots, slot, lane);
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
 }  // namespace kb

@@ -53,6 +53,7 @@ struct AxisGeom {
   int Mg;       // global extent of the domain
   int halo_lo;  // readable entries before local 0
   int halo_hi;  // readable entries after local len-1
+  int dbg;      // profiling switch (KB_DEBUG_MODE): bit0 skip MMAs, bit1 skip result stores
 };
 
 template <typename T>
