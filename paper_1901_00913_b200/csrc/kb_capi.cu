@@ -21,6 +21,7 @@
 #include "../../include/kronblur_b200.h"
 #include "kb_kernels.cuh"
 #include "kb_dmma.cuh"
+#include "kb_ffma.cuh"
 
 namespace {
 
@@ -101,10 +102,11 @@ int persistent_blocks() {
   return nb;
 }
 
-// TMA descriptor of a 3-D [planes][rows][cols] fp64 array (cols contiguous) with a
-// {36 cols x box_rows} box; false when TMA's alignment rules rule it out (caller falls back).
+// TMA descriptor of a 3-D [planes][rows][cols] array (cols contiguous) with a {box_cols x
+// box_rows} box: fp64 tiles are 36 columns wide (padded rows for the DMMA fragments), fp32 tiles
+// 32 (128-byte rows). False when TMA's alignment rules rule it out.
 bool make_tmap(CUtensorMap* map, const void* base, long long cols, long long rows, long long planes,
-               long long row_stride, long long plane_stride, int box_rows) {
+               long long row_stride, long long plane_stride, int box_rows, int esize = 8) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   static bool tried = false;
   if (!tried) {
@@ -116,24 +118,30 @@ bool make_tmap(CUtensorMap* map, const void* base, long long cols, long long row
       encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   if (!encode) return false;
-  if (reinterpret_cast<uintptr_t>(base) % 16 || (row_stride * 8) % 16 || (plane_stride * 8) % 16) return false;
+  if (reinterpret_cast<uintptr_t>(base) % 16 || (row_stride * esize) % 16 || (plane_stride * esize) % 16)
+    return false;
   if (box_rows < 1 || box_rows > 256) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)planes};
-  const cuuint64_t strides[2] = {(cuuint64_t)row_stride * 8, (cuuint64_t)plane_stride * 8};
-  const cuuint32_t box[3] = {36, (cuuint32_t)box_rows, 1};
+  const cuuint64_t strides[2] = {(cuuint64_t)row_stride * esize, (cuuint64_t)plane_stride * esize};
+  const cuuint32_t box[3] = {esize == 8 ? 36u : 32u, (cuuint32_t)box_rows, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
-  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
+  return encode(map, esize == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                const_cast<void*>(base), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // fp64 runs on the TMA + DMMA kernels when both image extents are even (16-byte row strides)
 bool use_dmma(const kb_op* op) { return op->dtype == KB_F64 && op->m % 2 == 0 && op->n % 2 == 0; }
+// fp32 runs on the persistent TMA + FFMA kernels when both extents are multiples of 4 (16-byte
+// row strides and vector stores); other shapes take the generic tiled kernels.
+bool use_tma_f32(const kb_op* op) { return op->dtype == KB_F32 && op->m % 4 == 0 && op->n % 4 == 0; }
+bool persistent_sum(const kb_op* op) { return use_dmma(op) || use_tma_f32(op); }
 
 // Norm partial slots of the sum pass per image: one per warp (fp64 persistent kernel) or
 // one per block (fp32).
 int sum_blocks(const kb_op* op) {
-  if (use_dmma(op)) {  // per-warp slots
+  if (persistent_sum(op)) {  // per-warp slots
     int parts, nb;
     kb::plan_items(op->n, (op->m + 31) / 32, op->batch, persistent_blocks(), parts, nb);
     return nb * kb::kNW;
@@ -244,6 +252,22 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
     }
     return launch_a_g<T, kGmaxF64>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
   } else {
+    if (use_tma_f32(op)) {
+      const kb::TileBoxesF tb = kb::tile_boxes_f(kb::kNW * 8 + g.Wp);
+      CUtensorMap map;
+      if (!make_tmap(&map, in - (long long)g.halo_lo * g.other, g.other, g.len + g.halo_lo + g.halo_hi,
+                     op->batch, g.other, in_bs, tb.box_rows, 4))
+        return fail(KB_ERR_ARGUMENT, "input plane not 16-byte aligned for TMA");
+      const size_t smem = sizeof(float) * ((size_t)kb::kStages * tb.stage_elems + (size_t)op->r * g.Wp);
+      auto kern = kb::kb_pass_split_f<kGmaxF32>;
+      KB_TRY(allow_smem(kern, smem));
+      int parts, nb;
+      kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
+      kern<<<nb, dim3(32, kb::kNW), smem, s>>>(map, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r,
+                                               op->batch, parts);
+      KB_CUDA(cudaGetLastError());
+      return KB_OK;
+    }
     return launch_a_g<T, kGmaxF32>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
   }
 }
@@ -265,6 +289,25 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g, c
       int parts, nb;
       kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
       if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // warps skip untouched images
+        KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kNW, s));
+      kern<<<nb, dim3(32, kb::kNW), smem, s>>>(map, op->r, tin, (long long)op->r * g.Wp, g, tsign, e,
+                                               op->batch, parts);
+      KB_CUDA(cudaGetLastError());
+      return KB_OK;
+    }
+  } else {
+    if (use_tma_f32(op)) {
+      const kb::TileBoxesF tb = kb::tile_boxes_f(kb::kNW * 16 + g.Wp);
+      const long long z_ps = (long long)g.len * g.other;
+      CUtensorMap map;
+      if (!make_tmap(&map, z, g.other, g.len, (long long)op->batch * op->r, g.other, z_ps, tb.box_rows, 4))
+        return fail(KB_ERR_ARGUMENT, "intermediate planes not 16-byte aligned for TMA");
+      const size_t smem = sizeof(float) * ((size_t)kb::kStages * tb.stage_elems + (size_t)op->r * g.Wp);
+      auto kern = kb::kb_pass_sum_f<MODE>;
+      KB_TRY(allow_smem(kern, smem));
+      int parts, nb;
+      kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
+      if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))
         KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kNW, s));
       kern<<<nb, dim3(32, kb::kNW), smem, s>>>(map, op->r, tin, (long long)op->r * g.Wp, g, tsign, e,
                                                op->batch, parts);

@@ -133,7 +133,9 @@ struct ChunkWalk {
   long long it, it_end;
   int S, LT, parts;
   int b = 0, lt = 0, s = 0, s_end = 0;
-  __device__ ChunkWalk(int S_, int LT_, int parts_, int batch) : S(S_), LT(LT_), parts(parts_) {
+  int align;  // part boundaries rounded down to multiples of `align` rows (vector stores)
+  __device__ ChunkWalk(int S_, int LT_, int parts_, int batch, int align_ = 1)
+      : S(S_), LT(LT_), parts(parts_), align(align_) {
     const long long I = (long long)batch * LT * parts;
     it = I * blockIdx.x / gridDim.x;
     it_end = I * (blockIdx.x + 1) / gridDim.x;
@@ -145,8 +147,8 @@ struct ChunkWalk {
     const int part = (int)(it - q * parts);
     b = (int)(q / LT);
     lt = (int)(q - (long long)b * LT);
-    s = (int)((long long)part * S / parts);
-    s_end = (int)((long long)(part + 1) * S / parts);
+    s = (int)((long long)part * S / parts) / align * align;
+    s_end = part + 1 == parts ? S : (int)((long long)(part + 1) * S / parts) / align * align;
   }
   __device__ bool next(Chunk& c, int TS) {
     while (it < it_end) {
