@@ -74,12 +74,19 @@ struct kb_op {
   void* tb_conv = nullptr;
   void* tb_corr = nullptr;
   GraphCache* graph = nullptr;
+  mutable int last_mirror = 0;  // the latest split pass stored Z^T's reflected halo rows
+  mutable int last_slots = 0;  // norm partial slots per image written by the latest sum pass
 };
 
 namespace {
 
 size_t elem(const kb_op* op) { return op->dtype == KB_F64 ? 8 : 4; }
 size_t plane_elems(const kb_op* op) { return (size_t)op->m * op->n; }
+// Z_i^T planes are [n + 2 Hb][m]: Hb halo rows on each side hold the reflected rows the
+// persistent split kernels store for a reflect-filled sum pass (kb_dmma.cuh, kb_ffma.cuh).
+long long z_plane(const kb_op* op) { return (long long)(op->n + 2 * op->Hb) * op->m; }
+template <typename T>
+T* z_row0(const kb_op* op, void* z) { return static_cast<T*>(z) + (long long)op->Hb * op->m; }
 
 // workspace: [Z: batch*r planes][R: batch planes][partials][scalars]
 struct Work {
@@ -136,19 +143,26 @@ bool use_dmma(const kb_op* op) { return op->dtype == KB_F64 && op->m % 2 == 0 &&
 // fp32 runs on the persistent TMA + FFMA kernels when both extents are multiples of 4 (16-byte
 // row strides and vector stores); other shapes take the generic tiled kernels.
 bool use_tma_f32(const kb_op* op) { return op->dtype == KB_F32 && op->m % 4 == 0 && op->n % 4 == 0; }
-bool persistent_sum(const kb_op* op) { return use_dmma(op) || use_tma_f32(op); }
+bool al16(const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; }
+// the persistent sum kernels move epilogue operands as 16-byte vectors
+template <typename T>
+bool epi_aligned(const kb::Epi<T>& e) {
+  return al16(e.out) && al16(e.bsub) && al16(e.x) && al16(e.y) && al16(e.vin);
+}
 
-// Norm partial slots of the sum pass per image: one per warp (fp64 persistent kernel) or
-// one per block (fp32).
-int sum_blocks(const kb_op* op) {
-  if (persistent_sum(op)) {  // per-warp slots
-    int parts, nb;
-    kb::plan_items(op->n, (op->m + 31) / 32, op->batch, persistent_blocks(), parts, nb);
-    return nb * kb::kNW;
-  }
+// Norm partial slots of the sum pass per image: one per warp of the persistent kernels, one
+// per block of the generic tiled kernel (used for shapes / pointers the persistent kernels
+// do not take). The workspace holds the larger count; each launch records its own.
+int persistent_slots(const kb_op* op) {
+  int parts, nb;
+  kb::plan_items(op->n, (op->m + 31) / 32, op->batch, persistent_blocks(), parts, nb);
+  return nb * kb::kNW;
+}
+int generic_slots(const kb_op* op) {
   const int TS = kb::kNW * kRB;
   return ((op->n + TS - 1) / TS) * ((op->m + 31) / 32);
 }
+int sum_blocks(const kb_op* op) { return std::max(persistent_slots(op), generic_slots(op)); }
 
 Work layout(const kb_op* op, void* base) {
   Work w;
@@ -156,7 +170,7 @@ Work layout(const kb_op* op, void* base) {
   const size_t pe = plane_elems(op) * elem(op);
   unsigned char* b = static_cast<unsigned char*>(base);
   w.z = b ? b + off : nullptr;
-  off = align_up(off + pe * op->r * op->batch, 256);
+  off = align_up(off + (size_t)z_plane(op) * elem(op) * op->r * op->batch, 256);
   w.rp = b ? b + off : nullptr;
   off = align_up(off + pe * op->batch, 256);
   w.fold = b ? b + off : nullptr;
@@ -224,64 +238,79 @@ int launch_a_g(const T* in, long long in_bs, T* z, long long z_ps, long long z_b
   return KB_OK;
 }
 
+// Pass A into the Z^T planes (z: row 0 of image 0, term 0). mirror_h > 0 asks the persistent
+// kernels to also store the reflected halo rows (times msign[b][i]) for a reflect-filled pass B;
+// op->last_mirror records whether they did.
 template <typename T>
 int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeom& g,
-             const kb::Groups& grp, const double* nw2, cudaStream_t s) {
+             const kb::Groups& grp, const double* nw2, int mirror_h, const T* msign, cudaStream_t s) {
   const long long in_bs = (long long)plane_elems(op);
-  const long long z_ps = (long long)g.len * g.other;
+  const long long z_ps = z_plane(op);
+  op->last_mirror = 0;
   const long long z_bs = z_ps * op->r;
   const long long t_bs = (long long)op->r * g.Wp;
   if constexpr (sizeof(T) == 8) {
     constexpr int TS = kb::kNW * 8;
     const kb::TileBoxes tb = kb::tile_boxes(kb::dmma_rows(TS, g.Wp));
     CUtensorMap map;
-    if (use_dmma(op)) {
-      if (!make_tmap(&map, in - (long long)g.halo_lo * g.other, g.other, g.len + g.halo_lo + g.halo_hi,
-                     op->batch, g.other, in_bs, tb.box_rows))
-        return fail(KB_ERR_ARGUMENT, "input plane not 16-byte aligned for TMA");
+    if (use_dmma(op) && make_tmap(&map, in - (long long)g.halo_lo * g.other, g.other,
+                                  g.len + g.halo_lo + g.halo_hi, op->batch, g.other, in_bs, tb.box_rows)) {
       const size_t smem = sizeof(double) * ((size_t)kb::kStages * tb.stage_elems +
                                             (size_t)op->r * kb::dmma_cstride_split(g.Wp));
       auto kern = kb::kb_pass_split_dmma<kGmaxF64>;
       KB_TRY(allow_smem(kern, smem));
-      int parts, nb;
-      kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
+      int parts, nb, eparts;  // edge L-tiles also store the reflected halo rows: smaller parts
+      kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb,
+                     mirror_h > 0 ? &eparts : nullptr);
+      if (mirror_h == 0) eparts = parts;
       kern<<<nb, dim3(32, kb::kNW), smem, s>>>(map, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r,
-                                               op->batch, parts);
+                                               op->batch, parts, eparts, mirror_h, msign);
       KB_CUDA(cudaGetLastError());
+      op->last_mirror = mirror_h > 0;
       return KB_OK;
     }
     return launch_a_g<T, kGmaxF64>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
   } else {
-    if (use_tma_f32(op)) {
-      const kb::TileBoxesF tb = kb::tile_boxes_f(kb::kNW * 8 + g.Wp);
-      CUtensorMap map;
-      if (!make_tmap(&map, in - (long long)g.halo_lo * g.other, g.other, g.len + g.halo_lo + g.halo_hi,
-                     op->batch, g.other, in_bs, tb.box_rows, 4))
-        return fail(KB_ERR_ARGUMENT, "input plane not 16-byte aligned for TMA");
+    const kb::TileBoxesF tb = kb::tile_boxes_f(kb::kNW * 8 + g.Wp);
+    CUtensorMap map;
+    if (use_tma_f32(op) && make_tmap(&map, in - (long long)g.halo_lo * g.other, g.other,
+                                     g.len + g.halo_lo + g.halo_hi, op->batch, g.other, in_bs,
+                                     tb.box_rows, 4)) {
       const size_t smem = sizeof(float) * ((size_t)kb::kStages * tb.stage_elems + (size_t)op->r * g.Wp);
       auto kern = kb::kb_pass_split_f<kGmaxF32>;
       KB_TRY(allow_smem(kern, smem));
-      int parts, nb;
-      kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
+      int parts, nb, eparts;  // edge L-tiles also store the reflected halo rows: smaller parts
+      kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb,
+                     mirror_h > 0 ? &eparts : nullptr);
+      if (mirror_h == 0) eparts = parts;
       kern<<<nb, dim3(32, kb::kNW), smem, s>>>(map, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r,
-                                               op->batch, parts);
+                                               op->batch, parts, eparts, mirror_h, msign);
       KB_CUDA(cudaGetLastError());
+      op->last_mirror = mirror_h > 0;
       return KB_OK;
     }
     return launch_a_g<T, kGmaxF32>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
   }
 }
 
+// Pass B over the Z^T planes (z: row 0 of image 0, term 0). The persistent kernels read a
+// reflect-filled pass's out-of-domain rows from the halo rows the split pass stored (the TMA
+// map then spans them: halo_lo = Hb); without them the generic kernel folds at read time.
 template <typename T, int MODE>
-int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g, const T* tsign,
+int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in, const T* tsign,
              const kb::Epi<T>& e, cudaStream_t s) {
+  const long long z_ps = z_plane(op);
+  const bool mirrored = g_in.fill && op->last_mirror;
+  kb::AxisGeom g = g_in;
+  if (mirrored) g.halo_lo = g.halo_hi = op->Hb;
+  const T* zmap = z - (long long)g.halo_lo * g.other;
+  const long long zrows = g.len + g.halo_lo + g.halo_hi;
+  const bool persistent_ok = (!g_in.fill || mirrored) && epi_aligned(e);
   if constexpr (sizeof(T) == 8) {
     const kb::TileBoxes tb = kb::tile_boxes(kb::dmma_rows(kb::kNW * 16, g.Wp));
-    const long long z_ps = (long long)g.len * g.other;
     CUtensorMap map;
-    if (use_dmma(op)) {
-      if (!make_tmap(&map, z, g.other, g.len, (long long)op->batch * op->r, g.other, z_ps, tb.box_rows))
-        return fail(KB_ERR_ARGUMENT, "intermediate planes not 16-byte aligned for TMA");
+    if (use_dmma(op) && persistent_ok &&
+        make_tmap(&map, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, tb.box_rows)) {
       const size_t smem = sizeof(double) * ((size_t)kb::kStages * tb.stage_elems +
                                             (size_t)op->r * kb::dmma_cstride_sum(g.Wp));
       auto kern = kb::kb_pass_sum_dmma<MODE>;
@@ -290,18 +319,17 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g, c
       kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
       if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // warps skip untouched images
         KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kNW, s));
-      kern<<<nb, dim3(32, kb::kNW), smem, s>>>(map, op->r, tin, (long long)op->r * g.Wp, g, tsign, e,
+      op->last_slots = nb * kb::kNW;
+      kern<<<nb, dim3(32, kb::kNW), smem, s>>>(map, op->r, tin, (long long)op->r * g.Wp, g, e,
                                                op->batch, parts);
       KB_CUDA(cudaGetLastError());
       return KB_OK;
     }
   } else {
-    if (use_tma_f32(op)) {
-      const kb::TileBoxesF tb = kb::tile_boxes_f(kb::kNW * 16 + g.Wp);
-      const long long z_ps = (long long)g.len * g.other;
-      CUtensorMap map;
-      if (!make_tmap(&map, z, g.other, g.len, (long long)op->batch * op->r, g.other, z_ps, tb.box_rows, 4))
-        return fail(KB_ERR_ARGUMENT, "intermediate planes not 16-byte aligned for TMA");
+    const kb::TileBoxesF tb = kb::tile_boxes_f(kb::kNW * 16 + g.Wp);
+    CUtensorMap map;
+    if (use_tma_f32(op) && persistent_ok &&
+        make_tmap(&map, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, tb.box_rows, 4)) {
       const size_t smem = sizeof(float) * ((size_t)kb::kStages * tb.stage_elems + (size_t)op->r * g.Wp);
       auto kern = kb::kb_pass_sum_f<MODE>;
       KB_TRY(allow_smem(kern, smem));
@@ -309,7 +337,8 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g, c
       kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
       if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))
         KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kNW, s));
-      kern<<<nb, dim3(32, kb::kNW), smem, s>>>(map, op->r, tin, (long long)op->r * g.Wp, g, tsign, e,
+      op->last_slots = nb * kb::kNW;
+      kern<<<nb, dim3(32, kb::kNW), smem, s>>>(map, op->r, tin, (long long)op->r * g.Wp, g, e,
                                                op->batch, parts);
       KB_CUDA(cudaGetLastError());
       return KB_OK;
@@ -319,11 +348,12 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g, c
   const size_t smem = sizeof(T) * (2 * (size_t)(TS + g.Wp) * 32 + 2 * (size_t)g.Wp);
   auto kern = kb::kb_pass_sum<T, kRB, MODE>;
   KB_TRY(allow_smem(kern, smem));
-  const long long z_ps = (long long)g.len * g.other;
+  g = g_in;
   const long long z_bs = z_ps * op->r;
   const long long t_bs = (long long)op->r * g.Wp;
   dim3 grid((g.other + 31) / 32, (g.len + TS - 1) / TS, op->batch);
   dim3 block(32, kb::kNW);
+  op->last_slots = (int)(grid.x * grid.y);
   kern<<<grid, block, smem, s>>>(z, z_ps, z_bs, op->r, tin, t_bs, g, tsign, e);
   KB_CUDA(cudaGetLastError());
   return KB_OK;
@@ -387,16 +417,22 @@ kb::Epi<T> epi_base(const kb_op* op, int mode) {
 template <typename T>
 int stage_a(const kb_op* op, int adjoint, const T* in, const Work& w, const RowBlock& rb,
             const double* nw2, cudaStream_t s) {
-  T* z = static_cast<T*>(w.z);
+  T* z = z_row0<T>(op, w.z);
   const kb::AxisGeom ga = geom_a(op, adjoint, rb);
+  // the following pass B reflect-fills axis 1: let the split store Z^T's reflected halo rows
+  const int mirror_h = geom_b(op, adjoint).fill ? op->Hb : 0;
+  const T* msign = (adjoint && op->sym_b) ? static_cast<const T*>(op->sign_b) : nullptr;
+  if (mirror_h > op->n)  // folds leaving the domain: those halo rows must read as zero
+    KB_CUDA(cudaMemsetAsync(w.z, 0, (size_t)z_plane(op) * op->r * op->batch * sizeof(T), s));
   KB_TRY(launch_a<T>(op, in, z, static_cast<const T*>(adjoint ? op->ta_corr : op->ta_conv), ga,
-                     adjoint ? op->grp_adj : op->grp_fwd, nw2, s));
+                     adjoint ? op->grp_adj : op->grp_fwd, nw2, mirror_h, msign, s));
   if (adjoint && op->bc_a == KB_BC_REFLECTIVE && !op->sym_a && op->Ha > 0) {
-    const long long z_ps = (long long)op->m * op->n;
+    const long long z_ps = z_plane(op);
     dim3 grid((op->n + 127) / 128, 2 * op->Ha * op->r, op->batch);
-    kb::kb_fold_split<T><<<grid, 128, 0, s>>>(in, z_ps, z, z_ps, z_ps * op->r, op->r,
+    kb::kb_fold_split<T><<<grid, 128, 0, s>>>(in, (long long)plane_elems(op), z, z_ps, z_ps * op->r, op->r,
                                                static_cast<const T*>(op->ta_conv),
-                                               (long long)op->r * op->Wpa, ga);
+                                               (long long)op->r * op->Wpa, ga,
+                                               op->last_mirror ? mirror_h : 0, msign);
     KB_CUDA(cudaGetLastError());
   }
   return KB_OK;
@@ -404,11 +440,11 @@ int stage_a(const kb_op* op, int adjoint, const T* in, const Work& w, const RowB
 
 template <typename T, int MODE>
 int stage_b(const kb_op* op, int adjoint, kb::Epi<T> e, const Work& w, cudaStream_t s) {
-  const T* z = static_cast<const T*>(w.z);
+  const T* z = z_row0<T>(op, w.z);
   const kb::AxisGeom gb = geom_b(op, adjoint);
   if (adjoint && op->bc_b == KB_BC_REFLECTIVE && !op->sym_b && op->Hb > 0) {
     dim3 grid((op->m + 127) / 128, 2 * op->Hb, op->batch);
-    const long long z_ps = (long long)op->m * op->n;
+    const long long z_ps = z_plane(op);
     kb::kb_fold_sum_pass<T><<<grid, 128, 0, s>>>(z, z_ps, z_ps * op->r, op->r,
                                                   static_cast<const T*>(op->tb_conv),
                                                   (long long)op->r * op->Wpb, gb,
@@ -468,7 +504,7 @@ int update_t(const kb_op* op, const T* R, T* X, T* Y, const Work& w, const RowBl
   KB_TRY((stage_b<T, kb::EPI_UPDATE>(op, 1, update_epi<T>(op, X, Y, w, beta, k, Ldev, ddev, project,
                                                           nonfinite, norms_out != nullptr), w, s)));
   if (norms_out) {
-    kb::kb_reduce_partials<<<op->batch, 256, 0, s>>>(w.partials, sum_blocks(op), 3, norms_out,
+    kb::kb_reduce_partials<<<op->batch, 256, 0, s>>>(w.partials, op->last_slots, 3, norms_out,
                                                       op->batch, 1);
     KB_CUDA(cudaGetLastError());
   }
@@ -510,7 +546,7 @@ int power_t(const kb_op* op, T* v, T* wbuf, const Work& w, int iters, double* hi
     e2.vnw2 = nw2;
     e2.partials = w.partials;
     KB_TRY((stage_b<T, kb::EPI_POWER>(op, 1, e2, w, s)));
-    kb::kb_reduce_partials<<<op->batch, 256, 0, s>>>(w.partials, sum_blocks(op), 2,
+    kb::kb_reduce_partials<<<op->batch, 256, 0, s>>>(w.partials, op->last_slots, 2,
                                                       hist + (size_t)k * 2 * op->batch,
                                                       op->batch, 1);
     KB_CUDA(cudaGetLastError());
@@ -640,11 +676,18 @@ int fma_peak_t(float* tflops, cudaStream_t s) {
   return KB_OK;
 }
 
+// Per-phase GPU time of one iteration's four kernels: each phase's `reps` launches are
+// captured into a CUDA graph (as in the solver's fast path, so host launch cost is excluded)
+// and the graph is timed with events on a private stream.
 template <typename T>
 int time_passes_t(const kb_op* op, const T* Y, const T* B, T* R, T* X, T* Yio, const Work& w,
-                  int reps, float* ms4, int* nonfinite, cudaStream_t s) {
-  cudaEvent_t ev[8];
-  for (auto& e : ev) cudaEventCreate(&e);
+                  int reps, float* ms4, int* nonfinite, cudaStream_t caller) {
+  cudaStream_t s;
+  KB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  KB_CUDA(cudaStreamSynchronize(caller));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
   const RowBlock rb{0, op->m, 0, 0};
   kb::Epi<T> er = epi_base<T>(op, kb::EPI_RESID);
   er.out = R;
@@ -653,8 +696,13 @@ int time_passes_t(const kb_op* op, const T* Y, const T* B, T* R, T* X, T* Yio, c
                                       nonfinite, false);
   int rc = KB_OK;
   for (int phase = 0; phase < 4 && rc == KB_OK; ++phase) {
-    for (int rep = -1; rep < reps && rc == KB_OK; ++rep) {  // rep -1: untimed warm-up
-      if (rep == 0) cudaEventRecord(ev[2 * phase], s);
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      rc = fail(KB_ERR_CUDA, "stream capture failed");
+      break;
+    }
+    for (int rep = 0; rep < reps && rc == KB_OK; ++rep) {
       switch (phase) {
         case 0: rc = stage_a<T>(op, 0, Y, w, rb, nullptr, s); break;
         case 1: rc = stage_b<T, kb::EPI_RESID>(op, 0, er, w, s); break;
@@ -662,20 +710,29 @@ int time_passes_t(const kb_op* op, const T* Y, const T* B, T* R, T* X, T* Yio, c
         default: rc = stage_b<T, kb::EPI_UPDATE>(op, 1, eu, w, s); break;
       }
     }
-    cudaEventRecord(ev[2 * phase + 1], s);
-  }
-  cudaError_t ce = cudaEventSynchronize(ev[7]);
-  if (rc == KB_OK && ce == cudaSuccess) {
-    for (int phase = 0; phase < 4; ++phase) {
+    cudaError_t ce = cudaStreamEndCapture(s, &graph);
+    if (rc == KB_OK && ce == cudaSuccess) ce = cudaGraphInstantiate(&exec, graph, 0);
+    if (rc == KB_OK && ce == cudaSuccess) ce = cudaGraphLaunch(exec, s);  // warm-up
+    if (rc == KB_OK && ce == cudaSuccess) {
+      cudaEventRecord(e0, s);
+      ce = cudaGraphLaunch(exec, s);
+      cudaEventRecord(e1, s);
+    }
+    if (rc == KB_OK && ce == cudaSuccess) ce = cudaEventSynchronize(e1);
+    if (rc == KB_OK && ce == cudaSuccess) {
       float ms = 0.f;
-      cudaEventElapsedTime(&ms, ev[2 * phase], ev[2 * phase + 1]);
+      cudaEventElapsedTime(&ms, e0, e1);
       ms4[phase] = ms / reps;
     }
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    if (rc == KB_OK && ce != cudaSuccess) rc = fail(KB_ERR_CUDA, cudaGetErrorString(ce));
   }
-  for (auto& e : ev) cudaEventDestroy(e);
-  if (rc != KB_OK) return rc;
-  if (ce != cudaSuccess) return fail(KB_ERR_CUDA, cudaGetErrorString(ce));
-  return KB_OK;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  return rc;
 }
 
 }  // namespace

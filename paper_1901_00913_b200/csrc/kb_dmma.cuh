@@ -4,22 +4,22 @@
 // DMMA, measured at 37 TF/s on the box (DFMA: 34 TF/s, tools/microbench.cu). One DMMA is 256
 // FMAs and its operands are single registers.
 //
-// A banded pass out[s] = sum_k c[k] x[s + k] over an 8-row output block is the product
-//     Out(8 x 8 cols) = T(8 x (Wp+7)) * X((Wp+7) x 8 cols),   T[s][t] = c[t - s],
-// cut into K-chunks of 4: the A fragment of chunk t0 is the Toeplitz slice c[t0 + col - row]
-// (read from a zero-guarded copy of the taps), the B fragment is 4 input rows of the tile.
-// The structural overhead is (Wp+7)/Wp (11% at Wp = 64). Fragment layouts (m8n8k4.f64):
+// A banded pass out[s] = sum_k c[k] x[s + k] for 8 consecutive outputs s and 8 columns l is
+//     Out^T(8 l x 8 s) = X^T(8 l x (Wp+7)) * T((Wp+7) x 8 s),   T[t][s] = c[t - s],
+// cut into K-chunks of 4: the A fragment is 4 input rows of the shared-memory tile read
+// transposed, the B fragment the Toeplitz slice c[t0 + row - col] of a zero-guarded tap copy.
+// The accumulator then holds, per lane, two consecutive outputs s of one column l, which is
+// the layout of the transposed outputs (Z_i^T[l][s], Y[m][n]): results leave as 16-byte
+// vectors. Structural overhead (Wp+7)/Wp (11% at Wp = 64). Fragment layouts (m8n8k4.f64):
 //   A: lane holds A[lane/4][lane%4];  B: B[lane%4][lane/4];  C: C[lane/4][2*(lane%4) + i].
 //
 // Both kernels are persistent (balanced (image, L-tile, S-part) work items, one block per
-// SM slot) and stream their input tiles through a shared-memory ring synchronised with
-// mbarriers, not block barriers: every thread issues its share of a tile as cp.async and arms
-// the stage's "full" barrier with cp.async.mbarrier.arrive; every warp releases a stage on its
-// "empty" barrier once its MMAs have read it. Warps therefore drift within the ring, and one
-// warp's epilogue (straight from its accumulators to global memory) overlaps the other warps'
-// MMAs. Out-of-domain tile rows are cp.async'd from their folded source row (or zero-filled);
-// the (anti)symmetric adjoint's fill sign is applied to the A fragment of those rows, so tiles
-// are never rewritten in shared memory.
+// SM slot). Thread 0 streams the input tiles by TMA (cp.async.bulk.tensor) into a ring of
+// shared-memory stages guarded by mbarriers ("full": transaction bytes landed, "empty": every
+// warp has read the stage). Warps synchronise only through the ring. For a reflect-filled pass
+// the out-of-domain rows of a tile at a domain edge are rewritten in shared memory from their
+// folded partner row (times the (anti)symmetric adjoint's sign) before the MMAs; edge tiles
+// are block-uniform and rare, interior tiles are used exactly as TMA delivered them.
 #pragma once
 #include <cuda.h>  // CUtensorMap
 
@@ -69,6 +69,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, u
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// order this thread's generic-proxy shared-memory writes before later async-proxy (TMA) access
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
 // TMA: 3-D box of `map` at (c0 = column, c1 = row, c2 = plane) -> shared memory, completion
 // counted in bytes on `bar`; out-of-range coordinates are zero-filled by the hardware
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
@@ -93,25 +97,6 @@ __host__ __device__ __forceinline__ TileBoxes tile_boxes(int rows) {
   return t;
 }
 
-// Tile row whose data stands in for tile row tr of a reflect-filled pass: rows outside the
-// domain read their folded partner inside the tile scaled by `sign` (at a domain edge the TMA
-// box contains every partner an in-chunk output needs). A fold leaving the domain or the tile
-// keeps the (zero-filled, out-of-range) row itself with weight 0: DMMA multiplies every B row by
-// the whole A column, so even zero-weighted rows must hold finite values.
-__device__ __forceinline__ int kb_src_row(int tr, int row_lo, int Mg, int rows, int sign, double& mul) {
-  const int gr = row_lo + tr;
-  mul = 1.0;
-  if (gr >= 0 && gr < Mg) return tr;
-  const int f = kb_fold(gr, Mg);
-  const int u = f - row_lo;
-  if (f < 0 || u < 0 || u >= rows) {
-    mul = 0.0;
-    return tr;
-  }
-  mul = (double)sign;
-  return u;
-}
-
 // K-chunk count covering t in [0, Wp + 7) for one 8-row output block
 __host__ __device__ __forceinline__ int dmma_chunks(int Wp) { return (Wp + 7 + 3) / 4; }
 // rows of the input tile the DMMA kernels read for TS outputs
@@ -131,24 +116,37 @@ struct Chunk {
 
 struct ChunkWalk {
   long long it, it_end;
-  int S, LT, parts;
+  int S, LT, parts, eparts, align;
   int b = 0, lt = 0, s = 0, s_end = 0;
-  int align;  // part boundaries rounded down to multiples of `align` rows (vector stores)
-  __device__ ChunkWalk(int S_, int LT_, int parts_, int batch, int align_ = 1)
-      : S(S_), LT(LT_), parts(parts_), align(align_) {
-    const long long I = (long long)batch * LT * parts;
+  // eparts: S-parts of the two edge L-tiles (0 and LT-1), which may carry extra work
+  __device__ ChunkWalk(int S_, int LT_, int parts_, int batch, int align_ = 1, int eparts_ = 0)
+      : S(S_), LT(LT_), parts(parts_), eparts(eparts_ > 0 ? eparts_ : parts_), align(align_) {
+    const long long I = (long long)batch * per_image();
     it = I * blockIdx.x / gridDim.x;
     it_end = I * (blockIdx.x + 1) / gridDim.x;
     load();
   }
+  __device__ int per_image() const { return LT >= 2 ? (LT - 2) * parts + 2 * eparts : eparts; }
   __device__ void load() {
     if (it >= it_end) return;
-    const long long q = it / parts;
-    const int part = (int)(it - q * parts);
-    b = (int)(q / LT);
-    lt = (int)(q - (long long)b * LT);
-    s = (int)((long long)part * S / parts) / align * align;
-    s_end = part + 1 == parts ? S : (int)((long long)(part + 1) * S / parts) / align * align;
+    const int pi = per_image();
+    b = (int)(it / pi);
+    int i = (int)(it - (long long)b * pi), np;
+    if (i < eparts) {
+      lt = 0;
+      np = eparts;
+    } else if (LT >= 2 && i >= eparts + (LT - 2) * parts) {
+      lt = LT - 1;
+      i -= eparts + (LT - 2) * parts;
+      np = eparts;
+    } else {
+      i -= eparts;
+      lt = 1 + i / parts;
+      i -= (lt - 1) * parts;
+      np = parts;
+    }
+    s = (int)((long long)i * S / np) / align * align;
+    s_end = i + 1 == np ? S : (int)((long long)(i + 1) * S / np) / align * align;
   }
   __device__ bool next(Chunk& c, int TS) {
     while (it < it_end) {
@@ -169,7 +167,7 @@ struct ChunkWalk {
 
 // Host side: items per L-tile and grid size for a persistent pass over S rows x LT L-tiles
 // (x batch). Minimises (waves of items) x (rows per item, rounded to m-tiles, + fill overhead).
-inline void plan_items(int S, int LT, int batch, int max_blocks, int& parts, int& nb) {
+inline void plan_items(int S, int LT, int batch, int max_blocks, int& parts, int& nb, int* eparts = nullptr) {
   long long best = -1;
   parts = 1;
   for (int p = 1; p <= S; ++p) {
@@ -183,46 +181,80 @@ inline void plan_items(int S, int LT, int batch, int max_blocks, int& parts, int
       parts = p;
     }
   }
-  const long long items = (long long)batch * LT * parts;
+  long long items = (long long)batch * LT * parts;
+  if (eparts) {  // one more S-part on each edge L-tile when that still fits the same wave
+    *eparts = parts;
+    const long long more = (long long)batch * (LT >= 2 ? 2 : 1);
+    const long long waves = (items + max_blocks - 1) / max_blocks;
+    if (parts < S / 16 && items + more <= waves * max_blocks) {
+      *eparts = parts + 1;
+      items += more;
+    }
+  }
   nb = (int)(items < max_blocks ? items : max_blocks);
 }
 
-// ------------------------------------------------------------------------------------------
-// split pass (fp64, DMMA): warp w owns S rows [8w, 8w+8) of a chunk x 32 L (four n-tiles)
-// for the G terms of a group: 4G accumulator tiles (8G registers). Results go straight from the
-// accumulators to Z_i^T (8 consecutive S values = 64 B per output row and store).
-// ------------------------------------------------------------------------------------------
-// MMA loop of one group: EDGE tiles (reflect-filled pass at a domain edge) read folded rows.
-template <int G, bool EDGE>
-__device__ __forceinline__ void kb_split_mma(double (&D)[G][4][2], const double* __restrict__ xs,
-                                             const double* __restrict__ ca, int cstride, int nch,
-                                             int s_off, int ar, int ac, int row_lo, int Mg,
-                                             int rows, int sign) {
-  const double* xb = xs + (s_off + ac) * kXS + ar;
-#pragma unroll 2
-  for (int c = 0; c < nch; ++c) {
-    double A[G], B[4];
-    double mul = 1.0;
-    const double* xr = xb + 4 * c * kXS;
-    if constexpr (EDGE) xr = xs + kb_src_row(s_off + 4 * c + ac, row_lo, Mg, rows, sign, mul) * kXS + ar;
+// Rewrite the out-of-domain rows of a landed [rows][kXS] tile: sign * folded partner row, or
+// zero when the single fold leaves the domain or the tile (block-level, edge tiles only). Only
+// the out-of-domain rows are visited, all threads at once, four independent elements per
+// thread in flight (partner rows are in-domain, so reads never see this pass's writes).
+__device__ __forceinline__ void kb_fold_tile_d(double* __restrict__ xs, int rows, int row_lo, int Mg,
+                                               int sign, int tid) {
+  const int top = min(max(-row_lo, 0), rows);        // tile rows [0, top) precede the domain
+  const int bot = max(min(Mg - row_lo, rows), top);  // tile rows [bot, rows) follow it
+  const int nel = (top + rows - bot) * 32;
+  for (int i0 = 0; i0 < nel; i0 += 4 * 32 * kNW) {
+    double v[4];
+    int dst[4];
 #pragma unroll
-    for (int gg = 0; gg < G; ++gg) A[gg] = EDGE ? ca[gg * cstride + 4 * c] * mul : ca[gg * cstride + 4 * c];
+    for (int k = 0; k < 4; ++k) {
+      const int idx = i0 + k * 32 * kNW + tid;
+      dst[k] = -1;
+      v[k] = 0.0;
+      if (idx < nel) {
+        const int q = idx >> 5, col = idx & 31;
+        const int rr = q < top ? q : bot + (q - top);
+        const int f = kb_fold(row_lo + rr, Mg);
+        const int u = f - row_lo;
+        if (f >= 0 && u >= 0 && u < rows) v[k] = xs[u * kXS + col];
+        dst[k] = rr * kXS + col;
+      }
+    }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) B[j] = xr[8 * j];
-#pragma unroll
-    for (int gg = 0; gg < G; ++gg)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dmma_884(D[gg][j][0], D[gg][j][1], A[gg], B[j]);
+    for (int k = 0; k < 4; ++k)
+      if (dst[k] >= 0) xs[dst[k]] = sign < 0 ? -v[k] : v[k];
+  }
+}
+__device__ __forceinline__ void kb_flip_tile_d(double* __restrict__ xs, int rows, int row_lo, int Mg,
+                                               int tid) {
+  const int top = min(max(-row_lo, 0), rows);
+  const int bot = max(min(Mg - row_lo, rows), top);
+  const int nel = (top + rows - bot) * 32;
+  for (int idx = tid; idx < nel; idx += 32 * kNW) {
+    const int q = idx >> 5, col = idx & 31;
+    const int rr = q < top ? q : bot + (q - top);
+    xs[rr * kXS + col] = -xs[rr * kXS + col];
   }
 }
 
+__device__ __forceinline__ void st_pair(double* p, double a, double b, bool both) {
+  if (both) *reinterpret_cast<double2*>(p) = make_double2(a, b);
+  else *p = a;
+}
+
+// ------------------------------------------------------------------------------------------
+// split pass (fp64, DMMA): warp w owns S rows [8w, 8w+8) of a chunk x 32 L (four 8-column
+// M-tiles) for the G terms of a group: 4G accumulator tiles. Lane (ar, ac) of M-tile j ends
+// with Z^T[l0 + 8j + ar][s0 + 8w + 2ac + {0,1}]: one 16-byte store per term and M-tile.
+// ------------------------------------------------------------------------------------------
 template <int G>
 __device__ __forceinline__ void kb_split_group_dmma(const double* __restrict__ xs,
                                                     const double* __restrict__ cb, int cstride,
                                                     const AxisGeom& g, int s_off, int lane,
                                                     double* __restrict__ z, long long z_ps,
                                                     int gstart, const Chunk& ch, double oscale,
-                                                    bool scaled, int row_lo, bool edge, int sign) {
+                                                    bool scaled, int mirror_h,
+                                                    const double* __restrict__ msign) {
   const int ar = lane >> 2, ac = lane & 3;
   double D[G][4][2];
 #pragma unroll
@@ -230,23 +262,41 @@ __device__ __forceinline__ void kb_split_group_dmma(const double* __restrict__ x
 #pragma unroll
     for (int j = 0; j < 4; ++j) D[gg][j][0] = D[gg][j][1] = 0.0;
   const int nch = (g.dbg & 1) ? 0 : dmma_chunks(g.Wp);
-  const double* ca = cb + kCG + ac - ar;
-  const int rows = dmma_rows(kNW * 8, g.Wp);
-  if (edge) kb_split_mma<G, true>(D, xs, ca, cstride, nch, s_off, ar, ac, row_lo, g.Mg, rows, sign);
-  else kb_split_mma<G, false>(D, xs, ca, cstride, nch, s_off, ar, ac, row_lo, g.Mg, rows, sign);
-  const int s = s_off + ar;
+  const double* cbl = cb + kCG + ac - ar;
+  const double* xb = xs + (s_off + ac) * kXS + ar;
+#pragma unroll 2
+  for (int c = 0; c < nch; ++c) {
+    double A[4], B[G];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) A[j] = xb[4 * c * kXS + 8 * j];
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) B[gg] = cbl[gg * cstride + 4 * c];
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_884(D[gg][j][0], D[gg][j][1], A[j], B[gg]);
+  }
+  const int s = s_off + 2 * ac;
   if (s >= ch.cnt || (g.dbg & 2)) return;
-  const int l0 = ch.lt * 32;
+  const bool both = s + 1 < ch.cnt;
+  const int l0 = ch.lt * 32 + ar;
 #pragma unroll
   for (int gg = 0; gg < G; ++gg) {
     double* zp = z + (long long)(gstart + gg) * z_ps + ch.s0 + s;
+    const double sg = msign ? msign[gstart + gg] : 1.0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int l = l0 + 8 * j + 2 * ac + i;
-        if (l < g.other) zp[(long long)l * g.len] = scaled ? D[gg][j][i] * oscale : D[gg][j][i];
+    for (int j = 0; j < 4; ++j) {
+      const int l = l0 + 8 * j;
+      if (l >= g.other) continue;
+      const double v0 = scaled ? D[gg][j][0] * oscale : D[gg][j][0];
+      const double v1 = scaled ? D[gg][j][1] * oscale : D[gg][j][1];
+      st_pair(zp + (long long)l * g.len, v0, v1, both);
+      if (mirror_h > 0 && !(g.dbg & 32)) {  // reflected halo rows of Z^T for the reflect-filled sum pass
+        if (l < mirror_h) st_pair(zp + (long long)(-1 - l) * g.len, sg * v0, sg * v1, both);
+        if (l >= g.other - mirror_h)
+          st_pair(zp + (long long)(2 * g.other - 1 - l) * g.len, sg * v0, sg * v1, both);
       }
+    }
   }
 }
 
@@ -254,8 +304,8 @@ template <int GMAX>
 __global__ void __launch_bounds__(32 * kNW, 2)
 kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict__ z,
                    long long z_ps, long long z_bs, const double* __restrict__ tin, long long t_bs,
-                   AxisGeom g, Groups grp, const double* __restrict__ nw2, int r, int batch,
-                   int parts) {
+                   AxisGeom g, Groups grp, const double* __restrict__ nw2, int r, int batch, int parts,
+                   int eparts, int mirror_h, const double* __restrict__ msign) {
   extern __shared__ __align__(128) unsigned char kb_smem_d[];
   __shared__ unsigned long long full[kStages], empty[kStages];
   constexpr int TS = kNW * 8;
@@ -279,14 +329,20 @@ kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict_
   __syncthreads();
 
   // thread 0 walks this block's chunk list ahead of the consumers and issues one TMA box per
-  // (<= 256-row) part of each tile; the map covers the local plane including its halo rows
-  ChunkWalk fill_walk(g.len, LT, parts, batch), use_walk(g.len, LT, parts, batch);
+  // (<= 256-row) part of each tile; the map covers the local plane including its halo rows.
+  // Chunks start on even S so the 16-byte result stores stay aligned.
+  ChunkWalk fill_walk(g.len, LT, parts, batch, 2, eparts), use_walk(g.len, LT, parts, batch, 2, eparts);
   Chunk fc, ch;
   int nfill = 0;
   auto issue = [&]() {
     if (tid != 0 || !fill_walk.next(fc, TS)) return;
     const int st = nfill % kStages;
     if (nfill >= kStages) mbar_wait(&empty[st], ((nfill / kStages) - 1) & 1);
+    if (g.dbg & 4) {  // profiling: no tile traffic
+      mbar_arrive(&full[st]);
+      ++nfill;
+      return;
+    }
     mbar_arrive_expect_tx(&full[st], (unsigned)(tb.nbox * tb.box_rows * 36 * sizeof(double)));
     const int row0 = fc.s0 - g.H + g.halo_lo;  // map row of tile row 0
     for (int k = 0; k < tb.nbox; ++k)
@@ -311,20 +367,32 @@ kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict_
     issue();  // keep kStages-1 tiles in flight ahead of the one consumed now
     const int st = t % kStages;
     mbar_wait(&full[st], (t / kStages) & 1);
-    const double* xt = xs + st * tb.stage_elems;
+    double* xt = xs + st * tb.stage_elems;
     const int row_lo = g.g0 + ch.s0 - g.H;
-    const bool edge = g.fill && (row_lo < 0 || row_lo + rows_tile > g.Mg);
+    const bool edge = g.fill && (row_lo < 0 || row_lo + rows_tile > g.Mg);  // block-uniform
+    if (edge && !(g.dbg & 64)) {
+      __syncthreads();
+      kb_fold_tile_d(xt, rows_tile, row_lo, g.Mg, grp.sign[0], tid);
+      fence_proxy_async();  // generic writes before the stage's next TMA fill
+      __syncthreads();
+    }
     const double oscale = nw2 ? 1.0 / sqrt(nw2[ch.b]) : 1.0;
     double* zb = z + ch.b * z_bs;
-    if (s_off < ch.cnt) {  // warp-uniform: warps past the chunk's rows idle
-      for (int gi = 0; gi < grp.n; ++gi) {
+    for (int gi = 0; gi < grp.n; ++gi) {
+      if (edge && gi > 0 && grp.sign[gi] != grp.sign[gi - 1]) {
+        __syncthreads();
+        kb_flip_tile_d(xt, rows_tile, row_lo, g.Mg, tid);
+        fence_proxy_async();
+        __syncthreads();
+      }
+      if (s_off < ch.cnt) {  // warp-uniform: warps past the chunk's rows idle
         const int gstart = grp.start[gi];
         const double* cb = cpad + gstart * cstride;
 #define KB_DGROUP(C)                                                                                  \
   case C:                                                                                             \
     if constexpr (C <= GMAX)                                                                          \
-      kb_split_group_dmma<C>(xt, cb, cstride, g, s_off, lane, zb, z_ps, gstart, ch, oscale,           \
-                             nw2 != nullptr, row_lo, edge, grp.sign[gi]);                             \
+      kb_split_group_dmma<C>(xt, cb, cstride, g, s_off, lane, zb, z_ps, gstart, ch, oscale, nw2 != nullptr, \
+                             mirror_h, msign ? msign + (long long)ch.b * r : nullptr);                \
     break;
         switch (grp.count[gi]) {
           KB_DGROUP(1)
@@ -344,9 +412,10 @@ kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict_
 }
 
 // ------------------------------------------------------------------------------------------
-// Fused epilogue straight from the sum pass accumulators: lane (ar, ac) of warp s_off holds
-// output S = s0+s_off+8mt+ar (n index) for L = l0+8j+2ac+i (m index), i.e. per store 8
-// consecutive n values (64 B) of 4 image rows. One m-tile at a time, operand loads first.
+// Fused epilogue straight from the sum pass accumulators: lane (ar, ac) holds, for S-tile mt
+// and M-tile j, Y[p = l0 + 8j + ar][q = s0 + s_off + 8mt + 2ac + {0,1}] (p: m index, q: n
+// index), so every operand load and result store is a 16-byte pair. Operand loads of an S-tile
+// are issued before any of its arithmetic.
 // ------------------------------------------------------------------------------------------
 template <int MODE>
 __device__ __forceinline__ void kb_sum_epilogue_regs(const double (&D)[2][4][2], const AxisGeom& g,
@@ -356,62 +425,89 @@ __device__ __forceinline__ void kb_sum_epilogue_regs(const double (&D)[2][4][2],
   const int n = g.len;
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) {
-    const int sl = s_off + 8 * mt + ar;  // row within the chunk
-    const int q = ch.s0 + sl;            // n index
-    if (sl >= ch.cnt || q >= n) continue;
+    const int sl = s_off + 8 * mt + 2 * ac;  // first of the lane's two S rows in the chunk
+    if (sl >= ch.cnt) continue;
+    const bool both = sl + 1 < ch.cnt;
+    const int q = ch.s0 + sl;
     const long long rowbase = (long long)ch.b * e.bstride + q;
     double u[4][2], w[4][2];
+    auto ld2 = [&](const double* a, long long at, double (&v)[2]) {
+      if (both) {
+        const double2 t = *reinterpret_cast<const double2*>(a + at);
+        v[0] = t.x;
+        v[1] = t.y;
+      } else {
+        v[0] = a[at];
+        v[1] = 0.0;
+      }
+    };
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int p = ch.lt * 32 + 8 * j + 2 * ac + i;
-        const long long at = rowbase + (long long)p * n;
-        const bool ok = p < g.other;
-        if constexpr (MODE == EPI_RESID) u[j][i] = ok ? e.bsub[at] : 0.0;
+    for (int j = 0; j < 4; ++j) {
+      const int p = ch.lt * 32 + 8 * j + ar;
+      const long long at = rowbase + (long long)p * n;
+      u[j][0] = u[j][1] = w[j][0] = w[j][1] = 0.0;
+      if (p < g.other) {
+        if constexpr (MODE == EPI_RESID) ld2(e.bsub, at, u[j]);
         if constexpr (MODE == EPI_UPDATE) {
-          u[j][i] = ok ? e.y[at] : 0.0;
-          w[j][i] = ok ? e.x[at] : 0.0;
+          ld2(e.y, at, u[j]);
+          ld2(e.x, at, w[j]);
         }
-        if constexpr (MODE == EPI_POWER) u[j][i] = ok ? e.vin[at] : 0.0;
+        if constexpr (MODE == EPI_POWER) ld2(e.vin, at, u[j]);
       }
+    }
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 4; ++j) {
+      const int p = ch.lt * 32 + 8 * j + ar;
+      if (p >= g.other) continue;
+      const long long at = rowbase + (long long)p * n;
+      double val[2] = {D[mt][j][0], D[mt][j][1]};
+      if (e.foldH > 0) {
+        const int FH = e.foldH;
+        const double* f = e.fold + ((long long)ch.b * g.other + p) * (2 * FH);
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int p = ch.lt * 32 + 8 * j + 2 * ac + i;
-        if (p >= g.other) continue;
-        const long long at = rowbase + (long long)p * n;
-        double val = D[mt][j][i];
-        if (e.foldH > 0) {
-          const int FH = e.foldH;
-          const double* f = e.fold + ((long long)ch.b * g.other + p) * (2 * FH);
-          if (q < FH) val += f[q];
-          else if (q >= n - FH) val += f[q - (n - 2 * FH)];
+        for (int i = 0; i < 2; ++i) {
+          const int qi = q + i;
+          if (qi < FH) val[i] += f[qi];
+          else if (qi >= n - FH && qi < n) val[i] += f[qi - (n - 2 * FH)];
         }
-        if constexpr (MODE == EPI_PLAIN) {
-          e.out[at] = val;
-        } else if constexpr (MODE == EPI_RESID) {
-          e.out[at] = __dsub_rn(val, u[j][i]);
-        } else if constexpr (MODE == EPI_UPDATE) {
-          double xv = __ddiv_rn(__dsub_rn(__dmul_rn(e.L[ch.b], u[j][i]), val), e.denom[ch.b]);
-          if (e.project) xv = (xv > 0.0 || xv != xv) ? xv : 0.0;
-          const double d = __dsub_rn(xv, w[j][i]);
-          e.x[at] = xv;
-          e.y[at] = __dadd_rn(xv, __dmul_rn(e.beta, d));
-          bad |= !isfinite(xv);
-          if (e.want_norms) {
-            nrm[0] += d * d;
-            nrm[1] += w[j][i] * w[j][i];
-            nrm[2] += xv * xv;
+      }
+      if constexpr (MODE == EPI_PLAIN) {
+        st_pair(e.out + at, val[0], val[1], both);
+      } else if constexpr (MODE == EPI_RESID) {
+        st_pair(e.out + at, __dsub_rn(val[0], u[j][0]), __dsub_rn(val[1], u[j][1]), both);
+      } else if constexpr (MODE == EPI_UPDATE) {
+        const double Lb = e.L[ch.b], db = e.denom[ch.b];
+        double xv[2], yv[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          xv[i] = __ddiv_rn(__dsub_rn(__dmul_rn(Lb, u[j][i]), val[i]), db);
+          if (e.project) xv[i] = (xv[i] > 0.0 || xv[i] != xv[i]) ? xv[i] : 0.0;
+          const double d = __dsub_rn(xv[i], w[j][i]);
+          yv[i] = __dadd_rn(xv[i], __dmul_rn(e.beta, d));
+          if (i == 0 || both) {
+            bad |= !isfinite(xv[i]);
+            if (e.want_norms) {
+              nrm[0] += d * d;
+              nrm[1] += w[j][i] * w[j][i];
+              nrm[2] += xv[i] * xv[i];
+            }
           }
-        } else {  // EPI_POWER
-          const double vv = e.vnw2 ? u[j][i] / sqrt(e.vnw2[ch.b]) : u[j][i];
-          e.out[at] = val;
-          nrm[0] += vv * val;
-          nrm[1] += val * val;
         }
+        st_pair(e.x + at, xv[0], xv[1], both);
+        st_pair(e.y + at, yv[0], yv[1], both);
+      } else {  // EPI_POWER
+        const double vs = e.vnw2 ? sqrt(e.vnw2[ch.b]) : 1.0;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          if (i == 0 || both) {
+            const double vv = e.vnw2 ? u[j][i] / vs : u[j][i];
+            nrm[0] += vv * val[i];
+            nrm[1] += val[i] * val[i];
+          }
+        }
+        st_pair(e.out + at, val[0], val[1], both);
       }
+    }
   }
 }
 
@@ -435,52 +531,55 @@ __device__ __forceinline__ void kb_warp_finish(const Epi<double>& e, double (&nr
   }
 }
 
-// MMA loop of one (chunk, term) tile of the sum pass (two m-tiles sharing the B fragment).
-template <bool EDGE>
-__device__ __forceinline__ void kb_sum_mma(double (&D)[2][4][2], const double* __restrict__ xs,
-                                           const double* __restrict__ cb, int nchr, int s_off,
-                                           int ar, int ac, int row_lo, int Mg, int rows, int sign,
-                                           bool two) {
-  const double* xb = xs + (s_off + ac) * kXS + ar;
+// MMA loop of one (chunk, term) tile of the sum pass over K-chunks [c0, c1): S-tile 0 (B = taps
+// at t0) when M0, S-tile 1 (rows +8: taps at t0 - 8, sharing the A fragment) when M1.
+template <bool M0, bool M1>
+__device__ __forceinline__ void kb_sum_mma_range(double (&D)[2][4][2], const double* __restrict__ xb,
+                                                 const double* __restrict__ cb, int c0, int c1) {
 #pragma unroll 2
-  for (int c = 0; c < nchr; ++c) {
-    double mul = 1.0;
-    const double* xr = xb + 4 * c * kXS;
-    if constexpr (EDGE) xr = xs + kb_src_row(s_off + 4 * c + ac, row_lo, Mg, rows, sign, mul) * kXS + ar;
-    double B[4];
+  for (int c = c0; c < c1; ++c) {
+    double A[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) B[j] = xr[8 * j];
-    double a0 = cb[4 * c];      // zero beyond the band
-    double a1 = cb[4 * c - 8];  // zero for c < 2 (guard)
-    if constexpr (EDGE) {
-      a0 *= mul;
-      a1 *= mul;
-    }
+    for (int j = 0; j < 4; ++j) A[j] = xb[4 * c * kXS + 8 * j];
+    const double b0 = M0 ? cb[4 * c] : 0.0;
+    const double b1 = M1 ? cb[4 * c - 8] : 0.0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      dmma_884(D[0][j][0], D[0][j][1], a0, B[j]);
-      if (two) dmma_884(D[1][j][0], D[1][j][1], a1, B[j]);
+      if (M0) dmma_884(D[0][j][0], D[0][j][1], A[j], b0);
+      if (M1) dmma_884(D[1][j][0], D[1][j][1], A[j], b1);
     }
   }
 }
 
+// Whole tile: S-tile 0 needs K-chunks [0, nch), S-tile 1 [2, nch + 2); the shared middle range
+// runs both, the ends only the S-tile whose band they touch.
+__device__ __forceinline__ void kb_sum_mma(double (&D)[2][4][2], const double* __restrict__ xb,
+                                           const double* __restrict__ cb, int nch, bool two) {
+  if (!two) {
+    kb_sum_mma_range<true, false>(D, xb, cb, 0, nch);
+    return;
+  }
+  kb_sum_mma_range<true, false>(D, xb, cb, 0, 2);
+  kb_sum_mma_range<true, true>(D, xb, cb, 2, nch);
+  kb_sum_mma_range<false, true>(D, xb, cb, nch, nch + 2);
+}
+
 // ------------------------------------------------------------------------------------------
-// sum pass (fp64, DMMA): warp w owns S rows [16w, 16w+16) (two m-tiles) x 32 L of a chunk;
-// the (chunk, term) tiles stream through the mbarrier ring; m-tile 1 reuses the B fragment of
-// chunk t0 with the A fragment of t0 - 8. After a chunk's last term each warp runs the fused
-// epilogue from its registers. Norm partials are per warp: partials[b][block*kNW + warp].
+// sum pass (fp64, DMMA): warp w owns S rows [16w, 16w+16) (two S-tiles) x 32 L of a chunk;
+// the (chunk, term) tiles stream through the mbarrier ring. After a chunk's last term each warp
+// runs the fused epilogue from its registers. Norm partials are per warp:
+// partials[b][block*kNW + warp].
 // ------------------------------------------------------------------------------------------
 template <int MODE>
 __global__ void __launch_bounds__(32 * kNW, 2)
 kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* __restrict__ tin,
-                 long long t_bs, AxisGeom g, const double* __restrict__ tsign, Epi<double> e,
-                 int batch, int parts) {
+                 long long t_bs, AxisGeom g, Epi<double> e, int batch, int parts) {
   extern __shared__ __align__(128) unsigned char kb_smem_d[];
   __shared__ unsigned long long full[kStages], empty[kStages];
   constexpr int TS = kNW * 16;
   const int rows_tile = dmma_rows(TS, g.Wp);
   const TileBoxes tb = tile_boxes(rows_tile);
-  const int cstride = dmma_cstride_sum(g.Wp);  // taps at offset kCG + 8 (m-tile 1 reads t0 - 8)
+  const int cstride = dmma_cstride_sum(g.Wp);  // taps at offset kCG + 8 (S-tile 1 reads t0 - 8)
   double* xs = reinterpret_cast<double*>(kb_smem_d);  // [kStages][stage_elems]
   double* cpad = xs + kStages * tb.stage_elems;        // [r][cstride]
   const int lane = threadIdx.x, warp = threadIdx.y;
@@ -501,7 +600,7 @@ kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* 
   __syncthreads();
 
   // tile sequence: (chunk, term) for every chunk of this block; thread 0 issues the TMA boxes
-  ChunkWalk fill_walk(g.len, LT, parts, batch), use_walk(g.len, LT, parts, batch);
+  ChunkWalk fill_walk(g.len, LT, parts, batch, 2), use_walk(g.len, LT, parts, batch, 2);
   Chunk fc;
   int fterm = r;  // forces fetching the first chunk
   bool fmore = true;
@@ -517,8 +616,14 @@ kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* 
     }
     const int st = nfill % kStages;
     if (nfill >= kStages) mbar_wait(&empty[st], ((nfill / kStages) - 1) & 1);
+    if (g.dbg & 4) {  // profiling: no tile traffic
+      mbar_arrive(&full[st]);
+      ++fterm;
+      ++nfill;
+      return;
+    }
     mbar_arrive_expect_tx(&full[st], (unsigned)(tb.nbox * tb.box_rows * 36 * sizeof(double)));
-    const int row0 = fc.s0 - g.H;  // Z^T planes are not row sharded
+    const int row0 = fc.s0 - g.H + g.halo_lo;  // halo_lo: reflected rows stored by the split pass
     for (int k = 0; k < tb.nbox; ++k)
       tma_load_3d(xs + st * tb.stage_elems + k * tb.box_rows * kXS, &tmap, fc.lt * 32,
                   row0 + k * tb.box_rows, fc.b * r + fterm, &full[st]);
@@ -554,22 +659,15 @@ kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* 
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
       for (int j = 0; j < 4; ++j) D[mt][j][0] = D[mt][j][1] = 0.0;
-    const int row_lo = g.g0 + ch.s0 - g.H;
-    const bool edge = g.fill && (row_lo < 0 || row_lo + rows_tile > g.Mg);
     const bool active = s_off < ch.cnt;  // warp-uniform
     const bool two = s_off + 8 < ch.cnt;
     for (int term = 0; term < r; ++term, ++t) {
       issue();
       const int st = t % kStages;
       mbar_wait(&full[st], (t / kStages) & 1);
-      if (active) {
-        const double* xt = xs + st * tb.stage_elems;
-        const double* cb = cpad + term * cstride + kCG + 8 + ac - ar;
-        const int sgn = (tsign && tsign[(long long)ch.b * r + term] < 0.0) ? -1 : 1;
-        const int nchr = (g.dbg & 1) ? 0 : nch + 2;
-        if (edge) kb_sum_mma<true>(D, xt, cb, nchr, s_off, ar, ac, row_lo, g.Mg, rows_tile, sgn, two);
-        else kb_sum_mma<false>(D, xt, cb, nchr, s_off, ar, ac, row_lo, g.Mg, rows_tile, sgn, two);
-      }
+      const double* xt = xs + st * tb.stage_elems;
+      if (active && !(g.dbg & 1))
+        kb_sum_mma(D, xt + (s_off + ac) * kXS + ar, cpad + term * cstride + kCG + 8 + ac - ar, nch, two);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }

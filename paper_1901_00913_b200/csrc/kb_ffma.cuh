@@ -7,8 +7,9 @@
 //
 // Thread mapping: lane = L column, warp = R consecutive S rows; tiles are [rows][32] floats
 // (128-byte rows, conflict-free column reads). For a reflect-filled pass at a domain edge the
-// out-of-domain rows of a landed tile are rewritten in shared memory from their folded partner
-// (times the term group's sign) before the MMA loop; block-uniform, edge tiles only.
+// out-of-domain rows of a landed split-pass tile are rewritten in shared memory from their folded
+// partner (times the term group's sign); the split pass also stores the reflected halo rows of
+// Z^T, so the sum pass reads its edge tiles as plain TMA boxes.
 #pragma once
 #include "kb_dmma.cuh"
 
@@ -26,24 +27,44 @@ __host__ __device__ __forceinline__ TileBoxesF tile_boxes_f(int rows) {
 }
 
 // rewrite the out-of-domain rows of a landed [rows][32] tile: sign * folded partner, or 0
+// (all threads, only the out-of-domain rows, four independent elements per thread in flight)
 __device__ __forceinline__ void kb_fold_tile_f(float* __restrict__ xs, int rows, int row_lo, int Mg,
-                                               int sign, int warp, int lane) {
-  for (int rr = warp; rr < rows; rr += kNW) {
-    const int gr = row_lo + rr;
-    if (gr >= 0 && gr < Mg) continue;
-    const int f = kb_fold(gr, Mg);
-    const int u = f - row_lo;
-    const float v = (f >= 0 && u >= 0 && u < rows) ? xs[u * 32 + lane] : 0.f;
-    xs[rr * 32 + lane] = sign < 0 ? -v : v;
+                                               int sign, int tid) {
+  const int top = min(max(-row_lo, 0), rows);
+  const int bot = max(min(Mg - row_lo, rows), top);
+  const int nel = (top + rows - bot) * 32;
+  for (int i0 = 0; i0 < nel; i0 += 4 * 32 * kNW) {
+    float v[4];
+    int dst[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int idx = i0 + k * 32 * kNW + tid;
+      dst[k] = -1;
+      v[k] = 0.f;
+      if (idx < nel) {
+        const int q = idx >> 5, col = idx & 31;
+        const int rr = q < top ? q : bot + (q - top);
+        const int f = kb_fold(row_lo + rr, Mg);
+        const int u = f - row_lo;
+        if (f >= 0 && u >= 0 && u < rows) v[k] = xs[u * 32 + col];
+        dst[k] = rr * 32 + col;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (dst[k] >= 0) xs[dst[k]] = sign < 0 ? -v[k] : v[k];
   }
 }
 
 // flip the out-of-domain rows (group sign change on an already folded tile)
-__device__ __forceinline__ void kb_flip_tile_f(float* __restrict__ xs, int rows, int row_lo, int Mg,
-                                               int warp, int lane) {
-  for (int rr = warp; rr < rows; rr += kNW) {
-    const int gr = row_lo + rr;
-    if (gr < 0 || gr >= Mg) xs[rr * 32 + lane] = -xs[rr * 32 + lane];
+__device__ __forceinline__ void kb_flip_tile_f(float* __restrict__ xs, int rows, int row_lo, int Mg, int tid) {
+  const int top = min(max(-row_lo, 0), rows);
+  const int bot = max(min(Mg - row_lo, rows), top);
+  const int nel = (top + rows - bot) * 32;
+  for (int idx = tid; idx < nel; idx += 32 * kNW) {
+    const int q = idx >> 5, col = idx & 31;
+    const int rr = q < top ? q : bot + (q - top);
+    xs[rr * 32 + col] = -xs[rr * 32 + col];
   }
 }
 
@@ -56,7 +77,8 @@ template <int G>
 __device__ __forceinline__ void kb_split_group_f(const float* __restrict__ xs, const float* __restrict__ cin,
                                                  int Wp, const AxisGeom& g, int s_off, int lane,
                                                  float* __restrict__ z, long long z_ps, int gstart,
-                                                 const Chunk& ch, float oscale, bool scaled) {
+                                                 const Chunk& ch, float oscale, bool scaled, int mirror_h,
+                                                 const float* __restrict__ msign) {
   float acc[G][8];
 #pragma unroll
   for (int gg = 0; gg < G; ++gg)
@@ -65,20 +87,29 @@ __device__ __forceinline__ void kb_split_group_f(const float* __restrict__ xs, c
   if (!(g.dbg & 1)) kb_taps<float, G, 8>(acc, xs + s_off * 32 + lane, cin, Wp, Wp);
   const int l = ch.lt * 32 + lane;
   if (l >= g.other || (g.dbg & 2)) return;
+  const bool full = s_off + 8 <= ch.cnt;
+  auto put = [&](float* zp, const float (&v)[8], float sg) {
+    if (full) {
+      reinterpret_cast<float4*>(zp)[0] = make_float4(sg * v[0], sg * v[1], sg * v[2], sg * v[3]);
+      reinterpret_cast<float4*>(zp)[1] = make_float4(sg * v[4], sg * v[5], sg * v[6], sg * v[7]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (s_off + j < ch.cnt) zp[j] = sg * v[j];
+    }
+  };
 #pragma unroll
   for (int gg = 0; gg < G; ++gg) {
-    float* zp = z + (long long)(gstart + gg) * z_ps + (long long)l * g.len + ch.s0 + s_off;
+    float* zp = z + (long long)(gstart + gg) * z_ps + ch.s0 + s_off;
     if (scaled) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[gg][j] *= oscale;
     }
-    if (s_off + 8 <= ch.cnt) {
-      reinterpret_cast<float4*>(zp)[0] = make_float4(acc[gg][0], acc[gg][1], acc[gg][2], acc[gg][3]);
-      reinterpret_cast<float4*>(zp)[1] = make_float4(acc[gg][4], acc[gg][5], acc[gg][6], acc[gg][7]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (s_off + j < ch.cnt) zp[j] = acc[gg][j];
+    put(zp + (long long)l * g.len, acc[gg], 1.f);
+    if (mirror_h > 0) {  // reflected halo rows of Z^T for the reflect-filled sum pass
+      const float sg = msign ? msign[gstart + gg] : 1.f;
+      if (l < mirror_h) put(zp + (long long)(-1 - l) * g.len, acc[gg], sg);
+      if (l >= g.other - mirror_h) put(zp + (long long)(2 * g.other - 1 - l) * g.len, acc[gg], sg);
     }
   }
 }
@@ -87,7 +118,8 @@ template <int GMAX>
 __global__ void __launch_bounds__(32 * kNW, 2)
 kb_pass_split_f(const __grid_constant__ CUtensorMap tmap, float* __restrict__ z, long long z_ps,
                 long long z_bs, const float* __restrict__ tin, long long t_bs, AxisGeom g, Groups grp,
-                const double* __restrict__ nw2, int r, int batch, int parts) {
+                const double* __restrict__ nw2, int r, int batch, int parts, int eparts, int mirror_h,
+                const float* __restrict__ msign) {
   extern __shared__ __align__(128) unsigned char kb_smem_f[];
   __shared__ unsigned long long full[kStages], empty[kStages];
   constexpr int TS = kNW * 8;
@@ -109,7 +141,7 @@ kb_pass_split_f(const __grid_constant__ CUtensorMap tmap, float* __restrict__ z,
   }
   __syncthreads();
 
-  ChunkWalk fill_walk(g.len, LT, parts, batch, 8), use_walk(g.len, LT, parts, batch, 8);
+  ChunkWalk fill_walk(g.len, LT, parts, batch, 4, eparts), use_walk(g.len, LT, parts, batch, 4, eparts);
   Chunk fc, ch;
   int nfill = 0;
   auto issue = [&]() {
@@ -142,7 +174,8 @@ kb_pass_split_f(const __grid_constant__ CUtensorMap tmap, float* __restrict__ z,
     const bool edge = g.fill && (row_lo < 0 || row_lo + rows_tile > g.Mg);
     if (edge) {  // block-uniform
       __syncthreads();
-      kb_fold_tile_f(xt, rows_tile, row_lo, g.Mg, grp.sign[0], warp, lane);
+      kb_fold_tile_f(xt, rows_tile, row_lo, g.Mg, grp.sign[0], tid);
+      fence_proxy_async();
       __syncthreads();
     }
     const float oscale = nw2 ? (float)(1.0 / sqrt(nw2[ch.b])) : 1.f;
@@ -150,7 +183,8 @@ kb_pass_split_f(const __grid_constant__ CUtensorMap tmap, float* __restrict__ z,
     for (int gi = 0; gi < grp.n; ++gi) {
       if (edge && gi > 0 && grp.sign[gi] != grp.sign[gi - 1]) {
         __syncthreads();
-        kb_flip_tile_f(xt, rows_tile, row_lo, g.Mg, warp, lane);
+        kb_flip_tile_f(xt, rows_tile, row_lo, g.Mg, tid);
+        fence_proxy_async();
         __syncthreads();
       }
       if (s_off < ch.cnt) {
@@ -159,7 +193,8 @@ kb_pass_split_f(const __grid_constant__ CUtensorMap tmap, float* __restrict__ z,
 #define KB_FGROUP(C)                                                                                  \
   case C:                                                                                             \
     if constexpr (C <= GMAX)                                                                          \
-      kb_split_group_f<C>(xt, cb, g.Wp, g, s_off, lane, zb, z_ps, gstart, ch, oscale, nw2 != nullptr); \
+      kb_split_group_f<C>(xt, cb, g.Wp, g, s_off, lane, zb, z_ps, gstart, ch, oscale, nw2 != nullptr, \
+                          mirror_h, msign ? msign + (long long)ch.b * r : nullptr);                 \
     break;
         switch (grp.count[gi]) {
           KB_FGROUP(1)
@@ -301,7 +336,7 @@ __device__ __forceinline__ void kb_warp_finish_f(const Epi<float>& e, double (&n
 template <int MODE>
 __global__ void __launch_bounds__(32 * kNW, 2)
 kb_pass_sum_f(const __grid_constant__ CUtensorMap tmap, int r, const float* __restrict__ tin, long long t_bs,
-              AxisGeom g, const float* __restrict__ tsign, Epi<float> e, int batch, int parts) {
+              AxisGeom g, Epi<float> e, int batch, int parts) {
   extern __shared__ __align__(128) unsigned char kb_smem_f[];
   __shared__ unsigned long long full[kStages], empty[kStages];
   constexpr int TS = kNW * 16;
@@ -324,7 +359,7 @@ kb_pass_sum_f(const __grid_constant__ CUtensorMap tmap, int r, const float* __re
   }
   __syncthreads();
 
-  ChunkWalk fill_walk(g.len, LT, parts, batch, 8), use_walk(g.len, LT, parts, batch, 8);
+  ChunkWalk fill_walk(g.len, LT, parts, batch, 4), use_walk(g.len, LT, parts, batch, 4);
   Chunk fc;
   int fterm = r;
   bool fmore = true;
@@ -341,7 +376,7 @@ kb_pass_sum_f(const __grid_constant__ CUtensorMap tmap, int r, const float* __re
     const int st = nfill % kStages;
     if (nfill >= kStages) mbar_wait(&empty[st], ((nfill / kStages) - 1) & 1);
     mbar_arrive_expect_tx(&full[st], (unsigned)(tb.stage_elems * sizeof(float)));
-    const int row0 = fc.s0 - g.H;
+    const int row0 = fc.s0 - g.H + g.halo_lo;  // halo_lo: reflected rows stored by the split pass
     for (int k = 0; k < tb.nbox; ++k)
       tma_load_3d(xs + st * tb.stage_elems + k * tb.box_rows * 32, &tmap, fc.lt * 32,
                   row0 + k * tb.box_rows, fc.b * r + fterm, &full[st]);
@@ -372,19 +407,11 @@ kb_pass_sum_f(const __grid_constant__ CUtensorMap tmap, int r, const float* __re
     float acc[1][16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[0][j] = 0.f;
-    const int row_lo = g.g0 + ch.s0 - g.H;
-    const bool edge = g.fill && (row_lo < 0 || row_lo + rows_tile > g.Mg);
     for (int term = 0; term < r; ++term, ++t) {
       issue();
       const int st = t % kStages;
       mbar_wait(&full[st], (t / kStages) & 1);
-      float* xt = xs + st * tb.stage_elems;
-      if (edge) {
-        __syncthreads();
-        const int sgn = (tsign && tsign[(long long)ch.b * r + term] < 0.f) ? -1 : 1;
-        kb_fold_tile_f(xt, rows_tile, row_lo, g.Mg, sgn, warp, lane);
-        __syncthreads();
-      }
+      const float* xt = xs + st * tb.stage_elems;
       if (s_off < ch.cnt && !(g.dbg & 1))
         kb_taps<float, 1, 16>(acc, xt + s_off * 32 + lane, cpad + term * g.Wp, 0, g.Wp);
       __syncwarp();

@@ -53,7 +53,8 @@ struct AxisGeom {
   int Mg;       // global extent of the domain
   int halo_lo;  // readable entries before local 0
   int halo_hi;  // readable entries after local len-1
-  int dbg;      // profiling switch (KB_DEBUG_MODE): bit0 skip MMAs, bit1 skip result stores
+  int dbg;      // profiling switch (KB_DEBUG_MODE): bit0 skip MMAs, bit1 skip result stores,
+                //   bit2 skip tile loads (persistent kernels)
 };
 
 template <typename T>
@@ -309,7 +310,8 @@ __device__ __forceinline__ T kb_fold_sum(const T* __restrict__ tc, const T* __re
 template <typename T>
 __global__ void __launch_bounds__(128)
 kb_fold_split(const T* __restrict__ in, long long in_bs, T* __restrict__ z, long long z_ps,
-              long long z_bs, int r, const T* __restrict__ tconv, long long t_bs, AxisGeom g) {
+              long long z_bs, int r, const T* __restrict__ tconv, long long t_bs, AxisGeom g,
+              int mirror_h, const T* __restrict__ msign) {
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   const int slot = blockIdx.y % (2 * g.H);
   const int i = blockIdx.y / (2 * g.H);
@@ -323,8 +325,13 @@ kb_fold_split(const T* __restrict__ in, long long in_bs, T* __restrict__ z, long
   const T* tc = tconv + b * t_bs + (long long)i * g.Wp;
   const T* src = in + b * in_bs + l - (long long)g.g0 * g.other;  // src[u*other] = global row u
   const T acc = kb_fold_sum<T>(tc, src, g.other, s, H, M);
-  T* zp = z + b * z_bs + (long long)i * z_ps + (long long)l * g.len + ls;
-  *zp = *zp + acc;
+  T* zp = z + b * z_bs + (long long)i * z_ps + ls;
+  zp[(long long)l * g.len] += acc;
+  if (mirror_h > 0) {  // keep the reflected halo rows of Z^T (see the persistent split) in step
+    const T sg = msign ? msign[(long long)b * r + i] : T(1);
+    if (l < mirror_h) zp[(long long)(-1 - l) * g.len] += sg * acc;
+    if (l >= g.other - mirror_h) zp[(long long)(2 * g.other - 1 - l) * g.len] += sg * acc;
+  }
 }
 
 // sum-pass fold: fold[b][l][slot] = sum_i fold over S of Z_i^T[:, l] for edge S positions

@@ -290,3 +290,53 @@ def test_batched_solve_matches_per_image(rng):
     for i in range(3):
         want, _ = port.sfista(ops[i], Bs[i], Ls[i], 0.02, 30, project=True)
         assert rel(x[i], want) <= 1e-10
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("orient", [0, 1])
+def test_mixed_axis_symmetry(dtype, orient, rng):
+    # one axis (anti)symmetric, the other general: the split pass stores Z^T's reflected halo
+    # rows while the other axis takes the exact fold kernels (which must keep the halo in step)
+    from paper_1901_00913_b200 import Psf
+    from paper_1901_00913_b200.device import DeviceOperator
+
+    u = np.array([1.0, 3.0, 5.0, 3.0, 1.0])
+    v = rng.random(5) + 0.1
+    vals = np.outer(u, v) if orient == 0 else np.outer(v, u)
+    op = kb.decompose(Psf(vals / vals.sum(), (3, 3)), REFL, s=1, shape=(64, 64))
+    info = DeviceOperator([op], dtype).info()
+    assert info["sym_a"] != info["sym_b"]
+    X = rng.standard_normal((64, 64))
+    pop = port.PortOperator(op)
+    tol = 1e-12 if dtype == "float64" else 1e-5
+    assert rel(kb.kron_apply_adjoint(op, X, dtype=dtype), port.kron_apply_adjoint(pop, X)) <= tol
+    assert rel(kb.kron_apply(op, X, dtype=dtype), port.kron_apply(pop, X)) <= tol
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_misaligned_device_buffers(dtype):
+    # views 8 bytes off a 16-byte boundary cannot feed TMA / vector epilogues: the generic
+    # kernels take over (and the sum pass must not expect reflected halo rows)
+    from paper_1901_00913_b200.device import DeviceOperator
+
+    rng = np.random.default_rng(11)
+    m = 96
+    op = kb.decompose(random_psf(rng, 9), REFL, s=3, shape=(m, m))
+    X = rng.standard_normal((m, m))
+    td = torch.float64 if dtype == "float64" else torch.float32
+    dev = DeviceOperator([op], dtype)
+    base = torch.zeros(m * m + 4, dtype=td, device="cuda")
+    off = 1 if dtype == "float64" else 2
+    xv = base[off:off + m * m].view(m, m)
+    xv.copy_(torch.from_numpy(X))
+    pop = port.PortOperator(op)
+    tol = 1e-12 if dtype == "float64" else 1e-5
+    xa = torch.from_numpy(X).to("cuda", td)
+    obase = torch.zeros(m * m + 4, dtype=td, device="cuda")
+    ov = obase[off:off + m * m].view(m, m)
+    for adjoint in (False, True):
+        want = port.kron_apply_adjoint(pop, X) if adjoint else port.kron_apply(pop, X)
+        got = dev.apply(xv, adjoint=adjoint).double().cpu().numpy()  # misaligned operand
+        assert rel(got, want) <= tol
+        dev.apply(xa, out=ov, adjoint=adjoint)  # aligned operand, misaligned result
+        assert rel(ov.double().cpu().numpy(), want) <= tol

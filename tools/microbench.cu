@@ -109,7 +109,8 @@ __global__ void dfma3_k(double* out, int iters, double a) {
   if (s == -1.2345) out[0] = s;
 }
 
-// the split-pass inner loop alone: tile [128][36] in smem, G=4 terms x 4 n-tiles, 18 chunks
+// the split-pass inner loop alone: tile [128][36] in smem, G terms x 4 n-tiles, 18 chunks
+template <int G>
 __global__ void __launch_bounds__(256, 2) dmma_split_k(double* out, int reps) {
   __shared__ double xs[136 * 36];
   __shared__ double cp[4 * 96];
@@ -118,27 +119,27 @@ __global__ void __launch_bounds__(256, 2) dmma_split_k(double* out, int reps) {
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ar = lane >> 2, ac = lane & 3;
-  double D[4][4][2] = {};
+  double D[G][4][2] = {};
   const double* xb = xs + (warp * 8 + ac) * 36 + ar;
   const double* cb = cp + 8 + ac - ar;
   for (int rep = 0; rep < reps; ++rep) {
 #pragma unroll 2
     for (int c = 0; c < 18; ++c) {
-      double A[4], B[4];
+      double A[G], B[4];
 #pragma unroll
-      for (int g = 0; g < 4; ++g) A[g] = cb[g * 96 + 4 * c];
+      for (int g = 0; g < G; ++g) A[g] = cb[g * 96 + 4 * c];
 #pragma unroll
       for (int j = 0; j < 4; ++j) B[j] = xb[4 * c * 36 + 8 * j];
 #pragma unroll
-      for (int g = 0; g < 4; ++g)
+      for (int g = 0; g < G; ++g)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                       : "+d"(D[g][j][0]), "+d"(D[g][j][1]) : "d"(A[g]), "d"(B[j]));
+                       : "+d"(D[g][j][0]), "+d"(D[g][j][1]) : "d"(B[j]), "d"(A[g]));
     }
   }
   double s = 0;
-  for (int g = 0; g < 4; ++g)
+  for (int g = 0; g < G; ++g)
     for (int j = 0; j < 4; ++j) s += D[g][j][0] + D[g][j][1];
   if (s == -1.2345) out[0] = s;
 }
@@ -185,8 +186,16 @@ int main() {
   }
   {
     const int reps = 200;
-    float ms = timeit(dmma_split_k, sms * 2, 256, dout, reps);
-    printf("DMMA split-loop 16 warps/SM  %.2f TFLOP/s\n", 2.0 * 256 * 16 * 18 * reps * (double)sms * 2 * 8 / ms / 1e9);
+    for (int bps : {1, 2}) {
+      float ms = timeit(dmma_split_k<4>, sms * bps, 256, dout, reps);
+      printf("DMMA split-loop G=4 %d warps/SM  %.2f TFLOP/s\n", 8 * bps, 2.0 * 256 * 16 * 18 * reps * (double)sms * bps * 8 / ms / 1e9);
+      ms = timeit(dmma_split_k<3>, sms * bps, 256, dout, reps);
+      printf("DMMA split-loop G=3 %d warps/SM  %.2f TFLOP/s\n", 8 * bps, 2.0 * 256 * 12 * 18 * reps * (double)sms * bps * 8 / ms / 1e9);
+      ms = timeit(dmma_split_k<2>, sms * bps, 256, dout, reps);
+      printf("DMMA split-loop G=2 %d warps/SM  %.2f TFLOP/s\n", 8 * bps, 2.0 * 256 * 8 * 18 * reps * (double)sms * bps * 8 / ms / 1e9);
+      ms = timeit(dmma_split_k<1>, sms * bps, 256, dout, reps);
+      printf("DMMA split-loop G=1 %d warps/SM  %.2f TFLOP/s\n", 8 * bps, 2.0 * 256 * 4 * 18 * reps * (double)sms * bps * 8 / ms / 1e9);
+    }
   }
   return 0;
 }
