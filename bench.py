@@ -53,6 +53,18 @@ def dist_env():
     return rank, world, local
 
 
+def committed_traffic(dtype):
+    """DRAM bytes (read + write) of one iteration's four kernels from the committed ncu capture
+    (profiles/traffic_cfg2.json, written by tools/ncu_traffic.py from an `ncu --set full
+    --cache-control none` run of tools/time_kernels.py), or None when absent."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic_cfg2.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(dtype)
+    except (OSError, ValueError):
+        return None
+
+
 def algorithmic(cfg):
     """Per pixel*iteration: flops F = 8 r w (forward + adjoint, 2 passes each, w MACs per tap
     row), compulsory bytes 8*sizeof(T) (sweep 1 reads Y, B writes R; sweep 2 reads R, Y, X_prev,
@@ -228,13 +240,15 @@ def run_b200(args):
     achieved_tf = flops_it / (it_ms * 1e-3) / 1e12
     hbm_gbs = 8 * esz * m * m / (it_ms * 1e-3) / 1e9
     roofline = {
-        "bound": "fma",
+        "bound": "tensor" if args.dtype == "float64" else "fma",
         "kernel": "one sFISTA iteration = kb_pass_a(fwd) + kb_pass_b(resid) + kb_pass_a(adj) + kb_pass_b(update)",
         "achieved": round(achieved_tf, 3), "peak": round(peak_fma, 3), "unit": "TFLOP/s",
         "frac": round(achieved_tf / peak_fma, 4),
-        "peak_source": f"measured live by kb_fma_peak ({args.dtype} FMA chains) in this run",
+        "peak_source": ("measured live by kb_fma_peak in this run: "
+                        + ("FP64 tensor-core DMMA m8n8k4 burn (the pass kernels' instruction)"
+                           if args.dtype == "float64" else "FFMA chains")),
         "per_kernel_ms": [round(x, 5) for x in kern_ms],
-        "traffic": None,
+        "traffic": committed_traffic(args.dtype),
         "hbm": {"achieved": round(hbm_gbs, 1), "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                 "frac": round(hbm_gbs / peaks.get("hbm_gbs", 6550.0), 4), "peak_source": peak_kind,
                 "algorithmic_bytes_per_px_it": 8 * esz},

@@ -111,13 +111,18 @@ int kb_block_update(const kb_op* op, const void* Rh, void* X, void* Y, void* wor
 
 /*
  * Measurement helpers used by bench.py (no reference counterpart).
- * kb_fma_peak: FMA throughput of this GPU in TFLOP/s for dtype (roofline denominator).
+ * kb_fma_peak: measured throughput (TFLOP/s) of the arithmetic instruction the pass kernels issue
+ * for dtype - FP64 tensor-core DMMA (m8n8k4) for KB_F64, FFMA for KB_F32 (roofline denominator).
  * kb_time_passes: average device time (ms, CUDA events on `stream`) of each of the four kernels of
  * one sFISTA iteration, `reps` back-to-back launches each: ms4 = {forward pass A, forward pass B
  * (residual epilogue), adjoint pass A, adjoint pass B (update epilogue, beta = 0)}. X/Yio are
  * overwritten.
  */
 int kb_fma_peak(int dtype, float* tflops, void* stream);
+/* Profiling timeline of the latest fp64 pass kernels launched with KB_DEBUG_MODE bit 7 set:
+ * host[kind][block][slot] %globaltimer stamps (kind 0 split, 1 sum; 1024 blocks x 8 slots,
+ * slot 7 = SM id); copies min(n, 16384) values. */
+int kb_debug_trace(unsigned long long* host, int n);
 int kb_time_passes(const kb_op* op, const void* Y, const void* B, void* R, void* X, void* Yio,
                    void* work, int reps, const double* L, double lam, int* nonfinite,
                    float* ms4, void* stream);

@@ -214,6 +214,10 @@ int allow_smem(K kernel, size_t dyn_bytes) {
       KB_CUDA(cudaFuncGetAttributes(&attr, kernel));
       limit = 227 * 1024 - (int)attr.sharedSizeBytes;
       KB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
+      // one carveout (all shared memory) for every pass kernel: consecutive kernels of an
+      // iteration then never wait for an SM's L1/shared split to be reconfigured
+      KB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                   (int)cudaSharedmemCarveoutMaxShared));
       g_smem_limit[key] = limit;
     } else {
       limit = it->second;
@@ -221,6 +225,13 @@ int allow_smem(K kernel, size_t dyn_bytes) {
   }
   if (dyn_bytes > (size_t)limit) return fail(KB_ERR_ARGUMENT, "band too wide for the shared-memory tile");
   return KB_OK;
+}
+
+// Launch a persistent pass kernel (one block of 32 x kNW threads per work slot).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_persistent(void (*kernel)(KArgs...), int nb, size_t smem, cudaStream_t s, Args&&... args) {
+  kernel<<<nb, dim3(32, kb::kNW), smem, s>>>(std::forward<Args>(args)...);
+  return cudaGetLastError();
 }
 
 template <typename T, int GMAX>
@@ -263,9 +274,8 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
       kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb,
                      mirror_h > 0 ? &eparts : nullptr);
       if (mirror_h == 0) eparts = parts;
-      kern<<<nb, dim3(32, kb::kNW), smem, s>>>(map, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r,
-                                               op->batch, parts, eparts, mirror_h, msign);
-      KB_CUDA(cudaGetLastError());
+      KB_CUDA(launch_persistent(kern, nb, smem, s, map, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r, op->batch,
+                         parts, eparts, mirror_h, msign));
       op->last_mirror = mirror_h > 0;
       return KB_OK;
     }
@@ -283,9 +293,8 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
       kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb,
                      mirror_h > 0 ? &eparts : nullptr);
       if (mirror_h == 0) eparts = parts;
-      kern<<<nb, dim3(32, kb::kNW), smem, s>>>(map, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r,
-                                               op->batch, parts, eparts, mirror_h, msign);
-      KB_CUDA(cudaGetLastError());
+      KB_CUDA(launch_persistent(kern, nb, smem, s, map, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r, op->batch,
+                         parts, eparts, mirror_h, msign));
       op->last_mirror = mirror_h > 0;
       return KB_OK;
     }
@@ -320,9 +329,7 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
       if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // warps skip untouched images
         KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kNW, s));
       op->last_slots = nb * kb::kNW;
-      kern<<<nb, dim3(32, kb::kNW), smem, s>>>(map, op->r, tin, (long long)op->r * g.Wp, g, e,
-                                               op->batch, parts);
-      KB_CUDA(cudaGetLastError());
+      KB_CUDA(launch_persistent(kern, nb, smem, s, map, op->r, tin, (long long)op->r * g.Wp, g, e, op->batch, parts));
       return KB_OK;
     }
   } else {
@@ -338,9 +345,7 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
       if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))
         KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kNW, s));
       op->last_slots = nb * kb::kNW;
-      kern<<<nb, dim3(32, kb::kNW), smem, s>>>(map, op->r, tin, (long long)op->r * g.Wp, g, e,
-                                               op->batch, parts);
-      KB_CUDA(cudaGetLastError());
+      KB_CUDA(launch_persistent(kern, nb, smem, s, map, op->r, tin, (long long)op->r * g.Wp, g, e, op->batch, parts));
       return KB_OK;
     }
   }
@@ -648,6 +653,23 @@ __global__ void kb_fma_burn(T* out, int iters, T a, T b) {
   if (s == T(-12345.678)) out[0] = s;  // never true; keeps the chains alive
 }
 
+// FP64 tensor-core burn: 8 independent m8n8k4 DMMA accumulators per warp (256 FMAs each)
+__global__ void kb_dmma_burn(double* out, int iters) {
+  const double a = threadIdx.x * 1e-3, b = threadIdx.x * 2e-3;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) kb::dmma_884(c[i][0], c[i][1], a, b);
+  }
+  double sum = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sum += c[i][0] + c[i][1];
+  if (sum == -12345.678) out[0] = sum;
+}
+
+// Peak of the arithmetic instruction the pass kernels issue: DMMA for fp64, FFMA for fp32.
 template <typename T>
 int fma_peak_t(float* tflops, cudaStream_t s) {
   int dev = 0, sms = 0;
@@ -659,10 +681,14 @@ int fma_peak_t(float* tflops, cudaStream_t s) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  kb_fma_burn<T><<<blocks, threads, 0, s>>>(out, iters, T(0.999999), T(1e-7));  // warm-up
-  cudaEventRecord(e0, s);
   const int reps = 5;
-  for (int r = 0; r < reps; ++r) kb_fma_burn<T><<<blocks, threads, 0, s>>>(out, iters, T(0.999999), T(1e-7));
+  auto burn = [&]() {
+    if constexpr (sizeof(T) == 8) kb_dmma_burn<<<blocks, threads, 0, s>>>(out, iters / 8);
+    else kb_fma_burn<T><<<blocks, threads, 0, s>>>(out, iters, T(0.999999), T(1e-7));
+  };
+  burn();  // warm-up
+  cudaEventRecord(e0, s);
+  for (int r = 0; r < reps; ++r) burn();
   cudaEventRecord(e1, s);
   cudaError_t ce = cudaEventSynchronize(e1);
   float ms = 0.f;
@@ -671,7 +697,8 @@ int fma_peak_t(float* tflops, cudaStream_t s) {
   cudaEventDestroy(e1);
   cudaFree(out);
   if (ce != cudaSuccess) return fail(KB_ERR_CUDA, cudaGetErrorString(ce));
-  const double flops = 2.0 * 8.0 * (double)iters * threads * blocks * reps;
+  const double flops = sizeof(T) == 8 ? 2.0 * 256.0 * 8.0 * (double)(iters / 8) * (threads / 32) * blocks * reps
+                                      : 2.0 * 8.0 * (double)iters * threads * blocks * reps;
   *tflops = (float)(flops / (ms * 1e-3) / 1e12);
   return KB_OK;
 }
@@ -991,6 +1018,13 @@ int kb_fma_peak(int dtype, float* tflops, void* stream) {
   if (!tflops) return fail(KB_ERR_ARGUMENT, "null output");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return dtype == KB_F64 ? fma_peak_t<double>(tflops, s) : fma_peak_t<float>(tflops, s);
+}
+
+int kb_debug_trace(unsigned long long* host, int n) {
+  if (!host || n < 0) return fail(KB_ERR_ARGUMENT, "bad kb_debug_trace arguments");
+  const size_t all = sizeof(kb::kb_trace);
+  KB_CUDA(cudaMemcpyFromSymbol(host, kb::kb_trace, std::min(all, (size_t)n * sizeof(unsigned long long))));
+  return KB_OK;
 }
 
 int kb_time_passes(const kb_op* op, const void* Y, const void* B, void* R, void* X, void* Yio,

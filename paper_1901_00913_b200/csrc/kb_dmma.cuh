@@ -69,6 +69,22 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, u
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// Profiling timeline (KB_DEBUG_MODE bit 7): thread 0 of block b stamps %globaltimer into
+// kb_trace[kind][b][slot] (kind 0 split, 1 sum; read back with kb_debug_trace).
+constexpr int kTraceBlocks = 1024;
+__device__ unsigned long long kb_trace[2][kTraceBlocks][8];
+__device__ __forceinline__ void kb_stamp(const AxisGeom& g, int kind, int slot) {
+  if ((g.dbg & 128) && threadIdx.x == 0 && threadIdx.y == 0 && blockIdx.x < kTraceBlocks) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    kb_trace[kind][blockIdx.x][slot] = t;
+    if (slot == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      kb_trace[kind][blockIdx.x][7] = smid;
+    }
+  }
+}
 // order this thread's generic-proxy shared-memory writes before later async-proxy (TMA) access
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -237,6 +253,16 @@ __device__ __forceinline__ void kb_flip_tile_d(double* __restrict__ xs, int rows
   }
 }
 
+// a / d correctly rounded for normal results, given rd = RN(1/d): q = RN(a*rd) is within an ulp
+// and one exact-remainder correction RN(q + (a - d*q)*rd) rounds correctly (Markstein). Three
+// FP64 operations instead of a full division per element, whose dependent Newton chain stalls
+// behind the DMMAs of the other warps on the shared FP64 pipe.
+__device__ __forceinline__ double kb_quot(double a, double d, double rd) {
+  const double q = __dmul_rn(a, rd);
+  const double rem = fma(-d, q, a);
+  return fma(rem, rd, q);
+}
+
 __device__ __forceinline__ void st_pair(double* p, double a, double b, bool both) {
   if (both) *reinterpret_cast<double2*>(p) = make_double2(a, b);
   else *p = a;
@@ -307,6 +333,7 @@ kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict_
                    AxisGeom g, Groups grp, const double* __restrict__ nw2, int r, int batch, int parts,
                    int eparts, int mirror_h, const double* __restrict__ msign) {
   extern __shared__ __align__(128) unsigned char kb_smem_d[];
+  kb_stamp(g, 0, 0);
   __shared__ unsigned long long full[kStages], empty[kStages];
   constexpr int TS = kNW * 8;
   const int rows_tile = dmma_rows(TS, g.Wp);
@@ -327,6 +354,7 @@ kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict_
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  kb_stamp(g, 0, 1);
 
   // thread 0 walks this block's chunk list ahead of the consumers and issues one TMA box per
   // (<= 256-row) part of each tile; the map covers the local plane including its halo rows.
@@ -363,10 +391,12 @@ kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict_
       }
       __syncthreads();
       taps_b = ch.b;
+      if (t == 0) kb_stamp(g, 0, 2);
     }
     issue();  // keep kStages-1 tiles in flight ahead of the one consumed now
     const int st = t % kStages;
     mbar_wait(&full[st], (t / kStages) & 1);
+    if (t == 0) kb_stamp(g, 0, 3);
     double* xt = xs + st * tb.stage_elems;
     const int row_lo = g.g0 + ch.s0 - g.H;
     const bool edge = g.fill && (row_lo < 0 || row_lo + rows_tile > g.Mg);  // block-uniform
@@ -408,7 +438,9 @@ kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict_
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
+    if (t < 2) kb_stamp(g, 0, 4 + t);
   }
+  kb_stamp(g, 0, 6);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -423,6 +455,14 @@ __device__ __forceinline__ void kb_sum_epilogue_regs(const double (&D)[2][4][2],
                                                      int s_off, int ar, int ac, double (&nrm)[3],
                                                      bool& bad) {
   const int n = g.len;
+  // per-image scalars, loaded once (the result stores below may alias them for the compiler)
+  double Lb = 0.0, db = 1.0, rd = 1.0, vs = 1.0;
+  if constexpr (MODE == EPI_UPDATE) {
+    Lb = e.L[ch.b];
+    db = e.denom[ch.b];
+    rd = 1.0 / db;  // correctly rounded reciprocal: quotients below via Markstein's correction
+  }
+  if constexpr (MODE == EPI_POWER) vs = e.vnw2 ? sqrt(e.vnw2[ch.b]) : 1.0;
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) {
     const int sl = s_off + 8 * mt + 2 * ac;  // first of the lane's two S rows in the chunk
@@ -476,11 +516,10 @@ __device__ __forceinline__ void kb_sum_epilogue_regs(const double (&D)[2][4][2],
       } else if constexpr (MODE == EPI_RESID) {
         st_pair(e.out + at, __dsub_rn(val[0], u[j][0]), __dsub_rn(val[1], u[j][1]), both);
       } else if constexpr (MODE == EPI_UPDATE) {
-        const double Lb = e.L[ch.b], db = e.denom[ch.b];
         double xv[2], yv[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-          xv[i] = __ddiv_rn(__dsub_rn(__dmul_rn(Lb, u[j][i]), val[i]), db);
+          xv[i] = kb_quot(__dsub_rn(__dmul_rn(Lb, u[j][i]), val[i]), db, rd);
           if (e.project) xv[i] = (xv[i] > 0.0 || xv[i] != xv[i]) ? xv[i] : 0.0;
           const double d = __dsub_rn(xv[i], w[j][i]);
           yv[i] = __dadd_rn(xv[i], __dmul_rn(e.beta, d));
@@ -496,7 +535,6 @@ __device__ __forceinline__ void kb_sum_epilogue_regs(const double (&D)[2][4][2],
         st_pair(e.x + at, xv[0], xv[1], both);
         st_pair(e.y + at, yv[0], yv[1], both);
       } else {  // EPI_POWER
-        const double vs = e.vnw2 ? sqrt(e.vnw2[ch.b]) : 1.0;
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           if (i == 0 || both) {
@@ -575,6 +613,7 @@ __global__ void __launch_bounds__(32 * kNW, 2)
 kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* __restrict__ tin,
                  long long t_bs, AxisGeom g, Epi<double> e, int batch, int parts) {
   extern __shared__ __align__(128) unsigned char kb_smem_d[];
+  kb_stamp(g, 1, 0);
   __shared__ unsigned long long full[kStages], empty[kStages];
   constexpr int TS = kNW * 16;
   const int rows_tile = dmma_rows(TS, g.Wp);
@@ -598,6 +637,7 @@ kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* 
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  kb_stamp(g, 1, 1);
 
   // tile sequence: (chunk, term) for every chunk of this block; thread 0 issues the TMA boxes
   ChunkWalk fill_walk(g.len, LT, parts, batch, 2), use_walk(g.len, LT, parts, batch, 2);
@@ -648,6 +688,7 @@ kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* 
       }
       __syncthreads();
       taps_b = ch.b;
+      if (t == 0) kb_stamp(g, 1, 2);
     }
     if (ch.b != norm_b) {
       if (norm_b >= 0) kb_warp_finish<MODE>(e, nrm, bad, norm_b, nslots, slot, lane);
@@ -665,15 +706,19 @@ kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* 
       issue();
       const int st = t % kStages;
       mbar_wait(&full[st], (t / kStages) & 1);
+      if (t == 0) kb_stamp(g, 1, 3);
       const double* xt = xs + st * tb.stage_elems;
       if (active && !(g.dbg & 1))
         kb_sum_mma(D, xt + (s_off + ac) * kXS + ar, cpad + term * cstride + kCG + 8 + ac - ar, nch, two);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
+    if (t == r) kb_stamp(g, 1, 4);
     if (active && !(g.dbg & 2)) kb_sum_epilogue_regs<MODE>(D, g, e, ch, s_off, ar, ac, nrm, bad);
+    if (t == r) kb_stamp(g, 1, 5);
   }
   if (norm_b >= 0) kb_warp_finish<MODE>(e, nrm, bad, norm_b, nslots, slot, lane);
+  kb_stamp(g, 1, 6);
 }
 
 }  // namespace kb

@@ -60,6 +60,7 @@ EXPORTS = {
     "kb_apply_block": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
     "kb_block_residual": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
     "kb_fma_peak": (_c_int, [_c_int, ctypes.POINTER(ctypes.c_float), _vp]),
+    "kb_debug_trace": (_c_int, [ctypes.POINTER(ctypes.c_ulonglong), _c_int]),
     "kb_time_passes": (
         _c_int,
         [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_dp, _c_double, _vp,
