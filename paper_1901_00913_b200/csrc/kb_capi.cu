@@ -22,6 +22,7 @@
 #include "kb_kernels.cuh"
 #include "kb_dmma.cuh"
 #include "kb_ffma.cuh"
+#include "kb_tf32.cuh"
 
 namespace {
 
@@ -47,7 +48,7 @@ int fail(int code, const std::string& msg) {
 
 constexpr int kMaxHalf = 1024;
 constexpr int kGmaxF64 = 3;  // pass A term group (register budget: G*R accumulators)
-constexpr int kGmaxF32 = 8;
+constexpr int kGmaxF32 = 4;
 constexpr double kSymTol = 1e-11;  // (anti)symmetry residual allowed for sign-reflected fills
 constexpr int kRA = 8;   // pass A rows per warp
 constexpr int kRB = 16;  // pass B columns per warp
@@ -113,7 +114,8 @@ int persistent_blocks() {
 // box_rows} box: fp64 tiles are 36 columns wide (padded rows for the DMMA fragments), fp32 tiles
 // 32 (128-byte rows). False when TMA's alignment rules rule it out.
 bool make_tmap(CUtensorMap* map, const void* base, long long cols, long long rows, long long planes,
-               long long row_stride, long long plane_stride, int box_rows, int esize = 8) {
+               long long row_stride, long long plane_stride, int box_rows, int esize = 8,
+               int box_cols = 0) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   static bool tried = false;
   if (!tried) {
@@ -130,7 +132,8 @@ bool make_tmap(CUtensorMap* map, const void* base, long long cols, long long row
   if (box_rows < 1 || box_rows > 256) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)planes};
   const cuuint64_t strides[2] = {(cuuint64_t)row_stride * esize, (cuuint64_t)plane_stride * esize};
-  const cuuint32_t box[3] = {esize == 8 ? 36u : 32u, (cuuint32_t)box_rows, 1};
+  const cuuint32_t box[3] = {box_cols > 0 ? (cuuint32_t)box_cols : (esize == 8 ? 36u : 32u),
+                             (cuuint32_t)box_rows, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   return encode(map, esize == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                 const_cast<void*>(base), dims, strides, box, estr,
@@ -143,6 +146,15 @@ bool use_dmma(const kb_op* op) { return op->dtype == KB_F64 && op->m % 2 == 0 &&
 // fp32 runs on the persistent TMA + FFMA kernels when both extents are multiples of 4 (16-byte
 // row strides and vector stores); other shapes take the generic tiled kernels.
 bool use_tma_f32(const kb_op* op) { return op->dtype == KB_F32 && op->m % 4 == 0 && op->n % 4 == 0; }
+// fp32 arithmetic of the persistent kernels: 3xTF32 tensor-core MMA (kb_tf32.cuh, default) or
+// FFMA register windows (kb_ffma.cuh; KB_FP32_PATH=ffma)
+bool use_tf32(const kb_op* op) {
+  static const bool ffma = [] {
+    const char* v = std::getenv("KB_FP32_PATH");
+    return v && std::string(v) == "ffma";
+  }();
+  return use_tma_f32(op) && !ffma;
+}
 bool al16(const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; }
 // the persistent sum kernels move epilogue operands as 16-byte vectors
 template <typename T>
@@ -227,11 +239,43 @@ int allow_smem(K kernel, size_t dyn_bytes) {
   return KB_OK;
 }
 
-// Launch a persistent pass kernel (one block of 32 x kNW threads per work slot).
+// Tile ring depth for a persistent kernel: as many stages (2..kMaxStages) as fit next to the
+// taps when two blocks share an SM. KB_RING_STAGES caps it (profiling).
+int ring_stages(size_t stage_bytes, size_t fixed_bytes) {
+  static const int cap = [] {
+    const char* v = std::getenv("KB_RING_STAGES");
+    return v ? std::max(2, std::min(kb::kMaxStages, std::atoi(v))) : kb::kMaxStages;
+  }();
+  const size_t budget = 113 * 1024 - 1024;  // per block, two blocks per SM
+  int n = 2;
+  while (n < cap && fixed_bytes + (n + 1) * stage_bytes <= budget) ++n;
+  return n;
+}
+
+// Launch a persistent pass kernel (one block of 32 x kNW threads per work slot) with
+// programmatic stream serialization: in a stream or captured graph it may start while the
+// previous kernel drains; it loads its taps, then waits in griddepcontrol.wait for that
+// kernel's results (kb_dmma.cuh: pdl_wait). KB_PDL=0 turns it off.
+bool use_pdl() {
+  static const bool on = [] {
+    const char* v = std::getenv("KB_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
 template <typename... KArgs, typename... Args>
 cudaError_t launch_persistent(void (*kernel)(KArgs...), int nb, size_t smem, cudaStream_t s, Args&&... args) {
-  kernel<<<nb, dim3(32, kb::kNW), smem, s>>>(std::forward<Args>(args)...);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nb);
+  cfg.blockDim = dim3(32, kb::kNW);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = use_pdl() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 template <typename T, int GMAX>
@@ -281,6 +325,26 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
     }
     return launch_a_g<T, kGmaxF64>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
   } else {
+    if (use_tf32(op)) {
+      const kb::TileBoxesX tx = kb::tile_boxes_x(kb::tf32_rows(kb::kNW * 8, g.Wp));
+      CUtensorMap mapx;
+      if (make_tmap(&mapx, in - (long long)g.halo_lo * g.other, g.other, g.len + g.halo_lo + g.halo_hi,
+                    op->batch, g.other, in_bs, tx.box_rows, 4, kb::kXF)) {
+        const int nst = ring_stages(tx.stage_elems * sizeof(float), 2 * (size_t)op->r * kb::tf32_cstride(g.Wp) * 4);
+        const size_t smem = sizeof(float) * ((size_t)nst * tx.stage_elems +
+                                             2 * (size_t)op->r * kb::tf32_cstride(g.Wp));
+        auto kern = kb::kb_pass_split_x<kGmaxF32>;
+        KB_TRY(allow_smem(kern, smem));
+        int parts, nb, eparts;
+        kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb,
+                       mirror_h > 0 ? &eparts : nullptr);
+        if (mirror_h == 0) eparts = parts;
+        KB_CUDA(launch_persistent(kern, nb, smem, s, mapx, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r,
+                                  op->batch, parts, eparts, mirror_h, msign, nst));
+        op->last_mirror = mirror_h > 0;
+        return KB_OK;
+      }
+    }
     const kb::TileBoxesF tb = kb::tile_boxes_f(kb::kNW * 8 + g.Wp);
     CUtensorMap map;
     if (use_tma_f32(op) && make_tmap(&map, in - (long long)g.halo_lo * g.other, g.other,
@@ -333,6 +397,26 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
       return KB_OK;
     }
   } else {
+    if (use_tf32(op) && persistent_ok) {
+      const kb::TileBoxesX tx = kb::tile_boxes_x(kb::tf32_rows(kb::kNW * 16, g.Wp));
+      CUtensorMap mapx;
+      if (make_tmap(&mapx, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, tx.box_rows, 4,
+                    kb::kXF)) {
+        const int nst = ring_stages(tx.stage_elems * sizeof(float), 2 * (size_t)op->r * kb::tf32_cstride(g.Wp) * 4);
+        const size_t smem = sizeof(float) * ((size_t)nst * tx.stage_elems +
+                                             2 * (size_t)op->r * kb::tf32_cstride(g.Wp));
+        auto kern = kb::kb_pass_sum_x<MODE>;
+        KB_TRY(allow_smem(kern, smem));
+        int parts, nb;
+        kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
+        if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))
+          KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kNW, s));
+        op->last_slots = nb * kb::kNW;
+        KB_CUDA(launch_persistent(kern, nb, smem, s, mapx, op->r, tin, (long long)op->r * g.Wp, g, e, op->batch,
+                                  parts, nst));
+        return KB_OK;
+      }
+    }
     const kb::TileBoxesF tb = kb::tile_boxes_f(kb::kNW * 16 + g.Wp);
     CUtensorMap map;
     if (use_tma_f32(op) && persistent_ok &&

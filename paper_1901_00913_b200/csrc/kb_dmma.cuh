@@ -85,6 +85,13 @@ __device__ __forceinline__ void kb_stamp(const AxisGeom& g, int kind, int slot) 
     }
   }
 }
+// Programmatic dependent launch (no-ops without the launch attribute): let the next kernel of
+// the stream start its prologue on SMs this grid frees; wait until the previous kernel's results
+// are visible before touching anything it wrote.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 // order this thread's generic-proxy shared-memory writes before later async-proxy (TMA) access
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -131,23 +138,23 @@ struct Chunk {
 };
 
 struct ChunkWalk {
-  long long it, it_end;
+  int it, it_end;  // 32-bit: item counts and S * parts stay far below 2^31 for any plane
   int S, LT, parts, eparts, align;
   int b = 0, lt = 0, s = 0, s_end = 0;
   // eparts: S-parts of the two edge L-tiles (0 and LT-1), which may carry extra work
   __device__ ChunkWalk(int S_, int LT_, int parts_, int batch, int align_ = 1, int eparts_ = 0)
       : S(S_), LT(LT_), parts(parts_), eparts(eparts_ > 0 ? eparts_ : parts_), align(align_) {
-    const long long I = (long long)batch * per_image();
-    it = I * blockIdx.x / gridDim.x;
-    it_end = I * (blockIdx.x + 1) / gridDim.x;
+    const unsigned I = (unsigned)(batch * per_image());
+    it = (int)(I * blockIdx.x / gridDim.x);
+    it_end = (int)(I * (blockIdx.x + 1) / gridDim.x);
     load();
   }
   __device__ int per_image() const { return LT >= 2 ? (LT - 2) * parts + 2 * eparts : eparts; }
   __device__ void load() {
     if (it >= it_end) return;
     const int pi = per_image();
-    b = (int)(it / pi);
-    int i = (int)(it - (long long)b * pi), np;
+    b = it / pi;
+    int i = it - b * pi, np;
     if (i < eparts) {
       lt = 0;
       np = eparts;
@@ -161,8 +168,8 @@ struct ChunkWalk {
       i -= (lt - 1) * parts;
       np = parts;
     }
-    s = (int)((long long)i * S / np) / align * align;
-    s_end = i + 1 == np ? S : (int)((long long)(i + 1) * S / np) / align * align;
+    s = (int)((unsigned)i * (unsigned)S / (unsigned)np) / align * align;
+    s_end = i + 1 == np ? S : (int)((unsigned)(i + 1) * (unsigned)S / (unsigned)np) / align * align;
   }
   __device__ bool next(Chunk& c, int TS) {
     while (it < it_end) {
@@ -261,6 +268,37 @@ __device__ __forceinline__ double kb_quot(double a, double d, double rd) {
   const double q = __dmul_rn(a, rd);
   const double rem = fma(-d, q, a);
   return fma(rem, rd, q);
+}
+
+// Per-image taps [r][Wp] -> shared [r][cstride] with `guard` zeros before each row's taps and
+// zeros after them. The taps move as 16-byte vectors (Wp is a multiple of 16), all loads of a
+// thread issued before any store: one memory round trip at kernel start instead of several.
+__device__ __forceinline__ void kb_load_taps_d(double* __restrict__ cpad, const double* __restrict__ tb, int r,
+                                               int Wp, int cstride, int guard, int tid) {
+  const int n2 = r * Wp / 2, nw = Wp / 2;
+  constexpr int kV = 4;
+  for (int j0 = 0; j0 < n2; j0 += kV * 32 * kNW) {
+    double2 v[kV];
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const int j = j0 + u * 32 * kNW + tid;
+      if (j < n2) v[u] = reinterpret_cast<const double2*>(tb)[j];
+    }
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const int j = j0 + u * 32 * kNW + tid;
+      if (j < n2) {
+        const int i = j / nw, k = 2 * (j - i * nw);
+        cpad[i * cstride + guard + k] = v[u].x;
+        cpad[i * cstride + guard + k + 1] = v[u].y;
+      }
+    }
+  }
+  const int ng = cstride - Wp;  // guard entries per row
+  for (int idx = tid; idx < r * ng; idx += 32 * kNW) {
+    const int i = idx / ng, k = idx - i * ng;
+    cpad[i * cstride + (k < guard ? k : Wp + k)] = 0.0;
+  }
 }
 
 __device__ __forceinline__ void st_pair(double* p, double a, double b, bool both) {
@@ -378,20 +416,22 @@ kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict_
                   row0 + k * tb.box_rows, fc.b, &full[st]);
     ++nfill;
   };
+  // the first image's taps do not depend on the previous kernel: load them, then wait for it
+  // (programmatic dependent launch) and start the tile ring
+  pdl_launch_dependents();
+  kb_load_taps_d(cpad, tin + use_walk.b * t_bs, r, g.Wp, cstride, kCG, tid);
+  __syncthreads();
+  int taps_b = use_walk.b;
+  kb_stamp(g, 0, 2);
+  pdl_wait();
   for (int k = 0; k < kStages - 1; ++k) issue();
 
-  int taps_b = -1;
   for (int t = 0; use_walk.next(ch, TS); ++t) {
     if (ch.b != taps_b) {  // per-image taps (uniform across the block: block-level reload)
       __syncthreads();
-      const double* tbp = tin + ch.b * t_bs;
-      for (int idx = tid; idx < r * cstride; idx += 32 * kNW) {
-        const int i = idx / cstride, k = idx - i * cstride - kCG;
-        cpad[idx] = (k >= 0 && k < g.Wp) ? tbp[(long long)i * g.Wp + k] : 0.0;
-      }
+      kb_load_taps_d(cpad, tin + ch.b * t_bs, r, g.Wp, cstride, kCG, tid);
       __syncthreads();
       taps_b = ch.b;
-      if (t == 0) kb_stamp(g, 0, 2);
     }
     issue();  // keep kStages-1 tiles in flight ahead of the one consumed now
     const int st = t % kStages;
@@ -670,25 +710,26 @@ kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* 
     ++fterm;
     ++nfill;
   };
+  pdl_launch_dependents();
+  kb_load_taps_d(cpad, tin + use_walk.b * t_bs, r, g.Wp, cstride, kCG + 8, tid);
+  __syncthreads();
+  int taps_b = use_walk.b;
+  kb_stamp(g, 1, 2);
+  pdl_wait();
   for (int k = 0; k < kStages - 1; ++k) issue();
 
   double nrm[3] = {0.0, 0.0, 0.0};
   bool bad = false;
-  int norm_b = -1, taps_b = -1;
+  int norm_b = -1;
   double D[2][4][2];
   Chunk ch;
   int t = 0;
   while (use_walk.next(ch, TS)) {
     if (ch.b != taps_b) {  // per-image taps (uniform across the block)
       __syncthreads();
-      const double* tb = tin + ch.b * t_bs;
-      for (int idx = tid; idx < r * cstride; idx += 32 * kNW) {
-        const int i = idx / cstride, k = idx - i * cstride - kCG - 8;
-        cpad[idx] = (k >= 0 && k < g.Wp) ? tb[(long long)i * g.Wp + k] : 0.0;
-      }
+      kb_load_taps_d(cpad, tin + ch.b * t_bs, r, g.Wp, cstride, kCG + 8, tid);
       __syncthreads();
       taps_b = ch.b;
-      if (t == 0) kb_stamp(g, 1, 2);
     }
     if (ch.b != norm_b) {
       if (norm_b >= 0) kb_warp_finish<MODE>(e, nrm, bad, norm_b, nslots, slot, lane);

@@ -144,6 +144,42 @@ __global__ void __launch_bounds__(256, 2) dmma_split_k(double* out, int reps) {
   if (s == -1.2345) out[0] = s;
 }
 
+// legacy warp-level TF32 MMA (m16n8k8): 8 independent accumulators per warp
+__global__ void tf32_k(float* out, int iters) {
+  unsigned a[4], b[2];
+  for (int i = 0; i < 4; ++i) a[i] = __float_as_uint(threadIdx.x * 1e-3f + i);
+  for (int i = 0; i < 2; ++i) b[i] = __float_as_uint(threadIdx.x * 2e-3f - i);
+  float c[8][4] = {};
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+                   : "+f"(c[i][0]), "+f"(c[i][1]), "+f"(c[i][2]), "+f"(c[i][3])
+                   : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+  }
+  float s = 0;
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1] + c[i][2] + c[i][3];
+  if (s == -1.2345f) out[0] = s;
+}
+
+// legacy warp-level BF16 MMA (m16n8k16)
+__global__ void bf16_k(float* out, int iters) {
+  unsigned a[4], b[2];
+  for (int i = 0; i < 4; ++i) a[i] = 0x3f803f80u + threadIdx.x + i;
+  for (int i = 0; i < 2; ++i) b[i] = 0x3f803f80u + threadIdx.x - i;
+  float c[8][4] = {};
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+                   : "+f"(c[i][0]), "+f"(c[i][1]), "+f"(c[i][2]), "+f"(c[i][3])
+                   : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+  }
+  float s = 0;
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1] + c[i][2] + c[i][3];
+  if (s == -1.2345f) out[0] = s;
+}
+
 template <typename K, typename... A>
 float timeit(K k, int blocks, int threads, A... a) {
   cudaEvent_t e0, e1;
@@ -183,6 +219,13 @@ int main() {
     printf("DMMAs tpb=%d  %.2f TFLOP/s\n", tpb, 2.0 * 256 * 16 * (it / 16) * (double)blocks * (tpb / 32) / ms / 1e9);
     ms = timeit(dfma3_k, blocks, tpb, dout, it, 0.999);
     printf("DFMA3 tpb=%d  %.2f TFLOP/s\n", tpb, 2.0 * 8 * it * (double)blocks * tpb / ms / 1e9);
+  }
+  for (int tpb : {128, 256, 512}) {
+    const int blocks = sms * 4, it = 2048;
+    float ms = timeit(tf32_k, blocks, tpb, fout, it);
+    printf("TF32 mma.sync m16n8k8 tpb=%d  %.1f TFLOP/s\n", tpb, 2.0 * 16 * 8 * 8 * 8 * it * (double)blocks * (tpb / 32) / ms / 1e9);
+    ms = timeit(bf16_k, blocks, tpb, fout, it);
+    printf("BF16 mma.sync m16n8k16 tpb=%d  %.1f TFLOP/s\n", tpb, 2.0 * 16 * 8 * 16 * 8 * it * (double)blocks * (tpb / 32) / ms / 1e9);
   }
   {
     const int reps = 200;

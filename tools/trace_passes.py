@@ -1,6 +1,6 @@
 """Per-block timeline of the fp64 pass kernels (KB_DEBUG_MODE bit 7, kb_debug_trace).
 
-usage: KB_DEBUG_MODE=128 python tools/trace_passes.py [m]
+usage: KB_DEBUG_MODE=128 python tools/trace_passes.py [m] [float64|float32]
 Runs kb_apply (forward: split + plain sum) and one sFISTA iteration (last kernels: adjoint split
 + update sum) on cfg2 and prints, per kernel, the distribution over blocks of each stamp
 relative to the kernel's earliest start (us).
@@ -22,11 +22,12 @@ from paper_1901_00913_b200.device import device_operator, load_library
 from paper_1901_00913_b200.solvers import momentum_table
 
 m = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+dtype = sys.argv[2] if len(sys.argv) > 2 else "float64"
 cfg = W.CONFIGS["cfg2"]
 _, psf, B = W.make_image_data(cfg, seed=0, m=m, counts=(cfg.n_rect, cfg.n_disk) if m == cfg.m else (50, 25))
 op = kb.decompose(psf, kb.BoundaryCondition(cfg.bc), s=cfg.r, shape=(m, m))
-dev = device_operator(op, "float64")
-Bd = torch.from_numpy(B).cuda()
+dev = device_operator(op, dtype)
+Bd = torch.from_numpy(B).to("cuda", dev.tdtype)
 
 
 def trace():
