@@ -240,13 +240,13 @@ int allow_smem(K kernel, size_t dyn_bytes) {
 }
 
 // Tile ring depth for a persistent kernel: as many stages (2..kMaxStages) as fit next to the
-// taps when two blocks share an SM. KB_RING_STAGES caps it (profiling).
-int ring_stages(size_t stage_bytes, size_t fixed_bytes) {
+// taps at `bps` resident blocks per SM. KB_RING_STAGES caps it (profiling).
+int ring_stages(size_t stage_bytes, size_t fixed_bytes, int bps) {
   static const int cap = [] {
     const char* v = std::getenv("KB_RING_STAGES");
     return v ? std::max(2, std::min(kb::kMaxStages, std::atoi(v))) : kb::kMaxStages;
   }();
-  const size_t budget = 113 * 1024 - 1024;  // per block, two blocks per SM
+  const size_t budget = (bps >= 2 ? 114 : 228) * 1024 - 1024 - 128;
   int n = 2;
   while (n < cap && fixed_bytes + (n + 1) * stage_bytes <= budget) ++n;
   return n;
@@ -293,6 +293,17 @@ int launch_a_g(const T* in, long long in_bs, T* z, long long z_ps, long long z_b
   return KB_OK;
 }
 
+// Resident blocks per SM of a persistent pass kernel with `smem` bytes of dynamic shared memory:
+// 2 when two fit, 1 when only one does (wide bands), 0 when none does (the generic tiled
+// kernels then take the pass).
+int blocks_per_sm(size_t smem) {
+  const size_t per = smem + 1024 + 128;  // per-block reservation and static shared memory
+  if (2 * per <= 228 * 1024) return 2;
+  if (per <= 228 * 1024) return 1;
+  return 0;
+}
+int sm_count() { return persistent_blocks() / 2; }
+
 // Pass A into the Z^T planes (z: row 0 of image 0, term 0). mirror_h > 0 asks the persistent
 // kernels to also store the reflected halo rows (times msign[b][i]) for a reflect-filled pass B;
 // op->last_mirror records whether they did.
@@ -304,22 +315,28 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
   op->last_mirror = 0;
   const long long z_bs = z_ps * op->r;
   const long long t_bs = (long long)op->r * g.Wp;
+  const T* in_map = in - (long long)g.halo_lo * g.other;
+  const long long in_rows = g.len + g.halo_lo + g.halo_hi;
+  // common tail of the persistent launches: balanced items on `bps` blocks per SM
+  auto plan = [&](int bps, int& parts, int& nb, int& eparts) {
+    kb::plan_items(g.len, (g.other + 31) / 32, op->batch, sm_count() * bps, parts, nb,
+                   mirror_h > 0 ? &eparts : nullptr);  // edge L-tiles also store the halo rows
+    if (mirror_h == 0) eparts = parts;
+  };
   if constexpr (sizeof(T) == 8) {
-    constexpr int TS = kb::kNW * 8;
-    const kb::TileBoxes tb = kb::tile_boxes(kb::dmma_rows(TS, g.Wp));
+    const kb::TileBoxes tb = kb::tile_boxes(kb::dmma_rows(kb::kNW * 8, g.Wp));
+    const size_t smem = sizeof(double) * ((size_t)kb::kStages * tb.stage_elems +
+                                          (size_t)op->r * kb::dmma_cstride_split(g.Wp));
+    const int bps = blocks_per_sm(smem);
     CUtensorMap map;
-    if (use_dmma(op) && make_tmap(&map, in - (long long)g.halo_lo * g.other, g.other,
-                                  g.len + g.halo_lo + g.halo_hi, op->batch, g.other, in_bs, tb.box_rows)) {
-      const size_t smem = sizeof(double) * ((size_t)kb::kStages * tb.stage_elems +
-                                            (size_t)op->r * kb::dmma_cstride_split(g.Wp));
+    if (use_dmma(op) && bps > 0 &&
+        make_tmap(&map, in_map, g.other, in_rows, op->batch, g.other, in_bs, tb.box_rows)) {
       auto kern = kb::kb_pass_split_dmma<kGmaxF64>;
       KB_TRY(allow_smem(kern, smem));
-      int parts, nb, eparts;  // edge L-tiles also store the reflected halo rows: smaller parts
-      kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb,
-                     mirror_h > 0 ? &eparts : nullptr);
-      if (mirror_h == 0) eparts = parts;
+      int parts, nb, eparts;
+      plan(bps, parts, nb, eparts);
       KB_CUDA(launch_persistent(kern, nb, smem, s, map, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r, op->batch,
-                         parts, eparts, mirror_h, msign));
+                                parts, eparts, mirror_h, msign));
       op->last_mirror = mirror_h > 0;
       return KB_OK;
     }
@@ -327,18 +344,16 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
   } else {
     if (use_tf32(op)) {
       const kb::TileBoxesX tx = kb::tile_boxes_x(kb::tf32_rows(kb::kNW * 8, g.Wp));
+      const size_t fixed = 2 * (size_t)op->r * kb::tf32_cstride(g.Wp) * sizeof(float);
+      const int bps = blocks_per_sm(fixed + 2 * tx.stage_elems * sizeof(float));
+      const int nst = ring_stages(tx.stage_elems * sizeof(float), fixed, bps);
+      const size_t smem = fixed + sizeof(float) * (size_t)nst * tx.stage_elems;
       CUtensorMap mapx;
-      if (make_tmap(&mapx, in - (long long)g.halo_lo * g.other, g.other, g.len + g.halo_lo + g.halo_hi,
-                    op->batch, g.other, in_bs, tx.box_rows, 4, kb::kXF)) {
-        const int nst = ring_stages(tx.stage_elems * sizeof(float), 2 * (size_t)op->r * kb::tf32_cstride(g.Wp) * 4);
-        const size_t smem = sizeof(float) * ((size_t)nst * tx.stage_elems +
-                                             2 * (size_t)op->r * kb::tf32_cstride(g.Wp));
+      if (bps > 0 && make_tmap(&mapx, in_map, g.other, in_rows, op->batch, g.other, in_bs, tx.box_rows, 4, kb::kXF)) {
         auto kern = kb::kb_pass_split_x<kGmaxF32>;
         KB_TRY(allow_smem(kern, smem));
         int parts, nb, eparts;
-        kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb,
-                       mirror_h > 0 ? &eparts : nullptr);
-        if (mirror_h == 0) eparts = parts;
+        plan(bps, parts, nb, eparts);
         KB_CUDA(launch_persistent(kern, nb, smem, s, mapx, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r,
                                   op->batch, parts, eparts, mirror_h, msign, nst));
         op->last_mirror = mirror_h > 0;
@@ -346,19 +361,17 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
       }
     }
     const kb::TileBoxesF tb = kb::tile_boxes_f(kb::kNW * 8 + g.Wp);
+    const size_t smem = sizeof(float) * ((size_t)kb::kStages * tb.stage_elems + (size_t)op->r * g.Wp);
+    const int bps = blocks_per_sm(smem);
     CUtensorMap map;
-    if (use_tma_f32(op) && make_tmap(&map, in - (long long)g.halo_lo * g.other, g.other,
-                                     g.len + g.halo_lo + g.halo_hi, op->batch, g.other, in_bs,
-                                     tb.box_rows, 4)) {
-      const size_t smem = sizeof(float) * ((size_t)kb::kStages * tb.stage_elems + (size_t)op->r * g.Wp);
+    if (use_tma_f32(op) && bps > 0 &&
+        make_tmap(&map, in_map, g.other, in_rows, op->batch, g.other, in_bs, tb.box_rows, 4)) {
       auto kern = kb::kb_pass_split_f<kGmaxF32>;
       KB_TRY(allow_smem(kern, smem));
-      int parts, nb, eparts;  // edge L-tiles also store the reflected halo rows: smaller parts
-      kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb,
-                     mirror_h > 0 ? &eparts : nullptr);
-      if (mirror_h == 0) eparts = parts;
+      int parts, nb, eparts;
+      plan(bps, parts, nb, eparts);
       KB_CUDA(launch_persistent(kern, nb, smem, s, map, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r, op->batch,
-                         parts, eparts, mirror_h, msign));
+                                parts, eparts, mirror_h, msign));
       op->last_mirror = mirror_h > 0;
       return KB_OK;
     }
@@ -379,59 +392,46 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
   const T* zmap = z - (long long)g.halo_lo * g.other;
   const long long zrows = g.len + g.halo_lo + g.halo_hi;
   const bool persistent_ok = (!g_in.fill || mirrored) && epi_aligned(e);
+  // common tail of the persistent launches
+  auto launch = [&](auto kern, size_t smem, int bps, const CUtensorMap& map, auto... extra) -> int {
+    KB_TRY(allow_smem(kern, smem));
+    int parts, nb;
+    kb::plan_items(g.len, (g.other + 31) / 32, op->batch, sm_count() * bps, parts, nb);
+    if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // warps skip untouched images
+      KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kNW, s));
+    op->last_slots = nb * kb::kNW;
+    KB_CUDA(launch_persistent(kern, nb, smem, s, map, op->r, tin, (long long)op->r * g.Wp, g, e, op->batch,
+                              parts, extra...));
+    return KB_OK;
+  };
   if constexpr (sizeof(T) == 8) {
     const kb::TileBoxes tb = kb::tile_boxes(kb::dmma_rows(kb::kNW * 16, g.Wp));
+    const size_t smem = sizeof(double) * ((size_t)kb::kStages * tb.stage_elems +
+                                          (size_t)op->r * kb::dmma_cstride_sum(g.Wp));
+    const int bps = blocks_per_sm(smem);
     CUtensorMap map;
-    if (use_dmma(op) && persistent_ok &&
-        make_tmap(&map, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, tb.box_rows)) {
-      const size_t smem = sizeof(double) * ((size_t)kb::kStages * tb.stage_elems +
-                                            (size_t)op->r * kb::dmma_cstride_sum(g.Wp));
-      auto kern = kb::kb_pass_sum_dmma<MODE>;
-      KB_TRY(allow_smem(kern, smem));
-      int parts, nb;
-      kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
-      if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // warps skip untouched images
-        KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kNW, s));
-      op->last_slots = nb * kb::kNW;
-      KB_CUDA(launch_persistent(kern, nb, smem, s, map, op->r, tin, (long long)op->r * g.Wp, g, e, op->batch, parts));
-      return KB_OK;
-    }
+    if (use_dmma(op) && persistent_ok && bps > 0 &&
+        make_tmap(&map, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, tb.box_rows))
+      return launch(kb::kb_pass_sum_dmma<MODE>, smem, bps, map);
   } else {
     if (use_tf32(op) && persistent_ok) {
       const kb::TileBoxesX tx = kb::tile_boxes_x(kb::tf32_rows(kb::kNW * 16, g.Wp));
+      const size_t fixed = 2 * (size_t)op->r * kb::tf32_cstride(g.Wp) * sizeof(float);
+      const int bps = blocks_per_sm(fixed + 2 * tx.stage_elems * sizeof(float));
+      const int nst = ring_stages(tx.stage_elems * sizeof(float), fixed, bps);
+      const size_t smem = fixed + sizeof(float) * (size_t)nst * tx.stage_elems;
       CUtensorMap mapx;
-      if (make_tmap(&mapx, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, tx.box_rows, 4,
-                    kb::kXF)) {
-        const int nst = ring_stages(tx.stage_elems * sizeof(float), 2 * (size_t)op->r * kb::tf32_cstride(g.Wp) * 4);
-        const size_t smem = sizeof(float) * ((size_t)nst * tx.stage_elems +
-                                             2 * (size_t)op->r * kb::tf32_cstride(g.Wp));
-        auto kern = kb::kb_pass_sum_x<MODE>;
-        KB_TRY(allow_smem(kern, smem));
-        int parts, nb;
-        kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
-        if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))
-          KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kNW, s));
-        op->last_slots = nb * kb::kNW;
-        KB_CUDA(launch_persistent(kern, nb, smem, s, mapx, op->r, tin, (long long)op->r * g.Wp, g, e, op->batch,
-                                  parts, nst));
-        return KB_OK;
-      }
+      if (bps > 0 && make_tmap(&mapx, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps,
+                               tx.box_rows, 4, kb::kXF))
+        return launch(kb::kb_pass_sum_x<MODE>, smem, bps, mapx, nst);
     }
     const kb::TileBoxesF tb = kb::tile_boxes_f(kb::kNW * 16 + g.Wp);
+    const size_t smem = sizeof(float) * ((size_t)kb::kStages * tb.stage_elems + (size_t)op->r * g.Wp);
+    const int bps = blocks_per_sm(smem);
     CUtensorMap map;
-    if (use_tma_f32(op) && persistent_ok &&
-        make_tmap(&map, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, tb.box_rows, 4)) {
-      const size_t smem = sizeof(float) * ((size_t)kb::kStages * tb.stage_elems + (size_t)op->r * g.Wp);
-      auto kern = kb::kb_pass_sum_f<MODE>;
-      KB_TRY(allow_smem(kern, smem));
-      int parts, nb;
-      kb::plan_items(g.len, (g.other + 31) / 32, op->batch, persistent_blocks(), parts, nb);
-      if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))
-        KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kNW, s));
-      op->last_slots = nb * kb::kNW;
-      KB_CUDA(launch_persistent(kern, nb, smem, s, map, op->r, tin, (long long)op->r * g.Wp, g, e, op->batch, parts));
-      return KB_OK;
-    }
+    if (use_tma_f32(op) && persistent_ok && bps > 0 &&
+        make_tmap(&map, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, tb.box_rows, 4))
+      return launch(kb::kb_pass_sum_f<MODE>, smem, bps, map);
   }
   constexpr int TS = kb::kNW * kRB;
   const size_t smem = sizeof(T) * (2 * (size_t)(TS + g.Wp) * 32 + 2 * (size_t)g.Wp);

@@ -196,18 +196,29 @@ __device__ __forceinline__ void kb_split_group_x(const float* __restrict__ xs, c
     }
     // the three products of every accumulator are issued as three independent sweeps, so
     // consecutive MMAs never wait on each other's accumulator
+    // each K-step's products accumulate from zero and are added to D with a round-to-nearest
+    // FADD: the tensor core's own fp32 accumulation drifts over long K (wide bands, many terms)
+    float T[G][2][4];
 #pragma unroll
     for (int gg = 0; gg < G; ++gg)
 #pragma unroll
-      for (int m = 0; m < 2; ++m) mma_tf32(D[gg][m], al[m], bh[gg][0], bh[gg][1]);
+      for (int m = 0; m < 2; ++m) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) T[gg][m][i] = 0.f;
+        mma_tf32(T[gg][m], al[m], bh[gg][0], bh[gg][1]);
+      }
 #pragma unroll
     for (int gg = 0; gg < G; ++gg)
 #pragma unroll
-      for (int m = 0; m < 2; ++m) mma_tf32(D[gg][m], ah[m], bl[gg][0], bl[gg][1]);
+      for (int m = 0; m < 2; ++m) mma_tf32(T[gg][m], ah[m], bl[gg][0], bl[gg][1]);
 #pragma unroll
     for (int gg = 0; gg < G; ++gg)
 #pragma unroll
-      for (int m = 0; m < 2; ++m) mma_tf32(D[gg][m], ah[m], bh[gg][0], bh[gg][1]);
+      for (int m = 0; m < 2; ++m) {
+        mma_tf32(T[gg][m], ah[m], bh[gg][0], bh[gg][1]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) D[gg][m][i] += T[gg][m][i];
+      }
   }
   const int s = s_off + 2 * q;
   if (s >= ch.cnt || (g.dbg & 2)) return;
@@ -478,21 +489,29 @@ __device__ __forceinline__ void kb_sum_mma_x(float (&D)[2][2][4], const float* _
       l[nt][1] = bl[o + 4];
     }
     // three independent sweeps over the accumulators (see kb_split_group_x)
+    float T[2][2][4];  // per-K-step partials, added with round-to-nearest (see kb_split_group_x)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) T[nt][m][i] = 0.f;
+        if (nt == 0 ? N0 : N1) mma_tf32(T[nt][m], al[m], h[nt][0], h[nt][1]);
+      }
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int m = 0; m < 2; ++m)
-        if (nt == 0 ? N0 : N1) mma_tf32(D[nt][m], al[m], h[nt][0], h[nt][1]);
+        if (nt == 0 ? N0 : N1) mma_tf32(T[nt][m], ah[m], l[nt][0], l[nt][1]);
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int m = 0; m < 2; ++m)
-        if (nt == 0 ? N0 : N1) mma_tf32(D[nt][m], ah[m], l[nt][0], l[nt][1]);
+        if (nt == 0 ? N0 : N1) {
+          mma_tf32(T[nt][m], ah[m], h[nt][0], h[nt][1]);
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-      for (int m = 0; m < 2; ++m)
-        if (nt == 0 ? N0 : N1) mma_tf32(D[nt][m], ah[m], h[nt][0], h[nt][1]);
+          for (int i = 0; i < 4; ++i) D[nt][m][i] += T[nt][m][i];
+        }
   }
 }
 
