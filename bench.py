@@ -36,8 +36,8 @@ MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
-    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--config", default=CFG)
     p.add_argument("--dtype", default="float64", choices=["float64", "float32"])
@@ -63,6 +63,13 @@ def committed_traffic(dtype):
             return json.load(f).get(dtype)
     except (OSError, ValueError):
         return None
+
+
+def l2_note(cfg, dtype):
+    esz = 8 if dtype == "float64" else 4
+    ws = (4 + cfg.r) * cfg.m * cfg.m * esz / 1e6  # X, Y, B, R and the r Z planes
+    where = "L2-resident within a solve" if ws < 100 else "larger than L2 (HBM-backed)"
+    return f"flushed between steps (256 MiB write); {ws:.0f} MB working set is {where}"
 
 
 def algorithmic(cfg):
@@ -235,24 +242,31 @@ def run_b200(args):
     it_ms = sum(kern_ms)
     F = algorithmic(cfg)
     flops_it = F * m * m
-    peak_fma = fma_peak(args.dtype)
+    # binding compute roof: the tensor instruction the passes issue, measured live. fp32 runs
+    # 3xTF32 (three TF32 MMAs per fp32-accurate product), so its roof is the TF32 rate / 3.
+    peak_fma = fma_peak(args.dtype) / (3.0 if args.dtype == "float32" else 1.0)
     peaks, peak_kind = measured_peaks()
     achieved_tf = flops_it / (it_ms * 1e-3) / 1e12
     hbm_gbs = 8 * esz * m * m / (it_ms * 1e-3) / 1e9
     roofline = {
-        "bound": "tensor" if args.dtype == "float64" else "fma",
+        "bound": "tensor",
         "kernel": "one sFISTA iteration = kb_pass_a(fwd) + kb_pass_b(resid) + kb_pass_a(adj) + kb_pass_b(update)",
         "achieved": round(achieved_tf, 3), "peak": round(peak_fma, 3), "unit": "TFLOP/s",
         "frac": round(achieved_tf / peak_fma, 4),
         "peak_source": ("measured live by kb_fma_peak in this run: "
                         + ("FP64 tensor-core DMMA m8n8k4 burn (the pass kernels' instruction)"
-                           if args.dtype == "float64" else "FFMA chains")),
+                           if args.dtype == "float64" else
+                           "TF32 tensor-core mma.sync m16n8k8 burn / 3 (3xTF32 passes)")),
         "per_kernel_ms": [round(x, 5) for x in kern_ms],
         "traffic": committed_traffic(args.dtype),
         "hbm": {"achieved": round(hbm_gbs, 1), "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                 "frac": round(hbm_gbs / peaks.get("hbm_gbs", 6550.0), 4), "peak_source": peak_kind,
                 "algorithmic_bytes_per_px_it": 8 * esz},
         "algorithmic_flops_per_px_it": F,
+        # taps the kernels execute per axis after trimming entries below 1e-14 of a generator's
+        # peak; narrower than w when the PSF is ~0 near its window edges (cfg5's
+        # motion line), in which case achieved (counted with the nominal w) can exceed the roof
+        "executed_taps": [dev.bands[1], dev.bands[3]],
     }
 
     variants = {}
@@ -277,11 +291,11 @@ def run_b200(args):
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "f64" if args.dtype == "float64" else "f32",
-            "data": "synthetic (seeded phantom + PSF + exact-level Gaussian noise, BASELINE cfg2)",
+            "data": f"synthetic (seeded phantom + PSF + exact-level Gaussian noise, BASELINE {cfg.name})",
             "config": {"workload": f"{args.config}: {m}x{m} {cfg.bc} BC, w={cfg.w}, r={cfg.r}, "
                                    f"lam={cfg.lam}, x>=0, {iters} iterations per step",
                        "global_batch": world, "parallelism": f"replicas{world}",
-                       "l2": "flushed between steps (256 MiB write); 40 MB working set is L2-resident within a solve"},
+                       "l2": l2_note(cfg, args.dtype)},
             "e2e": e2e,
             "roofline": roofline,
             "gpu_launches": 4 * iters * args.steps,
@@ -351,7 +365,7 @@ def run_reference(args):
         "metric": "sFISTA Mpixel*iterations/s", "value": round(value, 4), "unit": "Mpixel*iterations/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (BASELINE cfg2)",
+        "data": f"synthetic (BASELINE {cfg.name})",
         "config": {"workload": f"{args.config}: one projected sFISTA iteration per step on the CPU port",
                    "global_batch": 1, "parallelism": "cpu"},
         "impl": "reference",
