@@ -65,11 +65,17 @@ def committed_traffic(dtype):
         return None
 
 
-def l2_note(cfg, dtype):
+def l2_note(cfg, dtype, images=1):
     esz = 8 if dtype == "float64" else 4
-    ws = (4 + cfg.r) * cfg.m * cfg.m * esz / 1e6  # X, Y, B, R and the r Z planes
+    ws = images * (4 + cfg.r) * cfg.m * cfg.m * esz / 1e6  # X, Y, B, R and the r Z planes
     where = "L2-resident within a solve" if ws < 100 else "larger than L2 (HBM-backed)"
     return f"flushed between steps (256 MiB write); {ws:.0f} MB working set is {where}"
+
+
+def device_operator_batch(ops, dtype):
+    from paper_1901_00913_b200.device import DeviceOperator
+
+    return DeviceOperator(list(ops), dtype)
 
 
 def algorithmic(cfg):
@@ -137,14 +143,25 @@ class ClockSampler:
                 "sm_max_mhz": num(rows[0][1]), "reasons": reasons, "samples": len(rows)}
 
 
-def build_problem(cfg, dtype, seed=0, device="cuda"):
+def build_problem(cfg, dtype, seed=0, device="cuda", images=None):
+    """Seeded data, operator(s) and Lipschitz constant(s) of a config. Single-image configs give
+    (B [m,m], op, L); batch configs (cfg3) give this rank's images (B [count,m,m], [op], [L])."""
     import paper_1901_00913_b200 as kb
     from paper_1901_00913_b200 import workloads as W
 
-    X, psf, B = W.make_image_data(cfg, seed=seed, device=device)
-    op = kb.decompose(psf, kb.BoundaryCondition(cfg.bc), s=cfg.r, shape=(cfg.m, cfg.m))
-    L = kb.lipschitz(op, iters=50, seed=seed, dtype="float64")
-    return X, psf, B, op, L
+    if images is None:
+        X, psf, B = W.make_image_data(cfg, seed=seed, device=device)
+        op = kb.decompose(psf, kb.BoundaryCondition(cfg.bc), s=cfg.r, shape=(cfg.m, cfg.m))
+        L = kb.lipschitz(op, iters=50, seed=seed, dtype="float64")
+        return B, op, L
+    Bs, ops, Ls = [], [], []
+    for i in images:  # each image has its own phantom and PSF (BASELINE cfg3)
+        _, psf, B = W.make_image_data(cfg, seed=0, index=i, device=device)
+        op = kb.decompose(psf, kb.BoundaryCondition(cfg.bc), s=cfg.r, shape=(cfg.m, cfg.m))
+        Bs.append(B)
+        ops.append(op)
+        Ls.append(kb.lipschitz(op, iters=50, seed=0, dtype="float64"))
+    return np.stack(Bs), ops, np.array(Ls)
 
 
 def run_b200(args):
@@ -178,11 +195,22 @@ def run_b200(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    X, psf, B, op, L = build_problem(cfg, args.dtype, seed=rank)
+    batched = cfg.batch > 1
+    if batched:  # cfg3: the batch is sharded across ranks with no communication (strong scaling)
+        from paper_1901_00913_b200.shard import batch_partition
+
+        start, count = batch_partition(cfg.batch, world)[rank]
+        B, ops, L = build_problem(cfg, args.dtype, images=range(start, start + count))
+        op = ops[0]
+    else:
+        B, op, L = build_problem(cfg, args.dtype, seed=rank)
+        ops = [op]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def measure(dtype, steps, warmup, clocks=False):
-        dev = device_operator(op, dtype)
+        from paper_1901_00913_b200.device import DeviceOperator
+
+        dev = DeviceOperator(ops, dtype) if batched else device_operator(op, dtype)
         _, beta = kb.momentum_table(iters)
         Bd = torch.from_numpy(B).to("cuda", dev.tdtype)
         Xd, Yd = torch.zeros_like(Bd), torch.zeros_like(Bd)
@@ -216,38 +244,50 @@ def run_b200(args):
     dev, Bd, ms, clocks = measure(args.dtype, args.steps, args.warmup, clocks=True)
     ms = max_over_ranks(ms)
     mpix_it = m * m * iters / 1e6
-    value = world * mpix_it / (ms / 1e3)
+    # whole-job units: every rank's images (batch) or one image per replica
+    units = cfg.batch if batched else world
+    value = units * mpix_it / (ms / 1e3)
 
     # ---- e2e: public API with host buffers (H2D of B and X0, D2H of x inside the region)
-    cfgsolve = kb.SolveConfig(lam=cfg.lam, lipschitz=L, max_iter=iters, record_history=False)
+    cfgsolve = kb.SolveConfig(lam=cfg.lam, lipschitz=float(np.max(L)), max_iter=iters, record_history=False)
     opts = kb.SolveOptions(dtype=args.dtype, project=True, use_graph=True)
-    for _ in range(args.warmup):
-        kb.sfista(op, B, cfgsolve, options=opts)
+    esz = 8 if args.dtype == "float64" else 4
+    if batched:  # public batch API with host arrays: H2D of B, D2H of x inside the region
+        dev_e2e = device_operator_batch(ops, args.dtype)
+
+        def e2e_call():
+            kb.sfista_batch(dev_e2e, B, L, cfg.lam, iters, options=opts)
+    else:
+        def e2e_call():
+            kb.sfista(op, B, cfgsolve, options=opts)
+    for _ in range(min(args.warmup, 3)):
+        e2e_call()
     e2e_t = []
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        run = kb.sfista(op, B, cfgsolve, options=opts)
+        e2e_call()
         torch.cuda.synchronize()
         e2e_t.append(time.perf_counter() - t0)
     e2e_s = max_over_ranks(sum(e2e_t) / len(e2e_t))
-    esz = 8 if args.dtype == "float64" else 4
-    e2e = {"value": world * mpix_it / e2e_s, "unit": "Mpixel*iterations/s",
-           "h2d_bytes_per_step": 2 * m * m * esz, "d2h_bytes_per_step": m * m * esz}
+    nimg = len(ops)
+    e2e = {"value": units * mpix_it / e2e_s, "unit": "Mpixel*iterations/s",
+           "h2d_bytes_per_step": (1 if batched else 2) * nimg * m * m * esz,
+           "d2h_bytes_per_step": nimg * m * m * esz}
 
     # ---- roofline of the iteration kernels (CUDA events, same stream)
     kern_ms = dev.time_passes(Bd, Bd, L, cfg.lam, reps=20)
     it_ms = sum(kern_ms)
     F = algorithmic(cfg)
-    flops_it = F * m * m
+    flops_it = F * m * m * len(ops)
     # binding compute roof: the tensor instruction the passes issue, measured live. fp32 runs
     # 3xTF32 (three TF32 MMAs per fp32-accurate product), so its roof is the TF32 rate / 3.
     peak_fma = fma_peak(args.dtype) / (3.0 if args.dtype == "float32" else 1.0)
     peaks, peak_kind = measured_peaks()
     achieved_tf = flops_it / (it_ms * 1e-3) / 1e12
-    hbm_gbs = 8 * esz * m * m / (it_ms * 1e-3) / 1e9
+    hbm_gbs = 8 * esz * m * m * len(ops) / (it_ms * 1e-3) / 1e9
     roofline = {
         "bound": "tensor",
         "kernel": "one sFISTA iteration = kb_pass_a(fwd) + kb_pass_b(resid) + kb_pass_a(adj) + kb_pass_b(update)",
@@ -272,11 +312,11 @@ def run_b200(args):
     variants = {}
     if not args.no_variants and world == 1 and "float32" in cfg.dtypes and args.dtype != "float32":
         _, _, ms32, _ = measure("float32", max(2, args.steps // 2), 2)
-        variants["float32"] = {"value": mpix_it / (ms32 / 1e3), "ms_per_step": ms32}
+        variants["float32"] = {"value": units * mpix_it / (ms32 / 1e3), "ms_per_step": ms32}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, op, B, L, iters_sample=2)
+        cpu = cpu_baseline(cfg, op, B[0] if batched else B, L[0] if batched else L, iters_sample=2)
 
     if rank == 0:
         line = {
@@ -288,14 +328,16 @@ def run_b200(args):
             "warmup": args.warmup,
             "ms_per_step": round(ms, 4),
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if batched else "weak",
             "vs_baseline": None,
             "dtype": "f64" if args.dtype == "float64" else "f32",
             "data": f"synthetic (seeded phantom + PSF + exact-level Gaussian noise, BASELINE {cfg.name})",
-            "config": {"workload": f"{args.config}: {m}x{m} {cfg.bc} BC, w={cfg.w}, r={cfg.r}, "
-                                   f"lam={cfg.lam}, x>=0, {iters} iterations per step",
-                       "global_batch": world, "parallelism": f"replicas{world}",
-                       "l2": l2_note(cfg, args.dtype)},
+            "config": {"workload": f"{args.config}: {(str(cfg.batch) + ' x ') if batched else ''}{m}x{m} "
+                                   f"{cfg.bc} BC, w={cfg.w}, r={cfg.r}, lam={cfg.lam}, x>=0, "
+                                   f"{iters} iterations per step",
+                       "global_batch": cfg.batch if batched else world,
+                       "parallelism": f"batch-shard{world}" if batched else f"replicas{world}",
+                       "l2": l2_note(cfg, args.dtype, len(ops))},
             "e2e": e2e,
             "roofline": roofline,
             "gpu_launches": 4 * iters * args.steps,
