@@ -324,9 +324,9 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
     if (mirror_h == 0) eparts = parts;
   };
   if constexpr (sizeof(T) == 8) {
-    const kb::TileBoxes tb = kb::tile_boxes(kb::dmma_rows(kb::kNW * 8, g.Wp));
+    const kb::TileBoxes tb = kb::tile_boxes(kb::dmma_rows(kb::kNW * 8, g.Kw));
     const size_t smem = sizeof(double) * ((size_t)kb::kStages * tb.stage_elems +
-                                          (size_t)op->r * kb::dmma_cstride_split(g.Wp));
+                                          (size_t)op->r * kb::dmma_cstride_split(g.Kw));
     const int bps = blocks_per_sm(smem);
     CUtensorMap map;
     if (use_dmma(op) && bps > 0 &&
@@ -343,8 +343,8 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
     return launch_a_g<T, kGmaxF64>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
   } else {
     if (use_tf32(op)) {
-      const kb::TileBoxesX tx = kb::tile_boxes_x(kb::tf32_rows(kb::kNW * 8, g.Wp));
-      const size_t fixed = 2 * (size_t)op->r * kb::tf32_cstride(g.Wp) * sizeof(float);
+      const kb::TileBoxesX tx = kb::tile_boxes_x(kb::tf32_rows(kb::kNW * 8, g.Kw));
+      const size_t fixed = 2 * (size_t)op->r * kb::tf32_cstride(g.Kw) * sizeof(float);
       const int bps = blocks_per_sm(fixed + 2 * tx.stage_elems * sizeof(float));
       const int nst = ring_stages(tx.stage_elems * sizeof(float), fixed, bps);
       const size_t smem = fixed + sizeof(float) * (size_t)nst * tx.stage_elems;
@@ -405,9 +405,9 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
     return KB_OK;
   };
   if constexpr (sizeof(T) == 8) {
-    const kb::TileBoxes tb = kb::tile_boxes(kb::dmma_rows(kb::kNW * 16, g.Wp));
+    const kb::TileBoxes tb = kb::tile_boxes(kb::dmma_rows(kb::kNW * 16, g.Kw));
     const size_t smem = sizeof(double) * ((size_t)kb::kStages * tb.stage_elems +
-                                          (size_t)op->r * kb::dmma_cstride_sum(g.Wp));
+                                          (size_t)op->r * kb::dmma_cstride_sum(g.Kw));
     const int bps = blocks_per_sm(smem);
     CUtensorMap map;
     if (use_dmma(op) && persistent_ok && bps > 0 &&
@@ -415,8 +415,8 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
       return launch(kb::kb_pass_sum_dmma<MODE>, smem, bps, map);
   } else {
     if (use_tf32(op) && persistent_ok) {
-      const kb::TileBoxesX tx = kb::tile_boxes_x(kb::tf32_rows(kb::kNW * 16, g.Wp));
-      const size_t fixed = 2 * (size_t)op->r * kb::tf32_cstride(g.Wp) * sizeof(float);
+      const kb::TileBoxesX tx = kb::tile_boxes_x(kb::tf32_rows(kb::kNW * 16, g.Kw));
+      const size_t fixed = 2 * (size_t)op->r * kb::tf32_cstride(g.Kw) * sizeof(float);
       const int bps = blocks_per_sm(fixed + 2 * tx.stage_elems * sizeof(float));
       const int nst = ring_stages(tx.stage_elems * sizeof(float), fixed, bps);
       const size_t smem = fixed + sizeof(float) * (size_t)nst * tx.stage_elems;
@@ -469,6 +469,7 @@ kb::AxisGeom geom_a(const kb_op* op, int adjoint, const RowBlock& rb) {
   g.other = op->n;
   g.H = op->Ha;
   g.Wp = op->Wpa;
+  g.Kw = (2 * op->Ha + 1 + 3) / 4 * 4;
   g.fill = op->bc_a == KB_BC_REFLECTIVE && (!adjoint || op->sym_a);
   g.g0 = rb.g0;
   g.Mg = rb.mg;
@@ -484,6 +485,7 @@ kb::AxisGeom geom_b(const kb_op* op, int adjoint) {  // sum pass over Z_i^T [n][
   g.other = op->m;
   g.H = op->Hb;
   g.Wp = op->Wpb;
+  g.Kw = (2 * op->Hb + 1 + 3) / 4 * 4;
   g.fill = op->bc_b == KB_BC_REFLECTIVE && (!adjoint || op->sym_b);
   g.g0 = 0;
   g.Mg = op->n;
@@ -753,7 +755,28 @@ __global__ void kb_dmma_burn(double* out, int iters) {
   if (sum == -12345.678) out[0] = sum;
 }
 
-// Peak of the arithmetic instruction the pass kernels issue: DMMA for fp64, FFMA for fp32.
+// TF32 tensor-core burn: 12 independent m16n8k8 accumulators per warp (1024 FMAs each)
+__global__ void kb_tf32_burn(float* out, int iters) {
+  unsigned a[4], b[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) a[i] = __float_as_uint(threadIdx.x * 1e-3f + i);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) b[i] = __float_as_uint(threadIdx.x * 2e-3f - i);
+  float c[12][4];
+#pragma unroll
+  for (int i = 0; i < 12; ++i) c[i][0] = c[i][1] = c[i][2] = c[i][3] = 0.f;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 12; ++i) kb::mma_tf32(c[i], a, b[0], b[1]);
+  }
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < 12; ++i) sum += c[i][0] + c[i][1] + c[i][2] + c[i][3];
+  if (sum == -12345.678f) out[0] = sum;
+}
+
+// Peak of the arithmetic instruction the pass kernels issue: DMMA for fp64, TF32 mma.sync for
+// fp32 (raw TF32 rate; the 3xTF32 passes issue three per product).
 template <typename T>
 int fma_peak_t(float* tflops, cudaStream_t s) {
   int dev = 0, sms = 0;
@@ -768,7 +791,7 @@ int fma_peak_t(float* tflops, cudaStream_t s) {
   const int reps = 5;
   auto burn = [&]() {
     if constexpr (sizeof(T) == 8) kb_dmma_burn<<<blocks, threads, 0, s>>>(out, iters / 8);
-    else kb_fma_burn<T><<<blocks, threads, 0, s>>>(out, iters, T(0.999999), T(1e-7));
+    else kb_tf32_burn<<<blocks, threads, 0, s>>>(reinterpret_cast<float*>(out), iters / 16);
   };
   burn();  // warm-up
   cudaEventRecord(e0, s);
@@ -782,7 +805,7 @@ int fma_peak_t(float* tflops, cudaStream_t s) {
   cudaFree(out);
   if (ce != cudaSuccess) return fail(KB_ERR_CUDA, cudaGetErrorString(ce));
   const double flops = sizeof(T) == 8 ? 2.0 * 256.0 * 8.0 * (double)(iters / 8) * (threads / 32) * blocks * reps
-                                      : 2.0 * 8.0 * (double)iters * threads * blocks * reps;
+                                      : 2.0 * 1024.0 * 12.0 * (double)(iters / 16) * (threads / 32) * blocks * reps;
   *tflops = (float)(flops / (ms * 1e-3) / 1e12);
   return KB_OK;
 }

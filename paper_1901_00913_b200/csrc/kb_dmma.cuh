@@ -270,11 +270,11 @@ __device__ __forceinline__ double kb_quot(double a, double d, double rd) {
   return fma(rem, rd, q);
 }
 
-// Per-image taps [r][Wp] -> shared [r][cstride] with `guard` zeros before each row's taps and
-// zeros after them. The taps move as 16-byte vectors (Wp is a multiple of 16), all loads of a
-// thread issued before any store: one memory round trip at kernel start instead of several.
+// Per-image taps (global [r][Wp], Wp a multiple of 16) -> shared [r][cstride]: the first Kw taps
+// of each row after `guard` zeros, zeros after them. The taps move as 16-byte vectors, all loads
+// of a thread issued before any store: one memory round trip at kernel start.
 __device__ __forceinline__ void kb_load_taps_d(double* __restrict__ cpad, const double* __restrict__ tb, int r,
-                                               int Wp, int cstride, int guard, int tid) {
+                                               int Wp, int Kw, int cstride, int guard, int tid) {
   const int n2 = r * Wp / 2, nw = Wp / 2;
   constexpr int kV = 4;
   for (int j0 = 0; j0 < n2; j0 += kV * 32 * kNW) {
@@ -289,15 +289,15 @@ __device__ __forceinline__ void kb_load_taps_d(double* __restrict__ cpad, const 
       const int j = j0 + u * 32 * kNW + tid;
       if (j < n2) {
         const int i = j / nw, k = 2 * (j - i * nw);
-        cpad[i * cstride + guard + k] = v[u].x;
-        cpad[i * cstride + guard + k + 1] = v[u].y;
+        if (k < Kw) cpad[i * cstride + guard + k] = v[u].x;
+        if (k + 1 < Kw) cpad[i * cstride + guard + k + 1] = v[u].y;
       }
     }
   }
-  const int ng = cstride - Wp;  // guard entries per row
+  const int ng = cstride - Kw;  // guard entries per row
   for (int idx = tid; idx < r * ng; idx += 32 * kNW) {
     const int i = idx / ng, k = idx - i * ng;
-    cpad[i * cstride + (k < guard ? k : Wp + k)] = 0.0;
+    cpad[i * cstride + (k < guard ? k : Kw + k)] = 0.0;
   }
 }
 
@@ -325,7 +325,7 @@ __device__ __forceinline__ void kb_split_group_dmma(const double* __restrict__ x
   for (int gg = 0; gg < G; ++gg)
 #pragma unroll
     for (int j = 0; j < 4; ++j) D[gg][j][0] = D[gg][j][1] = 0.0;
-  const int nch = (g.dbg & 1) ? 0 : dmma_chunks(g.Wp);
+  const int nch = (g.dbg & 1) ? 0 : dmma_chunks(g.Kw);
   const double* cbl = cb + kCG + ac - ar;
   const double* xb = xs + (s_off + ac) * kXS + ar;
 #pragma unroll 2
@@ -374,9 +374,9 @@ kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict_
   kb_stamp(g, 0, 0);
   __shared__ unsigned long long full[kStages], empty[kStages];
   constexpr int TS = kNW * 8;
-  const int rows_tile = dmma_rows(TS, g.Wp);
+  const int rows_tile = dmma_rows(TS, g.Kw);
   const TileBoxes tb = tile_boxes(rows_tile);
-  const int cstride = dmma_cstride_split(g.Wp);
+  const int cstride = dmma_cstride_split(g.Kw);
   double* xs = reinterpret_cast<double*>(kb_smem_d);  // [kStages][stage_elems]
   double* cpad = xs + kStages * tb.stage_elems;        // [r][cstride], taps at offset kCG
   const int lane = threadIdx.x, warp = threadIdx.y;
@@ -419,7 +419,7 @@ kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict_
   // the first image's taps do not depend on the previous kernel: load them, then wait for it
   // (programmatic dependent launch) and start the tile ring
   pdl_launch_dependents();
-  kb_load_taps_d(cpad, tin + use_walk.b * t_bs, r, g.Wp, cstride, kCG, tid);
+  kb_load_taps_d(cpad, tin + use_walk.b * t_bs, r, g.Wp, g.Kw, cstride, kCG, tid);
   __syncthreads();
   int taps_b = use_walk.b;
   kb_stamp(g, 0, 2);
@@ -429,7 +429,7 @@ kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict_
   for (int t = 0; use_walk.next(ch, TS); ++t) {
     if (ch.b != taps_b) {  // per-image taps (uniform across the block: block-level reload)
       __syncthreads();
-      kb_load_taps_d(cpad, tin + ch.b * t_bs, r, g.Wp, cstride, kCG, tid);
+      kb_load_taps_d(cpad, tin + ch.b * t_bs, r, g.Wp, g.Kw, cstride, kCG, tid);
       __syncthreads();
       taps_b = ch.b;
     }
@@ -656,9 +656,9 @@ kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* 
   kb_stamp(g, 1, 0);
   __shared__ unsigned long long full[kStages], empty[kStages];
   constexpr int TS = kNW * 16;
-  const int rows_tile = dmma_rows(TS, g.Wp);
+  const int rows_tile = dmma_rows(TS, g.Kw);
   const TileBoxes tb = tile_boxes(rows_tile);
-  const int cstride = dmma_cstride_sum(g.Wp);  // taps at offset kCG + 8 (S-tile 1 reads t0 - 8)
+  const int cstride = dmma_cstride_sum(g.Kw);  // taps at offset kCG + 8 (S-tile 1 reads t0 - 8)
   double* xs = reinterpret_cast<double*>(kb_smem_d);  // [kStages][stage_elems]
   double* cpad = xs + kStages * tb.stage_elems;        // [r][cstride]
   const int lane = threadIdx.x, warp = threadIdx.y;
@@ -666,7 +666,7 @@ kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* 
   const int LT = (g.other + 31) / 32;
   const int ar = lane >> 2, ac = lane & 3;
   const int s_off = warp * 16;
-  const int nch = dmma_chunks(g.Wp);
+  const int nch = dmma_chunks(g.Kw);
   const int nslots = gridDim.x * kNW, slot = blockIdx.x * kNW + warp;
 
   if (tid == 0) {
@@ -711,7 +711,7 @@ kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* 
     ++nfill;
   };
   pdl_launch_dependents();
-  kb_load_taps_d(cpad, tin + use_walk.b * t_bs, r, g.Wp, cstride, kCG + 8, tid);
+  kb_load_taps_d(cpad, tin + use_walk.b * t_bs, r, g.Wp, g.Kw, cstride, kCG + 8, tid);
   __syncthreads();
   int taps_b = use_walk.b;
   kb_stamp(g, 1, 2);
@@ -727,7 +727,7 @@ kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* 
   while (use_walk.next(ch, TS)) {
     if (ch.b != taps_b) {  // per-image taps (uniform across the block)
       __syncthreads();
-      kb_load_taps_d(cpad, tin + ch.b * t_bs, r, g.Wp, cstride, kCG + 8, tid);
+      kb_load_taps_d(cpad, tin + ch.b * t_bs, r, g.Wp, g.Kw, cstride, kCG + 8, tid);
       __syncthreads();
       taps_b = ch.b;
     }

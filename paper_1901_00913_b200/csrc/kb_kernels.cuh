@@ -47,7 +47,8 @@ struct AxisGeom {
   int len;      // local extent along S (rows of the input plane, columns of the output plane)
   int other;    // extent along L (columns of the input plane, rows of the output plane)
   int H;        // half width of the (symmetric, zero padded) tap window
-  int Wp;       // padded tap count (multiple of kUB, >= 2H+1)
+  int Wp;       // padded tap count (multiple of kUB, >= 2H+1): row stride of the tap tables
+  int Kw;       // taps the tensor-core passes cover: 2H+1 rounded up to a multiple of 4
   int fill;     // 1 = reflect-fill out-of-domain tile entries (forward, reflective kind)
   int g0;       // global index of local 0
   int Mg;       // global extent of the domain

@@ -103,10 +103,10 @@ __device__ __forceinline__ void kb_flip_tile_x(float* __restrict__ xs, int rows,
   }
 }
 
-// per-image tap tables [r][Wp] -> shared memory as zero-guarded tf32 hi / lo copies; 16-byte
-// loads, all issued before any store (one memory round trip at kernel start)
+// per-image tap tables [r][Wp] -> shared memory as zero-guarded tf32 hi / lo copies of the first
+// Kw taps of each row; 16-byte loads, all issued before any store (one memory round trip)
 __device__ __forceinline__ void kb_load_taps_x(unsigned* __restrict__ chi, unsigned* __restrict__ clo,
-                                               const float* __restrict__ tb, int r, int Wp, int cstride,
+                                               const float* __restrict__ tb, int r, int Wp, int Kw, int cstride,
                                                int guard, int tid) {
   const int n4 = r * Wp / 4, nw = Wp / 4;
   constexpr int kV = 4;
@@ -121,10 +121,11 @@ __device__ __forceinline__ void kb_load_taps_x(unsigned* __restrict__ chi, unsig
     for (int u = 0; u < kV; ++u) {
       const int j = j0 + u * 32 * kNW + tid;
       if (j < n4) {
-        const int i = j / nw, o = i * cstride + guard + 4 * (j - i * nw);
+        const int i = j / nw, k0 = 4 * (j - i * nw), o = i * cstride + guard + k0;
         const float c[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
+          if (k0 + e >= Kw) break;
           unsigned h, l;
           tf32_split_rn(c[e], h, l);
           chi[o + e] = h;
@@ -133,10 +134,10 @@ __device__ __forceinline__ void kb_load_taps_x(unsigned* __restrict__ chi, unsig
       }
     }
   }
-  const int ng = cstride - Wp;
+  const int ng = cstride - Kw;
   for (int idx = tid; idx < r * ng; idx += 32 * kNW) {
     const int i = idx / ng, k = idx - i * ng;
-    const int o = i * cstride + (k < guard ? k : Wp + k);
+    const int o = i * cstride + (k < guard ? k : Kw + k);
     chi[o] = 0u;
     clo[o] = 0u;
   }
@@ -177,7 +178,7 @@ __device__ __forceinline__ void kb_split_group_x(const float* __restrict__ xs, c
     for (int m = 0; m < 2; ++m)
 #pragma unroll
       for (int i = 0; i < 4; ++i) D[gg][m][i] = 0.f;
-  const int nk = (g.dbg & 1) ? 0 : tf32_ksteps(g.Wp);
+  const int nk = (g.dbg & 1) ? 0 : tf32_ksteps(g.Kw);
   const float* xb = xs + (s_off + q) * kXF + gq;
   const int boff = kTG + q - gq;  // b0 = c[8c + q - g], b1 = c[8c + q + 4 - g]
 #pragma unroll 2
@@ -258,9 +259,9 @@ kb_pass_split_x(const __grid_constant__ CUtensorMap tmap, float* __restrict__ z,
   kb_stamp(g, 0, 0);
   __shared__ unsigned long long full[kMaxStages], empty[kMaxStages];
   constexpr int TS = kNW * 8;
-  const int rows_tile = tf32_rows(TS, g.Wp);
+  const int rows_tile = tf32_rows(TS, g.Kw);
   const TileBoxesX tb = tile_boxes_x(rows_tile);
-  const int cstride = tf32_cstride(g.Wp);
+  const int cstride = tf32_cstride(g.Kw);
   float* xs = reinterpret_cast<float*>(kb_smem_x);                       // [nst][stage_elems]
   unsigned* chi = reinterpret_cast<unsigned*>(xs + nst * tb.stage_elems);  // [r][cstride]
   unsigned* clo = chi + r * cstride;
@@ -299,7 +300,7 @@ kb_pass_split_x(const __grid_constant__ CUtensorMap tmap, float* __restrict__ z,
     ++nfill;
   };
   pdl_launch_dependents();  // taps first, then wait for the previous kernel (see kb_dmma.cuh)
-  kb_load_taps_x(chi, clo, tin + use_walk.b * t_bs, r, g.Wp, cstride, kTG, tid);
+  kb_load_taps_x(chi, clo, tin + use_walk.b * t_bs, r, g.Wp, g.Kw, cstride, kTG, tid);
   __syncthreads();
   int taps_b = use_walk.b;
   kb_stamp(g, 0, 2);
@@ -309,7 +310,7 @@ kb_pass_split_x(const __grid_constant__ CUtensorMap tmap, float* __restrict__ z,
   for (int t = 0; use_walk.next(ch, TS); ++t) {
     if (ch.b != taps_b) {
       __syncthreads();
-      kb_load_taps_x(chi, clo, tin + ch.b * t_bs, r, g.Wp, cstride, kTG, tid);
+      kb_load_taps_x(chi, clo, tin + ch.b * t_bs, r, g.Wp, g.Kw, cstride, kTG, tid);
       __syncthreads();
       taps_b = ch.b;
     }
@@ -527,9 +528,9 @@ kb_pass_sum_x(const __grid_constant__ CUtensorMap tmap, int r, const float* __re
   kb_stamp(g, 1, 0);
   __shared__ unsigned long long full[kMaxStages], empty[kMaxStages];
   constexpr int TS = kNW * 16;
-  const int rows_tile = tf32_rows(TS, g.Wp);
+  const int rows_tile = tf32_rows(TS, g.Kw);
   const TileBoxesX tb = tile_boxes_x(rows_tile);
-  const int cstride = tf32_cstride(g.Wp);
+  const int cstride = tf32_cstride(g.Kw);
   float* xs = reinterpret_cast<float*>(kb_smem_x);
   unsigned* chi = reinterpret_cast<unsigned*>(xs + nst * tb.stage_elems);  // [r][cstride]
   unsigned* clo = chi + r * cstride;
@@ -538,7 +539,7 @@ kb_pass_sum_x(const __grid_constant__ CUtensorMap tmap, int r, const float* __re
   const int LT = (g.other + 31) / 32;
   const int gq = lane >> 2, q = lane & 3;
   const int s_off = warp * 16;
-  const int nk = tf32_ksteps(g.Wp);
+  const int nk = tf32_ksteps(g.Kw);
   const int nslots = gridDim.x * kNW, slot = blockIdx.x * kNW + warp;
 
   if (tid == 0) {
@@ -582,7 +583,7 @@ kb_pass_sum_x(const __grid_constant__ CUtensorMap tmap, int r, const float* __re
     ++nfill;
   };
   pdl_launch_dependents();
-  kb_load_taps_x(chi, clo, tin + use_walk.b * t_bs, r, g.Wp, cstride, kTG + 8, tid);
+  kb_load_taps_x(chi, clo, tin + use_walk.b * t_bs, r, g.Wp, g.Kw, cstride, kTG + 8, tid);
   __syncthreads();
   int taps_b = use_walk.b;
   kb_stamp(g, 1, 2);
@@ -598,7 +599,7 @@ kb_pass_sum_x(const __grid_constant__ CUtensorMap tmap, int r, const float* __re
   while (use_walk.next(ch, TS)) {
     if (ch.b != taps_b) {
       __syncthreads();
-      kb_load_taps_x(chi, clo, tin + ch.b * t_bs, r, g.Wp, cstride, kTG + 8, tid);
+      kb_load_taps_x(chi, clo, tin + ch.b * t_bs, r, g.Wp, g.Kw, cstride, kTG + 8, tid);
       __syncthreads();
       taps_b = ch.b;
     }

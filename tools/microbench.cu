@@ -180,6 +180,24 @@ __global__ void bf16_k(float* out, int iters) {
   if (s == -1.2345f) out[0] = s;
 }
 
+// DMMA with NACC independent accumulators per warp, operands in registers only
+template <int NACC>
+__global__ void dmma_ilp_k(double* out, int iters) {
+  double a[4], b[4];
+  for (int i = 0; i < 4; ++i) { a[i] = threadIdx.x * 1e-3 + i; b[i] = threadIdx.x * 2e-3 - i; }
+  double c[NACC][2];
+  for (int i = 0; i < NACC; ++i) c[i][0] = c[i][1] = 0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < NACC; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a[i & 3]), "d"(b[(i >> 2) & 3]));
+  }
+  double s = 0;
+  for (int i = 0; i < NACC; ++i) s += c[i][0] + c[i][1];
+  if (s == -1.2345) out[0] = s;
+}
+
 template <typename K, typename... A>
 float timeit(K k, int blocks, int threads, A... a) {
   cudaEvent_t e0, e1;
@@ -219,6 +237,15 @@ int main() {
     printf("DMMAs tpb=%d  %.2f TFLOP/s\n", tpb, 2.0 * 256 * 16 * (it / 16) * (double)blocks * (tpb / 32) / ms / 1e9);
     ms = timeit(dfma3_k, blocks, tpb, dout, it, 0.999);
     printf("DFMA3 tpb=%d  %.2f TFLOP/s\n", tpb, 2.0 * 8 * it * (double)blocks * tpb / ms / 1e9);
+  }
+  for (int wps : {4, 8, 16, 32}) {  // warps per SM (one block per SM)
+    const int it = 512;
+    float ms = timeit(dmma_ilp_k<8>, sms, 32 * wps, dout, it);
+    printf("DMMA ilp8  %2d warps/SM  %.1f TFLOP/s\n", wps, 2.0 * 256 * 8 * it * (double)sms * wps / ms / 1e9);
+    ms = timeit(dmma_ilp_k<16>, sms, 32 * wps, dout, it);
+    printf("DMMA ilp16 %2d warps/SM  %.1f TFLOP/s\n", wps, 2.0 * 256 * 16 * it * (double)sms * wps / ms / 1e9);
+    ms = timeit(dmma_ilp_k<32>, sms, 32 * wps, dout, it / 2);
+    printf("DMMA ilp32 %2d warps/SM  %.1f TFLOP/s\n", wps, 2.0 * 256 * 32 * (it / 2) * (double)sms * wps / ms / 1e9);
   }
   for (int tpb : {128, 256, 512}) {
     const int blocks = sms * 4, it = 2048;
