@@ -112,7 +112,8 @@ int kb_block_update(const kb_op* op, const void* Rh, void* X, void* Y, void* wor
 /*
  * Measurement helpers used by bench.py (no reference counterpart).
  * kb_fma_peak: measured throughput (TFLOP/s) of the arithmetic instruction the pass kernels issue
- * for dtype - FP64 tensor-core DMMA (m8n8k4) for KB_F64, FFMA for KB_F32 (roofline denominator).
+ * for dtype - FP64 tensor-core DMMA (m8n8k4) for KB_F64, TF32 tensor-core mma.sync (m16n8k8)
+ * for KB_F32, whose 3xTF32 passes issue three per product (roofline denominator).
  * kb_time_passes: average device time (ms, CUDA events on `stream`) of each of the four kernels of
  * one sFISTA iteration, `reps` back-to-back launches each: ms4 = {forward pass A, forward pass B
  * (residual epilogue), adjoint pass A, adjoint pass B (update epilogue, beta = 0)}. X/Yio are

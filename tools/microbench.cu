@@ -198,6 +198,33 @@ __global__ void dmma_ilp_k(double* out, int iters) {
   if (s == -1.2345) out[0] = s;
 }
 
+// half the warps DMMA, half DFMA: do the two FP64 paths share one pipe?
+__global__ void mixed_k(double* out, int iters) {
+  const int warp = threadIdx.x >> 5;
+  double s = 0;
+  if (warp & 1) {
+    double a = threadIdx.x * 1e-3, b = threadIdx.x * 2e-3;
+    double c[8][2];
+    for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+    }
+    for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  } else {
+    double x[8];
+    for (int i = 0; i < 8; ++i) x[i] = threadIdx.x + i;
+    // 64 DFMA per thread per DMMA-iteration keeps the flop count per warp equal (8 DMMA = 2048 FMA)
+    for (int it = 0; it < iters * 8; ++it)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = fma(x[i], 0.999999, 1e-7);
+    for (int i = 0; i < 8; ++i) s += x[i];
+  }
+  if (s == -1.2345) out[0] = s;
+}
+
 template <typename K, typename... A>
 float timeit(K k, int blocks, int threads, A... a) {
   cudaEvent_t e0, e1;
@@ -237,6 +264,15 @@ int main() {
     printf("DMMAs tpb=%d  %.2f TFLOP/s\n", tpb, 2.0 * 256 * 16 * (it / 16) * (double)blocks * (tpb / 32) / ms / 1e9);
     ms = timeit(dfma3_k, blocks, tpb, dout, it, 0.999);
     printf("DFMA3 tpb=%d  %.2f TFLOP/s\n", tpb, 2.0 * 8 * it * (double)blocks * tpb / ms / 1e9);
+  }
+  {
+    const int it = 256;
+    // per warp pair: DMMA warp 8*it DMMAs (8*256*it FMA... 2048*it flop*?), DFMA warp 32*64*it FMA
+    float ms = timeit(mixed_k, sms * 2, 512, dout, it);
+    const double fl_dmma = 2.0 * 256 * 8 * it * (double)sms * 2 * 8;      // 8 DMMA warps per block
+    const double fl_dfma = 2.0 * 32 * 8 * 8 * it * (double)sms * 2 * 8;   // 8 DFMA warps per block
+    printf("MIXED DMMA+DFMA  %.1f TFLOP/s total (dmma share %.1f, dfma share %.1f)\n", (fl_dmma + fl_dfma) / ms / 1e9,
+           fl_dmma / ms / 1e9, fl_dfma / ms / 1e9);
   }
   for (int wps : {4, 8, 16, 32}) {  // warps per SM (one block per SM)
     const int it = 512;
