@@ -484,108 +484,136 @@ kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict_
 }
 
 // ------------------------------------------------------------------------------------------
-// Fused epilogue straight from the sum pass accumulators: lane (ar, ac) holds, for S-tile mt
-// and M-tile j, Y[p = l0 + 8j + ar][q = s0 + s_off + 8mt + 2ac + {0,1}] (p: m index, q: n
-// index), so every operand load and result store is a 16-byte pair. Operand loads of an S-tile
-// are issued before any of its arithmetic.
+// Fused epilogue straight from the sum pass accumulators: lane (ar, ac) holds, for an S-tile at
+// row offset so and M-tile j, Y[p = l0 + 8j + ar][q = s0 + so + 2ac + {0,1}] (p: m index, q: n
+// index), so every operand load and result store is a 16-byte pair. kb_epi_load issues an
+// S-tile's operand loads (they can be in flight during MMAs), kb_epi_apply does the arithmetic
+// and the stores.
 // ------------------------------------------------------------------------------------------
+struct EpiScalars {
+  double Lb = 0.0, db = 1.0, rd = 1.0, vs = 1.0;
+};
+template <int MODE>
+__device__ __forceinline__ EpiScalars kb_epi_scalars(const Epi<double>& e, int b) {
+  EpiScalars c;  // per-image scalars, loaded once (result stores may alias them for the compiler)
+  if constexpr (MODE == EPI_UPDATE) {
+    c.Lb = e.L[b];
+    c.db = e.denom[b];
+    c.rd = 1.0 / c.db;  // correctly rounded reciprocal: quotients via Markstein's correction
+  }
+  if constexpr (MODE == EPI_POWER) c.vs = e.vnw2 ? sqrt(e.vnw2[b]) : 1.0;
+  return c;
+}
+
+template <int MODE>
+__device__ __forceinline__ void kb_epi_load(const AxisGeom& g, const Epi<double>& e, const Chunk& ch, int so,
+                                            int ar, int ac, double (&u)[4][2], double (&w)[4][2]) {
+  const int sl = so + 2 * ac;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) u[j][0] = u[j][1] = w[j][0] = w[j][1] = 0.0;
+  if constexpr (MODE == EPI_PLAIN) return;
+  if (sl >= ch.cnt) return;
+  const bool both = sl + 1 < ch.cnt;
+  const long long rowbase = (long long)ch.b * e.bstride + ch.s0 + sl;
+  auto ld2 = [&](const double* a, long long at, double (&v)[2]) {
+    if (both) {
+      const double2 t = *reinterpret_cast<const double2*>(a + at);
+      v[0] = t.x;
+      v[1] = t.y;
+    } else {
+      v[0] = a[at];
+    }
+  };
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int p = ch.lt * 32 + 8 * j + ar;
+    if (p >= g.other) continue;
+    const long long at = rowbase + (long long)p * g.len;
+    if constexpr (MODE == EPI_RESID) ld2(e.bsub, at, u[j]);
+    if constexpr (MODE == EPI_UPDATE) {
+      ld2(e.y, at, u[j]);
+      ld2(e.x, at, w[j]);
+    }
+    if constexpr (MODE == EPI_POWER) ld2(e.vin, at, u[j]);
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ void kb_epi_apply(const double (&D)[4][2], const AxisGeom& g, const Epi<double>& e,
+                                             const EpiScalars& sc, const Chunk& ch, int so, int ar, int ac,
+                                             const double (&u)[4][2], const double (&w)[4][2], double (&nrm)[3],
+                                             bool& bad) {
+  const int n = g.len;
+  const int sl = so + 2 * ac;  // first of the lane's two S rows in the chunk
+  if (sl >= ch.cnt) return;
+  const bool both = sl + 1 < ch.cnt;
+  const int q = ch.s0 + sl;
+  const long long rowbase = (long long)ch.b * e.bstride + q;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int p = ch.lt * 32 + 8 * j + ar;
+    if (p >= g.other) continue;
+    const long long at = rowbase + (long long)p * n;
+    double val[2] = {D[j][0], D[j][1]};
+    if (e.foldH > 0) {
+      const int FH = e.foldH;
+      const double* f = e.fold + ((long long)ch.b * g.other + p) * (2 * FH);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int qi = q + i;
+        if (qi < FH) val[i] += f[qi];
+        else if (qi >= n - FH && qi < n) val[i] += f[qi - (n - 2 * FH)];
+      }
+    }
+    if constexpr (MODE == EPI_PLAIN) {
+      st_pair(e.out + at, val[0], val[1], both);
+    } else if constexpr (MODE == EPI_RESID) {
+      st_pair(e.out + at, __dsub_rn(val[0], u[j][0]), __dsub_rn(val[1], u[j][1]), both);
+    } else if constexpr (MODE == EPI_UPDATE) {
+      double xv[2], yv[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        xv[i] = kb_quot(__dsub_rn(__dmul_rn(sc.Lb, u[j][i]), val[i]), sc.db, sc.rd);
+        if (e.project) xv[i] = (xv[i] > 0.0 || xv[i] != xv[i]) ? xv[i] : 0.0;
+        const double d = __dsub_rn(xv[i], w[j][i]);
+        yv[i] = __dadd_rn(xv[i], __dmul_rn(e.beta, d));
+        if (i == 0 || both) {
+          bad |= !isfinite(xv[i]);
+          if (e.want_norms) {
+            nrm[0] += d * d;
+            nrm[1] += w[j][i] * w[j][i];
+            nrm[2] += xv[i] * xv[i];
+          }
+        }
+      }
+      st_pair(e.x + at, xv[0], xv[1], both);
+      st_pair(e.y + at, yv[0], yv[1], both);
+    } else {  // EPI_POWER
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        if (i == 0 || both) {
+          const double vv = e.vnw2 ? u[j][i] / sc.vs : u[j][i];
+          nrm[0] += vv * val[i];
+          nrm[1] += val[i] * val[i];
+        }
+      }
+      st_pair(e.out + at, val[0], val[1], both);
+    }
+  }
+}
+
+// two S-tiles (the 16-row warps of kb_pass_sum_dmma): loads of a tile before its arithmetic
 template <int MODE>
 __device__ __forceinline__ void kb_sum_epilogue_regs(const double (&D)[2][4][2], const AxisGeom& g,
                                                      const Epi<double>& e, const Chunk& ch,
                                                      int s_off, int ar, int ac, double (&nrm)[3],
                                                      bool& bad) {
-  const int n = g.len;
-  // per-image scalars, loaded once (the result stores below may alias them for the compiler)
-  double Lb = 0.0, db = 1.0, rd = 1.0, vs = 1.0;
-  if constexpr (MODE == EPI_UPDATE) {
-    Lb = e.L[ch.b];
-    db = e.denom[ch.b];
-    rd = 1.0 / db;  // correctly rounded reciprocal: quotients below via Markstein's correction
-  }
-  if constexpr (MODE == EPI_POWER) vs = e.vnw2 ? sqrt(e.vnw2[ch.b]) : 1.0;
+  const EpiScalars sc = kb_epi_scalars<MODE>(e, ch.b);
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) {
-    const int sl = s_off + 8 * mt + 2 * ac;  // first of the lane's two S rows in the chunk
-    if (sl >= ch.cnt) continue;
-    const bool both = sl + 1 < ch.cnt;
-    const int q = ch.s0 + sl;
-    const long long rowbase = (long long)ch.b * e.bstride + q;
     double u[4][2], w[4][2];
-    auto ld2 = [&](const double* a, long long at, double (&v)[2]) {
-      if (both) {
-        const double2 t = *reinterpret_cast<const double2*>(a + at);
-        v[0] = t.x;
-        v[1] = t.y;
-      } else {
-        v[0] = a[at];
-        v[1] = 0.0;
-      }
-    };
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int p = ch.lt * 32 + 8 * j + ar;
-      const long long at = rowbase + (long long)p * n;
-      u[j][0] = u[j][1] = w[j][0] = w[j][1] = 0.0;
-      if (p < g.other) {
-        if constexpr (MODE == EPI_RESID) ld2(e.bsub, at, u[j]);
-        if constexpr (MODE == EPI_UPDATE) {
-          ld2(e.y, at, u[j]);
-          ld2(e.x, at, w[j]);
-        }
-        if constexpr (MODE == EPI_POWER) ld2(e.vin, at, u[j]);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int p = ch.lt * 32 + 8 * j + ar;
-      if (p >= g.other) continue;
-      const long long at = rowbase + (long long)p * n;
-      double val[2] = {D[mt][j][0], D[mt][j][1]};
-      if (e.foldH > 0) {
-        const int FH = e.foldH;
-        const double* f = e.fold + ((long long)ch.b * g.other + p) * (2 * FH);
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int qi = q + i;
-          if (qi < FH) val[i] += f[qi];
-          else if (qi >= n - FH && qi < n) val[i] += f[qi - (n - 2 * FH)];
-        }
-      }
-      if constexpr (MODE == EPI_PLAIN) {
-        st_pair(e.out + at, val[0], val[1], both);
-      } else if constexpr (MODE == EPI_RESID) {
-        st_pair(e.out + at, __dsub_rn(val[0], u[j][0]), __dsub_rn(val[1], u[j][1]), both);
-      } else if constexpr (MODE == EPI_UPDATE) {
-        double xv[2], yv[2];
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          xv[i] = kb_quot(__dsub_rn(__dmul_rn(Lb, u[j][i]), val[i]), db, rd);
-          if (e.project) xv[i] = (xv[i] > 0.0 || xv[i] != xv[i]) ? xv[i] : 0.0;
-          const double d = __dsub_rn(xv[i], w[j][i]);
-          yv[i] = __dadd_rn(xv[i], __dmul_rn(e.beta, d));
-          if (i == 0 || both) {
-            bad |= !isfinite(xv[i]);
-            if (e.want_norms) {
-              nrm[0] += d * d;
-              nrm[1] += w[j][i] * w[j][i];
-              nrm[2] += xv[i] * xv[i];
-            }
-          }
-        }
-        st_pair(e.x + at, xv[0], xv[1], both);
-        st_pair(e.y + at, yv[0], yv[1], both);
-      } else {  // EPI_POWER
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          if (i == 0 || both) {
-            const double vv = e.vnw2 ? u[j][i] / vs : u[j][i];
-            nrm[0] += vv * val[i];
-            nrm[1] += val[i] * val[i];
-          }
-        }
-        st_pair(e.out + at, val[0], val[1], both);
-      }
-    }
+    kb_epi_load<MODE>(g, e, ch, s_off + 8 * mt, ar, ac, u, w);
+    kb_epi_apply<MODE>(D[mt], g, e, sc, ch, s_off + 8 * mt, ar, ac, u, w, nrm, bad);
   }
 }
 
