@@ -47,7 +47,7 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 constexpr int kMaxHalf = 1024;
-constexpr int kGmaxF64 = 3;  // pass A term group (register budget: G*R accumulators)
+constexpr int kGmaxF64 = 2;  // pass A term group (register budget: G*R accumulators)
 constexpr int kGmaxF32 = 4;
 constexpr double kSymTol = 1e-11;  // (anti)symmetry residual allowed for sign-reflected fills
 constexpr int kRA = 8;   // pass A rows per warp
@@ -252,6 +252,14 @@ int ring_stages(size_t stage_bytes, size_t fixed_bytes, int bps) {
   return n;
 }
 
+int split_ns() {
+  static const int ns = [] {
+    const char* v = std::getenv("KB_SPLIT_NS");
+    return (v && v[0] == '1') ? 1 : 2;
+  }();
+  return ns;
+}
+
 // Launch a persistent pass kernel (one block of 32 x kNW threads per work slot) with
 // programmatic stream serialization: in a stream or captured graph it may start while the
 // previous kernel drains; it loads its taps, then waits in griddepcontrol.wait for that
@@ -324,14 +332,17 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
     if (mirror_h == 0) eparts = parts;
   };
   if constexpr (sizeof(T) == 8) {
-    const kb::TileBoxes tb = kb::tile_boxes(kb::dmma_rows(kb::kNW * 8, g.Kw));
+    // NS = 2: 16-row warps whose two S-tiles share the A fragments (KB_SPLIT_NS=1: 8-row warps)
+    const int ns = split_ns();
+    const kb::TileBoxes tb = kb::tile_boxes(kb::dmma_rows(kb::kNW * 8 * ns, g.Kw));
     const size_t smem = sizeof(double) * ((size_t)kb::kStages * tb.stage_elems +
-                                          (size_t)op->r * kb::dmma_cstride_split(g.Kw));
+                                          (size_t)op->r * (ns == 2 ? kb::dmma_cstride_sum(g.Kw)
+                                                                   : kb::dmma_cstride_split(g.Kw)));
     const int bps = blocks_per_sm(smem);
     CUtensorMap map;
     if (use_dmma(op) && bps > 0 &&
         make_tmap(&map, in_map, g.other, in_rows, op->batch, g.other, in_bs, tb.box_rows)) {
-      auto kern = kb::kb_pass_split_dmma<kGmaxF64>;
+      auto kern = ns == 2 ? kb::kb_pass_split_dmma<kGmaxF64, 2> : kb::kb_pass_split_dmma<kGmaxF64, 1>;
       KB_TRY(allow_smem(kern, smem));
       int parts, nb, eparts;
       plan(bps, parts, nb, eparts);

@@ -311,7 +311,40 @@ __device__ __forceinline__ void st_pair(double* p, double a, double b, bool both
 // M-tiles) for the G terms of a group: 4G accumulator tiles. Lane (ar, ac) of M-tile j ends
 // with Z^T[l0 + 8j + ar][s0 + 8w + 2ac + {0,1}]: one 16-byte store per term and M-tile.
 // ------------------------------------------------------------------------------------------
-template <int G>
+// MMA loop of one group over K-chunks [c0, c1): S-tile 0 when T0, S-tile 1 (outputs +8: taps at
+// t0 - 8, sharing the A fragment) when T1
+template <int G, int NS, bool T0, bool T1>
+__device__ __forceinline__ void kb_split_mma(double (&D)[G][NS][4][2], const double* __restrict__ xb,
+                                             const double* __restrict__ cbl, int cstride, int c0, int c1) {
+#pragma unroll 2
+  for (int c = c0; c < c1; ++c) {
+    double A[4], B0[G], B1[G];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) A[j] = xb[4 * c * kXS + 8 * j];
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+      B0[gg] = T0 ? cbl[gg * cstride + 4 * c] : 0.0;
+      B1[gg] = T1 ? cbl[gg * cstride + 4 * c - 8] : 0.0;
+    }
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (T0) dmma_884(D[gg][0][j][0], D[gg][0][j][1], A[j], B0[gg]);
+        if constexpr (NS == 2)
+          if (T1) dmma_884(D[gg][NS - 1][j][0], D[gg][NS - 1][j][1], A[j], B1[gg]);
+      }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// split pass (fp64, DMMA): warp w owns NS S-tiles of 8 rows ([8 NS w, 8 NS (w+1)) of a chunk) x
+// 32 L (four 8-column M-tiles) for the G terms of a group; with NS = 2 the two S-tiles share
+// every A fragment (the sum pass's trick). Lane (ar, ac) of M-tile j ends with
+// Z^T[l0 + 8j + ar][s0 + s_off + 8mt + 2ac + {0,1}]: one 16-byte store per term, S-tile and
+// M-tile (plus the reflected halo rows at an L edge).
+// ------------------------------------------------------------------------------------------
+template <int G, int NS>
 __device__ __forceinline__ void kb_split_group_dmma(const double* __restrict__ xs,
                                                     const double* __restrict__ cb, int cstride,
                                                     const AxisGeom& g, int s_off, int lane,
@@ -320,51 +353,54 @@ __device__ __forceinline__ void kb_split_group_dmma(const double* __restrict__ x
                                                     bool scaled, int mirror_h,
                                                     const double* __restrict__ msign) {
   const int ar = lane >> 2, ac = lane & 3;
-  double D[G][4][2];
+  double D[G][NS][4][2];
 #pragma unroll
   for (int gg = 0; gg < G; ++gg)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) D[gg][j][0] = D[gg][j][1] = 0.0;
+    for (int mt = 0; mt < NS; ++mt)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) D[gg][mt][j][0] = D[gg][mt][j][1] = 0.0;
   const int nch = (g.dbg & 1) ? 0 : dmma_chunks(g.Kw);
-  const double* cbl = cb + kCG + ac - ar;
+  const double* cbl = cb + (NS == 2 ? kCG + 8 : kCG) + ac - ar;
   const double* xb = xs + (s_off + ac) * kXS + ar;
-#pragma unroll 2
-  for (int c = 0; c < nch; ++c) {
-    double A[4], B[G];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) A[j] = xb[4 * c * kXS + 8 * j];
-#pragma unroll
-    for (int gg = 0; gg < G; ++gg) B[gg] = cbl[gg * cstride + 4 * c];
-#pragma unroll
-    for (int gg = 0; gg < G; ++gg)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dmma_884(D[gg][j][0], D[gg][j][1], A[j], B[gg]);
+  if constexpr (NS == 1) {
+    kb_split_mma<G, NS, true, false>(D, xb, cbl, cstride, 0, nch);
+  } else if (s_off + 8 < ch.cnt) {
+    kb_split_mma<G, NS, true, false>(D, xb, cbl, cstride, 0, 2);
+    kb_split_mma<G, NS, true, true>(D, xb, cbl, cstride, 2, nch);
+    kb_split_mma<G, NS, false, true>(D, xb, cbl, cstride, nch, nch + 2);
+  } else {
+    kb_split_mma<G, NS, true, false>(D, xb, cbl, cstride, 0, nch);
   }
-  const int s = s_off + 2 * ac;
-  if (s >= ch.cnt || (g.dbg & 2)) return;
-  const bool both = s + 1 < ch.cnt;
+  if (g.dbg & 2) return;
   const int l0 = ch.lt * 32 + ar;
 #pragma unroll
-  for (int gg = 0; gg < G; ++gg) {
-    double* zp = z + (long long)(gstart + gg) * z_ps + ch.s0 + s;
-    const double sg = msign ? msign[gstart + gg] : 1.0;
+  for (int mt = 0; mt < NS; ++mt) {
+    const int s = s_off + 8 * mt + 2 * ac;
+    if (s >= ch.cnt) continue;
+    const bool both = s + 1 < ch.cnt;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int l = l0 + 8 * j;
-      if (l >= g.other) continue;
-      const double v0 = scaled ? D[gg][j][0] * oscale : D[gg][j][0];
-      const double v1 = scaled ? D[gg][j][1] * oscale : D[gg][j][1];
-      st_pair(zp + (long long)l * g.len, v0, v1, both);
-      if (mirror_h > 0 && !(g.dbg & 32)) {  // reflected halo rows of Z^T for the reflect-filled sum pass
-        if (l < mirror_h) st_pair(zp + (long long)(-1 - l) * g.len, sg * v0, sg * v1, both);
-        if (l >= g.other - mirror_h)
-          st_pair(zp + (long long)(2 * g.other - 1 - l) * g.len, sg * v0, sg * v1, both);
+    for (int gg = 0; gg < G; ++gg) {
+      double* zp = z + (long long)(gstart + gg) * z_ps + ch.s0 + s;
+      const double sg = msign ? msign[gstart + gg] : 1.0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int l = l0 + 8 * j;
+        if (l >= g.other) continue;
+        const double v0 = scaled ? D[gg][mt][j][0] * oscale : D[gg][mt][j][0];
+        const double v1 = scaled ? D[gg][mt][j][1] * oscale : D[gg][mt][j][1];
+        st_pair(zp + (long long)l * g.len, v0, v1, both);
+        if (mirror_h > 0 && !(g.dbg & 32)) {  // reflected halo rows of Z^T for the reflect-filled sum pass
+          if (l < mirror_h) st_pair(zp + (long long)(-1 - l) * g.len, sg * v0, sg * v1, both);
+          if (l >= g.other - mirror_h)
+            st_pair(zp + (long long)(2 * g.other - 1 - l) * g.len, sg * v0, sg * v1, both);
+        }
       }
     }
   }
 }
 
-template <int GMAX>
+template <int GMAX, int NS>
 __global__ void __launch_bounds__(32 * kNW, 2)
 kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict__ z,
                    long long z_ps, long long z_bs, const double* __restrict__ tin, long long t_bs,
@@ -373,16 +409,17 @@ kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict_
   extern __shared__ __align__(128) unsigned char kb_smem_d[];
   kb_stamp(g, 0, 0);
   __shared__ unsigned long long full[kStages], empty[kStages];
-  constexpr int TS = kNW * 8;
+  constexpr int TS = kNW * 8 * NS;
   const int rows_tile = dmma_rows(TS, g.Kw);
   const TileBoxes tb = tile_boxes(rows_tile);
-  const int cstride = dmma_cstride_split(g.Kw);
+  const int cstride = NS == 2 ? dmma_cstride_sum(g.Kw) : dmma_cstride_split(g.Kw);
+  const int tguard = NS == 2 ? kCG + 8 : kCG;         // S-tile 1 reads taps at t0 - 8
   double* xs = reinterpret_cast<double*>(kb_smem_d);  // [kStages][stage_elems]
-  double* cpad = xs + kStages * tb.stage_elems;        // [r][cstride], taps at offset kCG
+  double* cpad = xs + kStages * tb.stage_elems;        // [r][cstride], taps at offset tguard
   const int lane = threadIdx.x, warp = threadIdx.y;
   const int tid = warp * 32 + lane;
   const int LT = (g.other + 31) / 32;
-  const int s_off = warp * 8;
+  const int s_off = warp * 8 * NS;
 
   if (tid == 0) {
     for (int st = 0; st < kStages; ++st) {
@@ -419,7 +456,7 @@ kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict_
   // the first image's taps do not depend on the previous kernel: load them, then wait for it
   // (programmatic dependent launch) and start the tile ring
   pdl_launch_dependents();
-  kb_load_taps_d(cpad, tin + use_walk.b * t_bs, r, g.Wp, g.Kw, cstride, kCG, tid);
+  kb_load_taps_d(cpad, tin + use_walk.b * t_bs, r, g.Wp, g.Kw, cstride, tguard, tid);
   __syncthreads();
   int taps_b = use_walk.b;
   kb_stamp(g, 0, 2);
@@ -429,7 +466,7 @@ kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict_
   for (int t = 0; use_walk.next(ch, TS); ++t) {
     if (ch.b != taps_b) {  // per-image taps (uniform across the block: block-level reload)
       __syncthreads();
-      kb_load_taps_d(cpad, tin + ch.b * t_bs, r, g.Wp, g.Kw, cstride, kCG, tid);
+      kb_load_taps_d(cpad, tin + ch.b * t_bs, r, g.Wp, g.Kw, cstride, tguard, tid);
       __syncthreads();
       taps_b = ch.b;
     }
@@ -461,7 +498,7 @@ kb_pass_split_dmma(const __grid_constant__ CUtensorMap tmap, double* __restrict_
 #define KB_DGROUP(C)                                                                                  \
   case C:                                                                                             \
     if constexpr (C <= GMAX)                                                                          \
-      kb_split_group_dmma<C>(xt, cb, cstride, g, s_off, lane, zb, z_ps, gstart, ch, oscale, nw2 != nullptr, \
+      kb_split_group_dmma<C, NS>(xt, cb, cstride, g, s_off, lane, zb, z_ps, gstart, ch, oscale, nw2 != nullptr, \
                              mirror_h, msign ? msign + (long long)ch.b * r : nullptr);                \
     break;
         switch (grp.count[gi]) {
