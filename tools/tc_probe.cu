@@ -38,7 +38,8 @@ __device__ __forceinline__ unsigned long long make_desc(unsigned addr, unsigned 
   return d;
 }
 
-__global__ void probe(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap kmap, const float* __restrict__ Bg, float* __restrict__ Dg,
+__global__ void probe(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap kmap,
+                      const __grid_constant__ CUtensorMap amap32, const float* __restrict__ Bg, float* __restrict__ Dg,
                       unsigned idesc, int* status, int dbg, const float* __restrict__ Ag, int amode,
                       unsigned getenv_lbo, unsigned getenv_sbo, int bmode) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -115,7 +116,7 @@ __global__ void probe(const __grid_constant__ CUtensorMap amap, const __grid_con
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
                 smem_u32(sa + j * 2048)),
-            "l"(&amap), "r"(32 * j), "r"(0), "r"(smem_u32(&bar_a))
+            "l"(amode == 4 ? &amap32 : &amap), "r"(32 * j), "r"(0), "r"(smem_u32(&bar_a))
             : "memory");
     }
     asm volatile(
@@ -124,7 +125,8 @@ __global__ void probe(const __grid_constant__ CUtensorMap amap, const __grid_con
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     for (int kk = 0; kk < K / 8; ++kk) {
       const unsigned lbo = getenv_lbo, sbo = getenv_sbo;
-      const unsigned long long ad = amode == 3 ? make_desc(smem_u32(sa) + (kk / 4) * 16384 + (kk % 4) * 32, lbo ? lbo : 16, sbo ? sbo : 1024, 2)
+      const unsigned long long ad = amode == 4 ? make_desc(smem_u32(sa) + kk * 1024, lbo ? lbo : 8192, sbo ? sbo : 512, 1)
+                                  : amode == 3 ? make_desc(smem_u32(sa) + (kk / 4) * 16384 + (kk % 4) * 32, lbo ? lbo : 16, sbo ? sbo : 1024, 2)
                                   : amode == 1 ? make_desc(smem_u32(sak) + kk * 4096, 128, 256, 0)
                                   : amode == 2 ? make_desc(smem_u32(sak) + kk * 4096, lbo ? lbo : 4096, sbo ? sbo : 128, 0)
                                                : make_desc(smem_u32(sa) + kk * 1024, lbo ? lbo : 8192, sbo ? sbo : 1024, 2);
@@ -216,6 +218,13 @@ int main() {
       return 1;
     }
   }
+  CUtensorMap amap32;
+  if (enc(&amap32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dA, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS) {
+    printf("amap32 encode failed\n");
+    return 1;
+  }
   unsigned idesc = 0;
   idesc |= 1u << 4;           // D format F32
   idesc |= 2u << 7;           // A TF32
@@ -231,7 +240,7 @@ int main() {
   const unsigned lbo = getenv("LBO") ? atoi(getenv("LBO")) : 0, sbo = getenv("SBO") ? atoi(getenv("SBO")) : 0;
   const int bmode = getenv("BMODE") ? atoi(getenv("BMODE")) : 0;
   if (bmode == 1) idesc |= 1u << 16;  // B MN-major
-  probe<<<1, 128, 81 * 1024>>>(amap, kmap, dB, dD, idesc, dS, dbg, dA, amode, lbo, sbo, bmode);
+  probe<<<1, 128, 81 * 1024>>>(amap, kmap, amap32, dB, dD, idesc, dS, dbg, dA, amode, lbo, sbo, bmode);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   int st = 0;
