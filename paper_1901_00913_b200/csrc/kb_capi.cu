@@ -23,6 +23,7 @@
 #include "kb_dmma.cuh"
 #include "kb_ffma.cuh"
 #include "kb_tf32.cuh"
+#include "kb_tc.cuh"
 
 namespace {
 
@@ -115,7 +116,7 @@ int persistent_blocks() {
 // 32 (128-byte rows). False when TMA's alignment rules rule it out.
 bool make_tmap(CUtensorMap* map, const void* base, long long cols, long long rows, long long planes,
                long long row_stride, long long plane_stride, int box_rows, int esize = 8,
-               int box_cols = 0) {
+               int box_cols = 0, CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_NONE) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   static bool tried = false;
   if (!tried) {
@@ -137,7 +138,7 @@ bool make_tmap(CUtensorMap* map, const void* base, long long cols, long long row
   const cuuint32_t estr[3] = {1, 1, 1};
   return encode(map, esize == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                 const_cast<void*>(base), dims, strides, box, estr,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -146,6 +147,14 @@ bool use_dmma(const kb_op* op) { return op->dtype == KB_F64 && op->m % 2 == 0 &&
 // fp32 runs on the persistent TMA + FFMA kernels when both extents are multiples of 4 (16-byte
 // row strides and vector stores); other shapes take the generic tiled kernels.
 bool use_tma_f32(const kb_op* op) { return op->dtype == KB_F32 && op->m % 4 == 0 && op->n % 4 == 0; }
+// fp32 zero-BC split pass on tcgen05 (kb_tc.cuh): KB_FP32_TC=1 (opt-in while it is validated)
+bool use_tc_split(const kb_op* op, const kb::AxisGeom& g, int mirror_h) {
+  static const bool on = [] {
+    const char* v = std::getenv("KB_FP32_TC");
+    return v && v[0] == '1';
+  }();
+  return on && use_tma_f32(op) && !g.fill && mirror_h == 0;
+}
 // fp32 arithmetic of the persistent kernels: 3xTF32 tensor-core MMA (kb_tf32.cuh, default) or
 // FFMA register windows (kb_ffma.cuh; KB_FP32_PATH=ffma)
 bool use_tf32(const kb_op* op) {
@@ -353,6 +362,45 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
     }
     return launch_a_g<T, kGmaxF64>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
   } else {
+    if (use_tc_split(op, g, mirror_h) && z_bs == (long long)op->r * z_ps) {
+      const int nbr = kb::tc_bricks(g.Kw);
+      // bricks and tap scratch of up to kTcG terms first, then as deep a tile ring as the rest of
+      // shared memory holds (at least 3 stages)
+      const size_t avail = 226 * 1024 - 1024 - kb::kTcStoreBytes;
+      static const int gmax = [] {
+        const char* v = std::getenv("KB_TC_G");
+        return v ? std::max(1, std::min(kb::kTcG, std::atoi(v))) : kb::kTcG;
+      }();
+      int G = std::min(op->r, gmax);
+      while (G > 1 && (size_t)G * nbr * 1024 + kb::tc_tap_bytes(G, g.Kw) + 3 * kb::kTcStageBytes > avail) --G;
+      const size_t fixed = (size_t)G * nbr * 1024 + kb::tc_tap_bytes(G, g.Kw);
+      const int nst = std::min<int>(kb::kTcRingMax, (int)((avail - std::min(fixed, avail)) / kb::kTcStageBytes));
+      const size_t smem = std::max<size_t>(1024 + kb::kTcStoreBytes + (size_t)nst * kb::kTcStageBytes + fixed,
+                                           116 * 1024);  // one CTA per SM
+      CUtensorMap mapt, mapz;
+      if (nst >= 3 &&
+          make_tmap(&mapt, in_map, g.other, in_rows, op->batch, g.other, in_bs, kb::kTcRB, 4, 128) &&
+          make_tmap(&mapz, z, g.len, g.other, (long long)op->batch * op->r, g.len, z_ps, 32, 4, 32,
+                    CU_TENSOR_MAP_SWIZZLE_128B)) {
+        auto kern = kb::kb_pass_split_tc;
+        KB_TRY(allow_smem(kern, smem));
+        int parts, nb;
+        kb::plan_items(g.len, (g.other + 127) / 128, op->batch, sm_count(), parts, nb);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(nb);
+        cfg.blockDim = dim3(kb::kTcThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = use_pdl() ? 1 : 0;
+        KB_CUDA(cudaLaunchKernelEx(&cfg, kern, mapt, mapz, z, z_ps, z_bs, tin, t_bs, g, nw2, op->r, op->batch, parts,
+                                   G, nst));
+        return KB_OK;
+      }
+    }
     if (use_tf32(op)) {
       const kb::TileBoxesX tx = kb::tile_boxes_x(kb::tf32_rows(kb::kNW * 8, g.Kw));
       const size_t fixed = 2 * (size_t)op->r * kb::tf32_cstride(g.Kw) * sizeof(float);

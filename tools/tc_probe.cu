@@ -57,7 +57,7 @@ __global__ void probe(const __grid_constant__ CUtensorMap amap, const __grid_con
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(&tmem_base)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tmem_base)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   // B bricks: brick kk holds B[n][8kk + k]: core (nb, kc) at nb*256 + kc*128, row i at 16 B
@@ -99,10 +99,33 @@ __global__ void probe(const __grid_constant__ CUtensorMap amap, const __grid_con
         "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
+  if (amode == 5 && warp < 4) {  // A[m][k] -> TMEM lane m, column 32 + k
+    const int m = 32 * warp + lane;
+    for (int k0 = 0; k0 < K; k0 += 16) {
+      unsigned v[16];
+      for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(Ag[(k0 + i) * M + m]);
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+              tmem + ((unsigned)(32 * warp) << 16) + 32 + k0),
+          "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+          "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (tid == 0) {
+  if (tid == 0 && amode == 5) {
+    for (int kk = 0; kk < K / 8; ++kk) {
+      const unsigned long long bd = make_desc(smem_u32(sb) + kk * 512, 128, 256, 0);
+      asm volatile(
+          "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem),
+          "r"(tmem + 32 + 8 * kk), "l"(bd), "r"(idesc), "r"(dbg ? 1 : kk));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar_mma))
+                 : "memory");
+  } else if (tid == 0) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar_a)), "r"(32768u) : "memory");
     if (amode == 3) {  // two boxes {32 K, 128 M} of the K-contiguous A^T copy
       for (int j = 0; j < 2; ++j)
@@ -168,7 +191,7 @@ __global__ void probe(const __grid_constant__ CUtensorMap amap, const __grid_con
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
 }
 
 int main() {
@@ -236,7 +259,7 @@ int main() {
   CK(cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 81 * 1024));
   const int dbg = getenv("DBG") ? 1 : 0;
   const int amode = getenv("AMODE") ? atoi(getenv("AMODE")) : 0;
-  if (amode == 1 || amode == 3) idesc &= ~(1u << 15);  // A K-major
+  if (amode == 1 || amode == 3 || amode == 5) idesc &= ~(1u << 15);  // A K-major (TMEM A: no major bit)
   const unsigned lbo = getenv("LBO") ? atoi(getenv("LBO")) : 0, sbo = getenv("SBO") ? atoi(getenv("SBO")) : 0;
   const int bmode = getenv("BMODE") ? atoi(getenv("BMODE")) : 0;
   if (bmode == 1) idesc |= 1u << 16;  // B MN-major
