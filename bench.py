@@ -53,15 +53,16 @@ def dist_env():
     return rank, world, local
 
 
-def committed_traffic(dtype):
-    """DRAM bytes (read + write) of one iteration's four kernels from the committed ncu capture
-    (profiles/traffic_cfg2.json, written by tools/ncu_traffic.py from an `ncu --set full
-    --cache-control none` run of tools/time_kernels.py), or None when absent."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic_cfg2.json")
+def committed_traffic(config, dtype):
+    """Per-kernel DRAM bytes (read + write) of one iteration's four pass kernels from the
+    committed ncu capture of this config (profiles/traffic_<config>.json, written by
+    tools/ncu_traffic.py from an `ncu --set full` run of tools/one_iter.py), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", f"traffic_{config}.json")
     try:
         with open(path) as f:
-            return json.load(f).get(dtype)
-    except (OSError, ValueError):
+            per = json.load(f).get("_per_kernel", {}).get(dtype)
+        return [int(k["dram_bytes"]) for k in per] if per else None
+    except (OSError, ValueError, KeyError, TypeError):
         return None
 
 
@@ -277,28 +278,53 @@ def run_b200(args):
            "h2d_bytes_per_step": (1 if batched else 2) * nimg * m * m * esz,
            "d2h_bytes_per_step": nimg * m * m * esz}
 
-    # ---- roofline of the iteration kernels (CUDA events, same stream)
+    # ---- roofline of the dominant pass kernel (CUDA events on the launching stream)
     kern_ms = dev.time_passes(Bd, Bd, L, cfg.lam, reps=20)
+    engines = dev.last_engines()
     it_ms = sum(kern_ms)
     F = algorithmic(cfg)
     flops_it = F * m * m * len(ops)
-    # binding compute roof: the tensor instruction the passes issue, measured live. fp32 runs
+    # binding compute roof: the tensor instruction each pass issues, measured live. fp32 runs
     # 3xTF32 (three TF32 MMAs per fp32-accurate product), so its roof is the TF32 rate / 3.
-    peak_fma = fma_peak(args.dtype) / (3.0 if args.dtype == "float32" else 1.0)
+    peak_of = {}
+
+    def engine_peak(eng):
+        if eng not in peak_of:
+            if eng == "dmma":
+                peak_of[eng] = (fma_peak("float64"), "FP64 tensor-core DMMA m8n8k4 burn")
+            elif eng == "tcgen05_tf32":
+                peak_of[eng] = (fma_peak("tcgen05_tf32") / 3.0,
+                                "tcgen05.mma kind::tf32 M128 N256 K8 burn / 3 (3xTF32 passes)")
+            else:  # mma.sync TF32 (and the FFMA / generic fallbacks, bounded by the same roof)
+                peak_of[eng] = (fma_peak("float32") / 3.0, "TF32 tensor-core mma.sync m16n8k8 burn / 3 (3xTF32 passes)")
+        return peak_of[eng]
+
+    k_dom = max(range(4), key=lambda i: kern_ms[i])
+    flops_pass = F / 4 * m * m * len(ops)  # one axis filter of all r terms over every pixel
+    achieved_tf = flops_pass / (kern_ms[k_dom] * 1e-3) / 1e12
+    peak_dom, peak_src = engine_peak(engines[k_dom])
+    traffic = committed_traffic(cfg.name, args.dtype)
     peaks, peak_kind = measured_peaks()
-    achieved_tf = flops_it / (it_ms * 1e-3) / 1e12
     hbm_gbs = 8 * esz * m * m * len(ops) / (it_ms * 1e-3) / 1e9
+    phase = ["pass A forward (split)", "pass B forward (sum, residual epilogue)",
+             "pass A adjoint (split)", "pass B adjoint (sum, fused FISTA update)"]
     roofline = {
         "bound": "tensor",
-        "kernel": "one sFISTA iteration = kb_pass_a(fwd) + kb_pass_b(resid) + kb_pass_a(adj) + kb_pass_b(update)",
-        "achieved": round(achieved_tf, 3), "peak": round(peak_fma, 3), "unit": "TFLOP/s",
-        "frac": round(achieved_tf / peak_fma, 4),
-        "peak_source": ("measured live by kb_fma_peak in this run: "
-                        + ("FP64 tensor-core DMMA m8n8k4 burn (the pass kernels' instruction)"
-                           if args.dtype == "float64" else
-                           "TF32 tensor-core mma.sync m16n8k8 burn / 3 (3xTF32 passes)")),
-        "per_kernel_ms": [round(x, 5) for x in kern_ms],
-        "traffic": committed_traffic(args.dtype),
+        "kernel": f"{phase[k_dom]} on {engines[k_dom]}: the longest of the iteration's four kernels",
+        "achieved": round(achieved_tf, 3), "peak": round(peak_dom, 3), "unit": "TFLOP/s",
+        "frac": round(achieved_tf / peak_dom, 4),
+        "peak_source": "measured live by kb_fma_peak in this run: " + peak_src,
+        "traffic": traffic[k_dom] if traffic else None,
+        # compulsory bytes of that launch: split reads X, writes r planes; residual sum reads r
+        # planes + B, writes R; update sum reads r planes + Y + X_prev, writes X, Y
+        "traffic_algorithmic_bytes": esz * m * m * len(ops) * (1 + cfg.r, cfg.r + 2, 1 + cfg.r, cfg.r + 4)[k_dom],
+        "iteration": {
+            "per_kernel_ms": [round(x, 5) for x in kern_ms],
+            "engines": engines,
+            "achieved": round(flops_it / (it_ms * 1e-3) / 1e12, 3),
+            "frac_of_peak": [round(F / 4 * m * m * len(ops) / (t * 1e-3) / 1e12 / engine_peak(e)[0], 4)
+                             for t, e in zip(kern_ms, engines)],
+        },
         "hbm": {"achieved": round(hbm_gbs, 1), "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                 "frac": round(hbm_gbs / peaks.get("hbm_gbs", 6550.0), 4), "peak_source": peak_kind,
                 "algorithmic_bytes_per_px_it": 8 * esz},

@@ -31,6 +31,14 @@ extern "C" {
 
 #define KB_F64 0
 #define KB_F32 1
+#define KB_PEAK_TC_TF32 2 /* kb_fma_peak only: the tcgen05 kind::tf32 rate */
+
+/* pass engines reported by kb_last_engines */
+#define KB_ENGINE_GENERIC 0  /* generic tiled kernels (odd shapes, misaligned buffers) */
+#define KB_ENGINE_FFMA 1     /* persistent FFMA register-window kernels (fp32) */
+#define KB_ENGINE_DMMA 2     /* persistent FP64 tensor-core DMMA kernels */
+#define KB_ENGINE_MMA_TF32 3 /* persistent 3xTF32 mma.sync kernels */
+#define KB_ENGINE_TC_TF32 4  /* tcgen05 3xTF32 kernels (tensor-memory accumulators) */
 
 #define KB_BC_ZERO 0
 #define KB_BC_REFLECTIVE 1
@@ -113,13 +121,17 @@ int kb_block_update(const kb_op* op, const void* Rh, void* X, void* Y, void* wor
  * Measurement helpers used by bench.py (no reference counterpart).
  * kb_fma_peak: measured throughput (TFLOP/s) of the arithmetic instruction the pass kernels issue
  * for dtype - FP64 tensor-core DMMA (m8n8k4) for KB_F64, TF32 tensor-core mma.sync (m16n8k8)
- * for KB_F32, whose 3xTF32 passes issue three per product (roofline denominator).
+ * for KB_F32, tcgen05.mma kind::tf32 (M128 N256 K8, operands in shared memory) for
+ * KB_PEAK_TC_TF32; the fp32 3xTF32 passes issue three per product (roofline denominator).
  * kb_time_passes: average device time (ms, CUDA events on `stream`) of each of the four kernels of
  * one sFISTA iteration, `reps` back-to-back launches each: ms4 = {forward pass A, forward pass B
  * (residual epilogue), adjoint pass A, adjoint pass B (update epilogue, beta = 0)}. X/Yio are
  * overwritten.
  */
 int kb_fma_peak(int dtype, float* tflops, void* stream);
+/* Arithmetic engine of each phase of the latest kb_time_passes on `op` (KB_ENGINE_*), so the
+ * roofline of a phase divides by the peak of the instruction it actually issued. */
+int kb_last_engines(const kb_op* op, int* engines4);
 /* Profiling timeline of the latest fp64 pass kernels launched with KB_DEBUG_MODE bit 7 set:
  * host[kind][block][slot] %globaltimer stamps (kind 0 split, 1 sum; 1024 blocks x 8 slots,
  * slot 7 = SM id); copies min(n, 16384) values. */

@@ -75,9 +75,17 @@ struct kb_op {
   void* ta_corr = nullptr;  // [batch][r][Wpa] taps c_{k-H}
   void* tb_conv = nullptr;
   void* tb_corr = nullptr;
+  // fp32: brick tables of the four tap tables (kb::kb_build_bricks) for the tcgen05 passes,
+  // [batch][r][nbr][256]; null where the axis' band is too narrow for them
+  unsigned* br_a_conv = nullptr;
+  unsigned* br_a_corr = nullptr;
+  unsigned* br_b_conv = nullptr;
+  unsigned* br_b_corr = nullptr;
   GraphCache* graph = nullptr;
   mutable int last_mirror = 0;  // the latest split pass stored Z^T's reflected halo rows
   mutable int last_slots = 0;  // norm partial slots per image written by the latest sum pass
+  mutable int last_engine = 0;  // KB_ENGINE_* of the latest pass launch
+  mutable int phase_engine[4] = {0, 0, 0, 0};  // engines of the latest kb_time_passes phases
 };
 
 namespace {
@@ -147,13 +155,34 @@ bool use_dmma(const kb_op* op) { return op->dtype == KB_F64 && op->m % 2 == 0 &&
 // fp32 runs on the persistent TMA + FFMA kernels when both extents are multiples of 4 (16-byte
 // row strides and vector stores); other shapes take the generic tiled kernels.
 bool use_tma_f32(const kb_op* op) { return op->dtype == KB_F32 && op->m % 4 == 0 && op->n % 4 == 0; }
-// fp32 zero-BC split pass on tcgen05 (kb_tc.cuh): KB_FP32_TC=1 (opt-in while it is validated)
-bool use_tc_split(const kb_op* op, const kb::AxisGeom& g, int mirror_h) {
-  static const bool on = [] {
+// fp32 zero-BC passes on tcgen05 (kb_tc.cuh). KB_FP32_TC=1 / 0 forces them on / off; by default
+// they take the wide bands where they measured faster than the mma.sync kernels on the box
+// (tools/time_kernels.py): split from Kw >= 64, sum from Kw >= 128, and only with
+// enough 64 x 128 chunks to occupy the SMs (a 256^2 image has 8).
+int tc_policy() {
+  static const int p = [] {
     const char* v = std::getenv("KB_FP32_TC");
-    return v && v[0] == '1';
+    return v ? (v[0] == '1' ? 1 : 0) : -1;
   }();
-  return on && use_tma_f32(op) && !g.fill && mirror_h == 0;
+  return p;
+}
+bool use_tc(const kb_op* op, const kb::AxisGeom& g, int min_kw) {
+  if (!use_tma_f32(op) || tc_policy() == 0) return false;
+  if (tc_policy() == 1) return true;
+  const long long chunks = (long long)((g.len + kb::kTcTS - 1) / kb::kTcTS) * ((g.other + 127) / 128) * op->batch;
+  return g.Kw >= min_kw && chunks >= 128;
+}
+// the brick table built from tap table `tin`, or null
+const unsigned* brick_table(const kb_op* op, const void* tin) {
+  if (tin == op->ta_conv) return op->br_a_conv;
+  if (tin == op->ta_corr) return op->br_a_corr;
+  if (tin == op->tb_conv) return op->br_b_conv;
+  if (tin == op->tb_corr) return op->br_b_corr;
+  return nullptr;
+}
+
+bool use_tc_split(const kb_op* op, const kb::AxisGeom& g, int mirror_h) {
+  return use_tc(op, g, 64) && !g.fill && mirror_h == 0;
 }
 // fp32 arithmetic of the persistent kernels: 3xTF32 tensor-core MMA (kb_tf32.cuh, default) or
 // FFMA register windows (kb_ffma.cuh; KB_FP32_PATH=ffma)
@@ -355,25 +384,28 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
       KB_TRY(allow_smem(kern, smem));
       int parts, nb, eparts;
       plan(bps, parts, nb, eparts);
+      op->last_engine = sizeof(T) == 8 ? KB_ENGINE_DMMA : KB_ENGINE_FFMA;
       KB_CUDA(launch_persistent(kern, nb, smem, s, map, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r, op->batch,
                                 parts, eparts, mirror_h, msign));
       op->last_mirror = mirror_h > 0;
       return KB_OK;
     }
+    op->last_engine = KB_ENGINE_GENERIC;
     return launch_a_g<T, kGmaxF64>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
   } else {
-    if (use_tc_split(op, g, mirror_h) && z_bs == (long long)op->r * z_ps) {
+    const unsigned* btab = brick_table(op, tin);
+    if (btab && use_tc_split(op, g, mirror_h) && z_bs == (long long)op->r * z_ps) {
       const int nbr = kb::tc_bricks(g.Kw);
-      // bricks and tap scratch of up to kTcG terms first, then as deep a tile ring as the rest of
-      // shared memory holds (at least 3 stages)
+      // bricks of up to kTcG terms first, then as deep a tile ring as the rest of shared memory
+      // holds (at least 3 stages)
       const size_t avail = 226 * 1024 - 1024 - kb::kTcStoreBytes;
       static const int gmax = [] {
         const char* v = std::getenv("KB_TC_G");
         return v ? std::max(1, std::min(kb::kTcG, std::atoi(v))) : kb::kTcG;
       }();
       int G = std::min(op->r, gmax);
-      while (G > 1 && (size_t)G * nbr * 1024 + kb::tc_tap_bytes(G, g.Kw) + 3 * kb::kTcStageBytes > avail) --G;
-      const size_t fixed = (size_t)G * nbr * 1024 + kb::tc_tap_bytes(G, g.Kw);
+      while (G > 1 && (size_t)G * nbr * 1024 + 3 * kb::kTcStageBytes > avail) --G;
+      const size_t fixed = (size_t)G * nbr * 1024;
       const int nst = std::min<int>(kb::kTcRingMax, (int)((avail - std::min(fixed, avail)) / kb::kTcStageBytes));
       const size_t smem = std::max<size_t>(1024 + kb::kTcStoreBytes + (size_t)nst * kb::kTcStageBytes + fixed,
                                            116 * 1024);  // one CTA per SM
@@ -396,7 +428,8 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = use_pdl() ? 1 : 0;
-        KB_CUDA(cudaLaunchKernelEx(&cfg, kern, mapt, mapz, z, z_ps, z_bs, tin, t_bs, g, nw2, op->r, op->batch, parts,
+        op->last_engine = KB_ENGINE_TC_TF32;
+        KB_CUDA(cudaLaunchKernelEx(&cfg, kern, mapt, mapz, z, z_ps, z_bs, btab, g, nw2, op->r, op->batch, parts,
                                    G, nst));
         return KB_OK;
       }
@@ -413,6 +446,7 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
         KB_TRY(allow_smem(kern, smem));
         int parts, nb, eparts;
         plan(bps, parts, nb, eparts);
+        op->last_engine = KB_ENGINE_MMA_TF32;
         KB_CUDA(launch_persistent(kern, nb, smem, s, mapx, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r,
                                   op->batch, parts, eparts, mirror_h, msign, nst));
         op->last_mirror = mirror_h > 0;
@@ -429,11 +463,13 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
       KB_TRY(allow_smem(kern, smem));
       int parts, nb, eparts;
       plan(bps, parts, nb, eparts);
+      op->last_engine = sizeof(T) == 8 ? KB_ENGINE_DMMA : KB_ENGINE_FFMA;
       KB_CUDA(launch_persistent(kern, nb, smem, s, map, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r, op->batch,
                                 parts, eparts, mirror_h, msign));
       op->last_mirror = mirror_h > 0;
       return KB_OK;
     }
+    op->last_engine = KB_ENGINE_GENERIC;
     return launch_a_g<T, kGmaxF32>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
   }
 }
@@ -471,8 +507,42 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
     CUtensorMap map;
     if (use_dmma(op) && persistent_ok && bps > 0 &&
         make_tmap(&map, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, tb.box_rows))
-      return launch(kb::kb_pass_sum_dmma<MODE>, smem, bps, map);
+      return op->last_engine = KB_ENGINE_DMMA, launch(kb::kb_pass_sum_dmma<MODE>, smem, bps, map);
   } else {
+    const unsigned* btab = brick_table(op, tin);
+    if (btab && use_tc(op, g, 128) && persistent_ok && !g_in.fill && !mirrored && e.foldH == 0) {
+      // tcgen05 sum pass (kb_tc.cuh): double-buffered bricks from the brick table, tile ring
+      const int nbr = kb::tc_bricks(g.Kw);
+      const size_t fixed = 2 * (size_t)nbr * 1024;
+      const size_t avail = 226 * 1024 - 1024;
+      const int nst = fixed < avail ? std::min<int>(kb::kTcRingMax, (int)((avail - fixed) / kb::kTcStageBytes)) : 0;
+      const size_t smem = std::max<size_t>(1024 + (size_t)nst * kb::kTcStageBytes + fixed, 116 * 1024);
+      // chunks are dealt round-robin over one block per SM (kb::StrideWalk)
+      const long long nch = (long long)((g.len + kb::kTcTS - 1) / kb::kTcTS) * ((g.other + 127) / 128) * op->batch;
+      const int nb = (int)std::min<long long>(sm_count(), nch);
+      CUtensorMap mapt;
+      if (nst >= 3 && nb * kb::kTcSumEpi <= sum_blocks(op) &&
+          make_tmap(&mapt, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, kb::kTcRB, 4, 128)) {
+        auto kern = kb::kb_pass_sum_tc<MODE>;
+        KB_TRY(allow_smem(kern, smem));
+        if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // warps skip untouched images
+          KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kTcSumEpi, s));
+        op->last_slots = nb * kb::kTcSumEpi;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(nb);
+        cfg.blockDim = dim3(kb::kTcSumThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = use_pdl() ? 1 : 0;
+        op->last_engine = KB_ENGINE_TC_TF32;
+        KB_CUDA(cudaLaunchKernelEx(&cfg, kern, mapt, op->r, btab, g, e, op->batch, nst));
+        return KB_OK;
+      }
+    }
     if (use_tf32(op) && persistent_ok) {
       const kb::TileBoxesX tx = kb::tile_boxes_x(kb::tf32_rows(kb::kNW * 16, g.Kw));
       const size_t fixed = 2 * (size_t)op->r * kb::tf32_cstride(g.Kw) * sizeof(float);
@@ -482,7 +552,7 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
       CUtensorMap mapx;
       if (bps > 0 && make_tmap(&mapx, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps,
                                tx.box_rows, 4, kb::kXF))
-        return launch(kb::kb_pass_sum_x<MODE>, smem, bps, mapx, nst);
+        return op->last_engine = KB_ENGINE_MMA_TF32, launch(kb::kb_pass_sum_x<MODE>, smem, bps, mapx, nst);
     }
     const kb::TileBoxesF tb = kb::tile_boxes_f(kb::kNW * 16 + g.Wp);
     const size_t smem = sizeof(float) * ((size_t)kb::kStages * tb.stage_elems + (size_t)op->r * g.Wp);
@@ -490,7 +560,7 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
     CUtensorMap map;
     if (use_tma_f32(op) && persistent_ok && bps > 0 &&
         make_tmap(&map, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, tb.box_rows, 4))
-      return launch(kb::kb_pass_sum_f<MODE>, smem, bps, map);
+      return op->last_engine = KB_ENGINE_FFMA, launch(kb::kb_pass_sum_f<MODE>, smem, bps, map);
   }
   constexpr int TS = kb::kNW * kRB;
   const size_t smem = sizeof(T) * (2 * (size_t)(TS + g.Wp) * 32 + 2 * (size_t)g.Wp);
@@ -502,6 +572,7 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
   dim3 grid((g.other + 31) / 32, (g.len + TS - 1) / TS, op->batch);
   dim3 block(32, kb::kNW);
   op->last_slots = (int)(grid.x * grid.y);
+  op->last_engine = KB_ENGINE_GENERIC;
   kern<<<grid, block, smem, s>>>(z, z_ps, z_bs, op->r, tin, t_bs, g, tsign, e);
   KB_CUDA(cudaGetLastError());
   return KB_OK;
@@ -742,6 +813,23 @@ int upload_tables(kb_op* op, int dlo, int w, const double* taps, const std::vect
   return KB_OK;
 }
 
+// brick tables of an axis' two fp32 tap tables, when its band can take the tcgen05 passes
+int build_brick_tables(kb_op* op, int H, int Wp, const void* conv, const void* corr, unsigned** bconv,
+                       unsigned** bcorr) {
+  const int Kw = (2 * H + 1 + 3) / 4 * 4;
+  if (Kw < 64 && tc_policy() != 1) return KB_OK;
+  const int nbr = kb::tc_bricks(Kw);
+  const long long bt = (long long)op->batch * op->r;
+  const size_t bytes = (size_t)bt * nbr * 1024;
+  KB_CUDA(cudaMalloc(bconv, bytes));
+  KB_CUDA(cudaMalloc(bcorr, bytes));
+  const int blocks = (int)std::min<long long>((bt * nbr * 128 + 255) / 256, 4096);
+  kb::kb_build_bricks<<<blocks, 256>>>(static_cast<const float*>(conv), Wp, Kw, nbr, bt, *bconv);
+  kb::kb_build_bricks<<<blocks, 256>>>(static_cast<const float*>(corr), Wp, Kw, nbr, bt, *bcorr);
+  KB_CUDA(cudaGetLastError());
+  KB_CUDA(cudaDeviceSynchronize());
+  return KB_OK;
+}
 template <typename T>
 int upload_signs(kb_op* op, const std::vector<int>& sign) {
   std::vector<T> v(sign.begin(), sign.end());
@@ -774,6 +862,10 @@ void free_op(kb_op* op) {
   cudaFree(op->ta_corr);
   cudaFree(op->tb_conv);
   cudaFree(op->tb_corr);
+  cudaFree(op->br_a_conv);
+  cudaFree(op->br_a_corr);
+  cudaFree(op->br_b_conv);
+  cudaFree(op->br_b_corr);
   if (op->graph) {
     if (op->graph->exec) cudaGraphExecDestroy(op->graph->exec);
     delete op->graph;
@@ -869,6 +961,29 @@ int fma_peak_t(float* tflops, cudaStream_t s) {
   return KB_OK;
 }
 
+// tcgen05 kind::tf32 rate (TFLOP/s): kb_tc_burn, one CTA per SM, two MMA streams each
+int tc_peak(float* tflops, cudaStream_t s) {
+  const int sms = sm_count(), iters = 4096, reps = 5;
+  float* out = nullptr;
+  KB_CUDA(cudaMalloc(&out, sizeof(float)));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  kb::kb_tc_burn<<<sms, 128, 0, s>>>(256, out);  // warm-up
+  cudaEventRecord(e0, s);
+  for (int r = 0; r < reps; ++r) kb::kb_tc_burn<<<sms, 128, 0, s>>>(iters, out);
+  cudaEventRecord(e1, s);
+  cudaError_t ce = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  if (ce != cudaSuccess) return fail(KB_ERR_CUDA, cudaGetErrorString(ce));
+  *tflops = (float)(2.0 * 128 * 256 * 8 * (double)iters * 2 * sms * reps / (ms * 1e-3) / 1e12);
+  return KB_OK;
+}
+
 // Per-phase GPU time of one iteration's four kernels: each phase's `reps` launches are
 // captured into a CUDA graph (as in the solver's fast path, so host launch cost is excluded)
 // and the graph is timed with events on a private stream.
@@ -903,6 +1018,7 @@ int time_passes_t(const kb_op* op, const T* Y, const T* B, T* R, T* X, T* Yio, c
         default: rc = stage_b<T, kb::EPI_UPDATE>(op, 1, eu, w, s); break;
       }
     }
+    op->phase_engine[phase] = op->last_engine;
     cudaError_t ce = cudaStreamEndCapture(s, &graph);
     if (rc == KB_OK && ce == cudaSuccess) ce = cudaGraphInstantiate(&exec, graph, 0);
     if (rc == KB_OK && ce == cudaSuccess) ce = cudaGraphLaunch(exec, s);  // warm-up
@@ -1018,6 +1134,10 @@ int kb_op_create(kb_op** out, int dtype, int m, int n, int r, int batch, int bc_
     rc = upload_tables<float>(op, a_dlo, a_w, a_taps, perm, Ha, op->Wpa, &op->ta_conv, &op->ta_corr);
     if (rc == KB_OK) rc = upload_tables<float>(op, b_dlo, b_w, b_taps, perm, Hb, op->Wpb, &op->tb_conv, &op->tb_corr);
     if (rc == KB_OK && ok_b) rc = upload_signs<float>(op, sign_b);
+    if (rc == KB_OK)
+      rc = build_brick_tables(op, Ha, op->Wpa, op->ta_conv, op->ta_corr, &op->br_a_conv, &op->br_a_corr);
+    if (rc == KB_OK)
+      rc = build_brick_tables(op, Hb, op->Wpb, op->tb_conv, op->tb_corr, &op->br_b_conv, &op->br_b_corr);
   }
   if (rc != KB_OK) {
     free_op(op);
@@ -1183,7 +1303,15 @@ int kb_power_iter(const kb_op* op, void* v, void* wb, void* work, int iters, dou
 int kb_fma_peak(int dtype, float* tflops, void* stream) {
   if (!tflops) return fail(KB_ERR_ARGUMENT, "null output");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == KB_PEAK_TC_TF32) return tc_peak(tflops, s);
   return dtype == KB_F64 ? fma_peak_t<double>(tflops, s) : fma_peak_t<float>(tflops, s);
+}
+
+int kb_last_engines(const kb_op* op, int* engines4) {
+  KB_TRY(check_op(op));
+  if (!engines4) return fail(KB_ERR_ARGUMENT, "null output");
+  for (int i = 0; i < 4; ++i) engines4[i] = op->phase_engine[i];
+  return KB_OK;
 }
 
 int kb_debug_trace(unsigned long long* host, int n) {

@@ -21,6 +21,10 @@
 // the other of two accumulator sets while the next chunk's MMAs run. Zero boundary conditions
 // only (no edge folds); the reflect-filled split takes the mma.sync kernels.
 #pragma once
+#ifndef KB_TC_SPIN_NS
+#define KB_TC_SPIN_NS 1000
+#endif
+#include "kb_ffma.cuh"
 #include "kb_tf32.cuh"
 
 namespace kb {
@@ -37,8 +41,7 @@ constexpr unsigned kTcStageBytes = kTcRB * 128 * 4;  // one [32 rows][128 cols] 
 // tensor memory: two accumulator sets of G x 64 columns, then the A stages
 __host__ __device__ __forceinline__ int tc_astages(int G) { return min(kTcStagesMax, (512 - 128 * G) / 32); }
 constexpr unsigned kTcStoreBytes = 4 * 2 * 4096;  // epilogue staging: 4 warps x 2 buffers x [32 L][32 S]
-// dynamic shared memory: [staging][tile ring][bricks][tap scratch] (1 KB alignment slack in front)
-__host__ __device__ __forceinline__ unsigned tc_tap_bytes(int G, int Kw) { return (G * Kw * 4 + 1023) & ~1023u; }
+// dynamic shared memory: [staging][tile ring][bricks] (1 KB alignment slack in front)
 
 __host__ __device__ __forceinline__ int tc_ksteps(int Kw) { return (Kw + 62) / 8 + 1; }
 __host__ __device__ __forceinline__ int tc_bricks(int Kw) { return (Kw + 14) / 8 + 1; }
@@ -64,8 +67,23 @@ struct TcProf {
   __device__ TcProf(const AxisGeom& g, bool me) : on((g.dbg & 128) && me && blockIdx.x < kTraceBlocks) {}
   __device__ __forceinline__ void start() { if (on) t0 = clock64(); }
   __device__ __forceinline__ void stop() { if (on) acc += clock64() - t0; }
-  __device__ __forceinline__ void put(int slot) { if (on) kb_trace[0][blockIdx.x][slot] = acc; }
+  __device__ __forceinline__ void put(int slot, int kind = 0) { if (on) kb_trace[kind][blockIdx.x][slot] = acc; }
 };
+
+// mbarrier wait for threads off the critical path (epilogue warps): each unsuccessful probe
+// suspends the thread for up to `ns` nanoseconds instead of re-polling at once, so the waiting
+// warps leave the issue slots to the converter and MMA warps that share their SM sub-partition
+__device__ __forceinline__ void mbar_wait_lazy(unsigned long long* bar, unsigned parity, unsigned ns) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAITL_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITL_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(ns)
+      : "memory");
+}
+
+// suspend-time hint of the tcgen05 kernels' barrier waits (KB_TC_SPIN_NS experiments)
+constexpr unsigned kTcSpinNs = KB_TC_SPIN_NS;
 
 // ring position: slot index and the parity of the current lap. Waiting on a consumer-release
 // barrier with parity (phase ^ 1) passes at once on the first lap (fresh barrier).
@@ -136,12 +154,51 @@ __device__ __forceinline__ void tc_ld16(unsigned addr, float (&v)[16]) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(u[i]);
 }
+__device__ __forceinline__ void tc_ld8(unsigned addr, float (&v)[8]) {
+  unsigned u[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7])
+               : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(u[i]);
+}
 __device__ __forceinline__ void tc_st16(unsigned addr, const unsigned (&u)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
           addr),
       "r"(u[0]), "r"(u[1]), "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7]), "r"(u[8]), "r"(u[9]),
       "r"(u[10]), "r"(u[11]), "r"(u[12]), "r"(u[13]), "r"(u[14]), "r"(u[15]));
+}
+
+// 1-D bulk copy global -> shared, completion counted in bytes on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// Brick table of one tap table [batch][r][Wp] (built once per operator at creation): per
+// (image, term) the nbr bricks of kb_pass_split_tc / kb_pass_sum_tc in their shared-memory
+// layout, [batch][r][nbr][hi 128 | lo 128 words], so a pass loads a term's bricks with one bulk
+// copy instead of rebuilding them on its threads.
+__global__ void kb_build_bricks(const float* __restrict__ tin, int Wp, int Kw, int nbr, long long bt_total,
+                                unsigned* __restrict__ out) {
+  const long long total = bt_total * nbr * 128;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long bt = idx / (nbr * 128);
+    const int rem = (int)(idx - bt * nbr * 128), qb = rem >> 7, e = rem & 127, nn = e >> 3, kk = e & 7;
+    const int ti = 8 * qb + kk - nn;
+    const float c = (ti >= 0 && ti < Kw) ? tin[bt * Wp + ti] : 0.f;
+    unsigned h, l;
+    tf32_split_rn(c, h, l);
+    const int off = (nn >> 3) * 64 + (kk >> 2) * 32 + (nn & 7) * 4 + (kk & 3);
+    unsigned* bp = out + (bt * nbr + qb) * 256;
+    bp[off] = h;
+    bp[128 + off] = l;
+  }
 }
 
 // Tensor-core split pass. Work: (image b, 128-column L-tile, S-part) items walked in 64-output
@@ -154,15 +211,12 @@ __device__ __forceinline__ void tc_st16(unsigned addr, const unsigned (&u)[16]) 
 // Z^T planes b * r + term), so every global write is a full line; ragged chunk ends store directly.
 __global__ void __launch_bounds__(kTcThreads, 1)
 kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap zmap,
-                 float* __restrict__ z, long long z_ps, long long z_bs,
-                 const float* __restrict__ tin, long long t_bs, AxisGeom g, const double* __restrict__ nw2, int r,
-                 int batch, int parts, int G, int nst) {
+                 float* __restrict__ z, long long z_ps, long long z_bs, const unsigned* __restrict__ btab,
+                 AxisGeom g, const double* __restrict__ nw2, int r, int batch, int parts, int G, int nst) {
   extern __shared__ __align__(1024) unsigned char kb_smem_tc[];
   __shared__ unsigned long long full[kTcRingMax], sfree[kTcRingMax], a_ready[kTcStagesMax],
-      a_free[kTcStagesMax], acc_full[2], acc_empty[2];
+      a_free[kTcStagesMax], acc_full[2], acc_empty[2], bready;
   __shared__ unsigned tmem_base;
-  __shared__ long long stamp_issue[kTcStagesMax], stamp_ready[kTcStagesMax];  // KB_DEBUG_MODE bit 9
-  const bool lat = (g.dbg & 512) && blockIdx.x < kTraceBlocks;
   unsigned char* base = kb_smem_tc + ((1024 - (smem_u32(kb_smem_tc) & 1023)) & 1023);
   float* staging = reinterpret_cast<float*>(base);  // [4 warps][2][32][32], 128-byte swizzled rows
   float* stages = reinterpret_cast<float*>(base + kTcStoreBytes);  // [nst][32][128]
@@ -174,12 +228,11 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
   const int nk = tc_ksteps(g.Kw), nrb = (nk + 3) / 4, na = (nk + 1) / 2, nbr = tc_bricks(g.Kw);
   const int ngroups = (r + G - 1) / G;
   const int nas = tc_astages(G), acol = 128 * G;  // A stages at columns acol + 32 st
-  float* taps_s = reinterpret_cast<float*>(bricks + G * nbr * 256);  // [G][Kw]
 
   if (tid == 0) {
     for (int st = 0; st < nst; ++st) {
       mbar_init(&full[st], 1);
-      mbar_init(&sfree[st], 8);
+      mbar_init(&sfree[st], 4);  // the owning converter set
     }
     for (int st = 0; st < nas; ++st) {
       mbar_init(&a_ready[st], 4);
@@ -189,6 +242,7 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
       mbar_init(&acc_full[b], kTcIssuers);
       mbar_init(&acc_empty[b], 4);
     }
+    mbar_init(&bready, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -229,7 +283,6 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     TcProf pe(g, warp == 1 && lane == 0), pa(g, warp == 1 && lane == 0);
     RingPos a;
     int chunk = 0;
-    long long lat_wake = 0, lat_n = 0;
     // brick descriptors advance by adding (bytes >> 4) to the start-address field
     const unsigned long long b0 = tc_desc(smem_u32(bricks), 128, 256, 0);
     const int qmax = (g.Kw + 14) >> 3;
@@ -252,10 +305,6 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
           mbar_wait(&a_ready[st], a.phase);  // A stage (and, at a group change, bricks) ready
           __syncwarp();  // reconverge: elect.sync below must see the whole warp
           pa.stop();
-          if (lat && warp == 1 && lane == 0) {
-            lat_wake += clock64() - stamp_ready[st];
-            ++lat_n;
-          }
           if (!(g.dbg & 8)) tc_fence_after();
           const unsigned ahi = tmem + acol + st * 32;
 #pragma unroll
@@ -276,29 +325,24 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
             }
           }
           tc_commit_elect(&a_free[st]);  // the A stage can be refilled once these MMAs have read it
-          if (lat && warp == 1 && lane == 0) stamp_issue[st] = clock64();
         }
         tc_commit_elect(&acc_full[ab]);
         ++chunk;
       }
     }
     if (!(g.dbg & 256)) pa.put(6);
-    if (lat && warp == 1 && lane == 0) {
-      kb_trace[0][blockIdx.x][4] = lat_wake;
-      kb_trace[0][blockIdx.x][6] = lat_n;
-    }
   } else if (warp < kTcEpi) {
     // ---------------- converters: bricks and A stages ----------------
-    // two sets of four warps (one per tensor-memory lane quarter) take alternate A stages
+    // two sets of four warps (one per tensor-memory lane quarter); set cs owns the tiles with
+    // global tile index parity cs and converts both of their A stages
     const int wt = tid - 32 * kTcConv;  // 0..255
     const int cs = wt >> 7;
     const int q = warp & 3;             // tensor-memory lane quarter this warp may access
     const unsigned lane_base = tmem + ((unsigned)(32 * q) << 16);
-    TcProf p1(g, wt == 0), p2(g, wt == 0), pt(g, wt == 0), pc(g, wt == 0), ps(g, wt == 0), pb(g, wt == 0), pm(g, wt == 0), pr(g, wt == 0);
+    TcProf p1(g, wt == 0), p2(g, wt == 0), pt(g, wt == 0), pc(g, wt == 0), ps(g, wt == 0), pb(g, wt == 0);
     pt.start();
     RingPos a, t;
-    int chunk = 0, bricks_key = -1;
-    long long lat_mma = 0;
+    int chunk = 0, bricks_key = -1, nbl = 0, tg = 0;
     for (int gr = 0; gr < ngroups; ++gr) {
       const int g0 = gr * G, gc = min(G, r - g0);
       ChunkWalk walk(g.len, LT, parts, batch, 4);
@@ -306,81 +350,66 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
       while (walk.next(ch, kTcTS)) {
         const int key = ch.b * ngroups + gr;
         if (key != bricks_key) {
+          // the group's bricks: one bulk copy from the brick table once the previous chunk's
+          // MMAs (the last readers of the old bricks) completed
           pb.start();
-          // the previous chunk's MMAs (the last readers of the old bricks) must have completed
-          if (chunk > 0) mbar_wait(&acc_full[(chunk - 1) & 1], ((chunk - 1) >> 1) & 1);
-          // taps -> shared scratch (independent loads), then bricks from the scratch
-          const float* tb = tin + ch.b * t_bs + (long long)g0 * g.Wp;
-#pragma unroll 4
-          for (int idx = wt; idx < gc * g.Kw; idx += 256) {
-            const int gg = idx / g.Kw;
-            taps_s[idx] = tb[(long long)gg * g.Wp + (idx - gg * g.Kw)];
+          if (wt == 0) {
+            if (chunk > 0) mbar_wait(&acc_full[(chunk - 1) & 1], ((chunk - 1) >> 1) & 1);
+            const unsigned bytes = (unsigned)(gc * nbr) * 1024;
+            mbar_arrive_expect_tx(&bready, bytes);
+            bulk_g2s(bricks, btab + ((long long)ch.b * r + g0) * nbr * 256, bytes, &bready);
           }
-          asm volatile("bar.sync 1, 256;" ::: "memory");
-          for (int idx = wt; idx < gc * nbr * 128; idx += 256) {
-            const int gg = idx / (nbr * 128), rem = idx - gg * nbr * 128, qb = rem >> 7, e = rem & 127;
-            const int nn = e >> 3, kk = e & 7;  // B[n][kk]
-            const int ti = 8 * qb + kk - nn;
-            const float c = (ti >= 0 && ti < g.Kw) ? taps_s[gg * g.Kw + ti] : 0.f;
-            unsigned h, l;
-            tf32_split_rn(c, h, l);
-            // K-major INTERLEAVE: core (n/8, kk/4) at (n/8)*256 + (kk/4)*128, row n%8 at 16 B
-            const int off = ((nn >> 3) * 64 + (kk >> 2) * 32 + (nn & 7) * 4 + (kk & 3));
-            unsigned* bp = bricks + (gg * nbr + qb) * 256;
-            bp[off] = h;
-            bp[128 + off] = l;
-          }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          asm volatile("bar.sync 1, 256;" ::: "memory");  // all bricks written before any a_ready
+          mbar_wait(&bready, nbl & 1);  // before any A stage of this chunk is announced
+          ++nbl;
           bricks_key = key;
           pb.stop();
         }
-        // A stages (16 tile rows each): column 32q + lane of each row -> tensor-memory lane, K -> column.
-        // Set cs converts the stages with n % 2 == cs; both sets release every tile once.
-        for (int ia = 0; ia < na; ++ia, a.advance(nas)) {
-          const int ts = t.i;
-          pm.start();
-          if ((a.i & 1) == cs) {  // nas is even: stage parity alternates with the global stage count
-            const int st = a.i;
+        for (int rb = 0; rb < nrb; ++rb, ++tg, t.advance(nst)) {
+          const int nat = min(2, na - 2 * rb);  // A stages of this tile
+          if ((tg & 1) != cs) {
+            a.advance(nas);
+            if (nat == 2) a.advance(nas);
+            continue;
+          }
+          p2.start();
+          mbar_wait(&full[t.i], t.phase);
+          p2.stop();
+          tc_fence_after();
+          const float* tile = stages + t.i * (kTcStageBytes / 4) + 32 * q + lane;
+          int st0 = a.i, st1 = -1;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (h == nat) break;
+            if (h == 1) st1 = a.i;
             p1.start();
-            mbar_wait(&a_free[st], a.phase ^ 1);
+            mbar_wait(&a_free[a.i], a.phase ^ 1);
             p1.stop();
-            if (lat && wt == 0 && a.phase) lat_mma += clock64() - stamp_issue[st];
-            p2.start();
-            mbar_wait(&full[ts], t.phase);
-            p2.stop();
-            if (!(g.dbg & 8)) tc_fence_after();
-            const float* tile = stages + ts * (kTcStageBytes / 4) + (ia & 1) * 16 * 128 + 32 * q + lane;
-            const unsigned ahi = lane_base + acol + st * 32;
             pc.start();
             if (!(g.dbg & 4)) {
               unsigned hi[16], lo[16];
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
-                const float x = tile[i * 128];
+                const float x = tile[(16 * h + i) * 128];
                 hi[i] = __float_as_uint(x) & 0xffffe000u;
                 lo[i] = __float_as_uint(x - __uint_as_float(hi[i]));
               }
+              const unsigned ahi = lane_base + acol + a.i * 32;
               tc_st16(ahi, hi);
               tc_st16(ahi + 16, lo);
             }
             pc.stop();
-            ps.start();
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            ps.stop();
-            if (!(g.dbg & 8)) tc_fence_before();
-            if (!(g.dbg & 16)) __syncwarp();
-            if (lat && (wt & 127) == 0) stamp_ready[st] = clock64();
-            if (lane == 0) mbar_arrive(&a_ready[st]);
+            a.advance(nas);
           }
-          pm.stop();
-          pr.start();
-          if ((ia & 1) || ia == na - 1) {  // this set is done with the tile: TMA may refill it
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sfree[ts]);
-            t.advance(nst);
+          ps.start();
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          ps.stop();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&a_ready[st0]);
+            if (st1 >= 0) mbar_arrive(&a_ready[st1]);
+            mbar_arrive(&sfree[t.i]);  // shared tile read: TMA may refill it
           }
-          pr.stop();
         }
         ++chunk;
       }
@@ -391,11 +420,6 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     pc.put(0);
     ps.put(5);
     pb.put(3);
-    if (lat && wt == 0) kb_trace[0][blockIdx.x][3] = lat_mma;
-    if (g.dbg & 256) {
-      pm.put(4);
-      pr.put(6);
-    }
     pt.put(7);
   } else {
     // ---------------- epilogue: accumulators -> Z^T rows ----------------
@@ -473,6 +497,421 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// Chunks of the tensor-core sum pass, dealt round-robin: block i takes global chunk indices i,
+// i + gridDim.x, ... with the S-chunk index fastest (then L-tile, then image). The blocks that run
+// at the same time then hold adjacent chunks of the same planes, so the 2H halo rows one block
+// re-reads were fetched moments earlier by its neighbour (L2 hits): with one block walking its
+// own chunk range instead, r term planes pass between its reuses and the halo rows come from
+// HBM again (5x the compulsory plane traffic at cfg4).
+struct StrideWalk {
+  int k, nsc, LT, S, total;
+  __device__ StrideWalk(int S_, int LT_, int batch, int TS) : nsc((S_ + TS - 1) / TS), LT(LT_), S(S_) {
+    k = blockIdx.x;
+    total = nsc * LT * batch;
+  }
+  __device__ bool next(Chunk& c, int TS) {
+    if (k >= total) return false;
+    const int sc = k % nsc, rest = k / nsc;
+    c.lt = rest % LT;
+    c.b = rest / LT;
+    c.s0 = sc * TS;
+    c.cnt = min(TS, S - c.s0);
+    k += gridDim.x;
+    return true;
+  }
+};
+
+// ------------------------------------------------------------------------------------------
+// Tensor-core sum pass: Y[l][s] = sum_i sum_t Z_i^T[t][l] d_i[t - s] for a 128-column L-tile and
+// 64-output chunks. Every (chunk, term) accumulates in its own 64-column tensor-memory slot (a
+// ring of four), and eight epilogue warps (lane quarter x 32-output half) add the slots into
+// fp32 registers in term order and run the fused epilogue after the last term: the tensor
+// core's own accumulation stays as long as one split-pass term (one accumulator across all r
+// terms drifts past the fp32 parity bound at the widest BASELINE band). Same producer /
+// issuer / converter pipeline as kb_pass_split_tc; the bricks of consecutive terms alternate
+// between two shared-memory buffers: the producer bulk-copies term t's bricks from the
+// operator's brick table (kb_build_bricks) once the MMAs of term t - 2 completed (bfree), and
+// the issuers wait for them (bready). Zero boundary conditions and no fold corrections;
+// epilogue operands move as 16-byte vectors per lane row.
+// ------------------------------------------------------------------------------------------
+constexpr int kTcSumSlots = 4;                       // per-term accumulator slots (64 columns each)
+constexpr int kTcSumEpi = 8;                         // epilogue warps
+constexpr int kTcSumThreads = 32 * (kTcEpi + kTcSumEpi);
+template <int MODE>
+__device__ __forceinline__ void tc_sum_epi8(const float (&v)[8], const Epi<float>& e, long long at, int cnt,
+                                            float Lb, float db, float rd, double vs, double (&nrm)[3],
+                                            bool& bad) {
+  // 8 consecutive outputs of one row: elements [at, at + cnt), cnt <= 8, at % 4 == 0 when cnt == 8
+  float u[8], w[8];
+  const bool full8 = cnt == 8;
+  auto ld8 = [&](const float* a, float (&o)[8]) {
+    if (full8) {
+      const float4 p0 = *reinterpret_cast<const float4*>(a + at), p1 = *reinterpret_cast<const float4*>(a + at + 4);
+      o[0] = p0.x, o[1] = p0.y, o[2] = p0.z, o[3] = p0.w, o[4] = p1.x, o[5] = p1.y, o[6] = p1.z, o[7] = p1.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = i < cnt ? a[at + i] : 0.f;
+    }
+  };
+  auto st8 = [&](float* a, const float (&o)[8]) {
+    if (full8) {
+      *reinterpret_cast<float4*>(a + at) = make_float4(o[0], o[1], o[2], o[3]);
+      *reinterpret_cast<float4*>(a + at + 4) = make_float4(o[4], o[5], o[6], o[7]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < cnt) a[at + i] = o[i];
+    }
+  };
+  if constexpr (MODE == EPI_PLAIN) {
+    st8(e.out, v);
+  } else if constexpr (MODE == EPI_RESID) {
+    ld8(e.bsub, u);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) u[i] = __fsub_rn(v[i], u[i]);
+    st8(e.out, u);
+  } else if constexpr (MODE == EPI_UPDATE) {
+    ld8(e.y, u);
+    ld8(e.x, w);
+    float xv[8], yv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float a = __fsub_rn(__fmul_rn(Lb, u[i]), v[i]);
+      const float q0 = __fmul_rn(a, rd);
+      xv[i] = fmaf(fmaf(-db, q0, a), rd, q0);
+      if (e.project) xv[i] = (xv[i] > 0.f || xv[i] != xv[i]) ? xv[i] : 0.f;
+      const float d = __fsub_rn(xv[i], w[i]);
+      yv[i] = __fadd_rn(xv[i], __fmul_rn((float)e.beta, d));
+      if (i < cnt) {
+        bad |= !isfinite(xv[i]);
+        if (e.want_norms) {
+          nrm[0] += (double)d * d;
+          nrm[1] += (double)w[i] * w[i];
+          nrm[2] += (double)xv[i] * xv[i];
+        }
+      }
+    }
+    st8(e.x, xv);
+    st8(e.y, yv);
+  } else {  // EPI_POWER
+    ld8(e.vin, u);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < cnt) {
+        const double vv = e.vnw2 ? (double)u[i] / vs : (double)u[i];
+        nrm[0] += vv * v[i];
+        nrm[1] += (double)v[i] * v[i];
+      }
+    st8(e.out, v);
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kTcSumThreads, 1)
+kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* __restrict__ btab, AxisGeom g,
+               Epi<float> e, int batch, int nst) {
+  extern __shared__ __align__(1024) unsigned char kb_smem_tc[];
+  __shared__ unsigned long long full[kTcRingMax], sfree[kTcRingMax], a_ready[kTcStagesMax],
+      a_free[kTcStagesMax], slot_full[kTcSumSlots], slot_empty[kTcSumSlots], bready[2], bfree[2];
+  __shared__ unsigned tmem_base;
+  unsigned char* base = kb_smem_tc + ((1024 - (smem_u32(kb_smem_tc) & 1023)) & 1023);
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
+  const int LT = (g.other + 127) / 128;
+  const int nk = tc_ksteps(g.Kw), nrb = (nk + 3) / 4, na = (nk + 1) / 2, nbr = tc_bricks(g.Kw);
+  const int nas = kTcStagesMax, acol = 64 * kTcSumSlots;  // term slots at 64 j, A stages above
+  float* stages = reinterpret_cast<float*>(base);  // [nst][32][128]
+  unsigned* bricks = reinterpret_cast<unsigned*>(base + nst * kTcStageBytes);  // [2][nbr][256]
+
+  if (tid == 0) {
+    for (int st = 0; st < nst; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&sfree[st], 4);
+    }
+    for (int st = 0; st < nas; ++st) {
+      mbar_init(&a_ready[st], 4);
+      mbar_init(&a_free[st], kTcIssuers);
+    }
+    for (int j = 0; j < kTcSumSlots; ++j) {
+      mbar_init(&slot_full[j], kTcIssuers);
+      mbar_init(&slot_empty[j], kTcSumEpi);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bready[b], 1);
+      mbar_init(&bfree[b], kTcIssuers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const unsigned tmem = __shfl_sync(0xffffffffu, tmem_base, 0);
+  pdl_launch_dependents();
+  pdl_wait();
+
+  if (warp == 0) {
+    // ---------------- TMA producer: per chunk and term, the term's bricks (bulk copy into the
+    // buffer the MMAs of term - 2 released) and its plane's tiles ----------------
+    if (lane == 0) {
+      RingPos t;
+      int tb = 0;
+      const unsigned bbytes = (unsigned)nbr * 1024;
+      StrideWalk walk(g.len, LT, batch, kTcTS);
+      Chunk ch;
+      while (walk.next(ch, kTcTS)) {
+        for (int term = 0; term < r; ++term, ++tb) {
+          const int bb = tb & 1;
+          if (tb >= 2) mbar_wait_lazy(&bfree[bb], ((tb >> 1) - 1) & 1, kTcSpinNs);
+          mbar_arrive_expect_tx(&bready[bb], bbytes);
+          bulk_g2s(bricks + bb * nbr * 256, btab + ((long long)ch.b * r + term) * nbr * 256, bbytes, &bready[bb]);
+          for (int rb = 0; rb < nrb; ++rb, t.advance(nst)) {
+            mbar_wait_lazy(&sfree[t.i], t.phase ^ 1, kTcSpinNs);
+            mbar_arrive_expect_tx(&full[t.i], kTcStageBytes);
+            const int row0 = ch.s0 - g.H + g.halo_lo + kTcRB * rb;
+            tma_load_3d(stages + t.i * (kTcStageBytes / 4), &tmap, ch.lt * 128, row0, ch.b * r + term, &full[t.i]);
+          }
+        }
+      }
+    }
+  } else if (warp < kTcConv) {
+    // ---------------- MMA issuers: one warp per N-block ----------------
+    const int nb = warp - 1;
+    RingPos a, sl;
+    int tb = 0;
+    TcProf pa(g, warp == 1 && lane == 0), pb(g, warp == 1 && lane == 0);
+    const unsigned long long b0 = tc_desc(smem_u32(bricks), 128, 256, 0);
+    const int qmax = (g.Kw + 14) >> 3;
+    StrideWalk walk(g.len, LT, batch, kTcTS);
+    Chunk ch;
+    while (walk.next(ch, kTcTS)) {
+      for (int term = 0; term < r; ++term, ++tb, sl.advance(kTcSumSlots)) {
+        const int bb = tb & 1;
+        pb.start();
+        mbar_wait_lazy(&slot_empty[sl.i], sl.phase ^ 1, kTcSpinNs);  // the epilogue added this slot's previous term
+        mbar_wait_lazy(&bready[bb], (tb >> 1) & 1, kTcSpinNs);        // this term's bricks are built
+        pb.stop();
+        __syncwarp();
+        tc_fence_after();
+        const unsigned dcol = tmem + sl.i * 64 + nb * 16;
+        bool first = true;
+        for (int ia = 0; ia < na; ++ia, a.advance(nas)) {
+          pa.start();
+          mbar_wait_lazy(&a_ready[a.i], a.phase, kTcSpinNs);
+          pa.stop();
+          __syncwarp();
+          tc_fence_after();
+          const unsigned ahi = tmem + acol + a.i * 32;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int k = 2 * ia + h, q = k - 2 * nb;
+            if (!(g.dbg & 1) && k < nk && q >= 0 && q <= qmax) {
+              const unsigned long long bh = b0 + ((unsigned)(bb * nbr + q) * 1024 >> 4);
+              tc_mma3(dcol, ahi + 8 * h, ahi + 16 + 8 * h, bh, bh + (512 >> 4), first ? 0u : 1u);
+              first = false;
+            }
+          }
+          tc_commit_elect(&a_free[a.i]);
+        }
+        tc_commit_elect(&bfree[bb]);       // the brick buffer may be rebuilt
+        tc_commit_elect(&slot_full[sl.i]);  // this term's accumulator is complete
+      }
+    }
+    pa.put(4, 1);
+    pb.put(5, 1);
+  } else if (warp < kTcEpi) {
+    // ---------------- converters: A stages ----------------
+    // set cs owns the tiles with global tile index parity cs and converts both of a tile's A
+    // stages (16 rows each: column 32q + lane of each row -> tensor-memory lane, K -> column)
+    const int wt = tid - 32 * kTcConv;  // 0..255
+    const int cs = wt >> 7;
+    const int q = warp & 3;
+    const unsigned lane_base = tmem + ((unsigned)(32 * q) << 16);
+    RingPos a, t;
+    int tg = 0;
+    TcProf p0(g, wt == 0), p1(g, wt == 0), p2(g, wt == 0), p6(g, wt == 0), p7(g, wt == 0);
+    p7.start();
+    StrideWalk walk(g.len, LT, batch, kTcTS);
+    Chunk ch;
+    while (walk.next(ch, kTcTS)) {
+      for (int term = 0; term < r; ++term) {
+        for (int rb = 0; rb < nrb; ++rb, ++tg, t.advance(nst)) {
+          const int nat = min(2, na - 2 * rb);  // A stages of this tile
+          if ((tg & 1) != cs) {
+            a.advance(nas);
+            if (nat == 2) a.advance(nas);
+            continue;
+          }
+          p2.start();
+          mbar_wait_lazy(&full[t.i], t.phase, kTcSpinNs);
+          p2.stop();
+          tc_fence_after();
+          const float* tile = stages + t.i * (kTcStageBytes / 4) + 32 * q + lane;
+          int st0 = a.i, st1 = -1;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (h == nat) break;
+            if (h == 1) st1 = a.i;
+            p1.start();
+            mbar_wait_lazy(&a_free[a.i], a.phase ^ 1, kTcSpinNs);
+            p1.stop();
+            p0.start();
+            if (!(g.dbg & 4)) {
+              unsigned hi[16], lo[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const float x = tile[(16 * h + i) * 128];
+                hi[i] = __float_as_uint(x) & 0xffffe000u;
+                lo[i] = __float_as_uint(x - __uint_as_float(hi[i]));
+              }
+              const unsigned ahi = lane_base + acol + a.i * 32;
+              tc_st16(ahi, hi);
+              tc_st16(ahi + 16, lo);
+            }
+            p0.stop();
+            a.advance(nas);
+          }
+          p6.start();
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          p6.stop();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&a_ready[st0]);
+            if (st1 >= 0) mbar_arrive(&a_ready[st1]);
+            mbar_arrive(&sfree[t.i]);  // shared tile read: TMA may refill it
+          }
+        }
+      }
+    }
+    p7.stop();
+    p0.put(0, 1);
+    p1.put(1, 1);
+    p2.put(2, 1);
+    p6.put(6, 1);
+    p7.put(7, 1);
+  } else {
+    // ---------------- epilogue: term slots -> fp32 sums -> fused update of the output rows ----------------
+    const int ew = warp - kTcEpi, q = warp & 3, hh = ew >> 2;  // lane quarter, 32-output half
+    const unsigned lane_base = tmem + ((unsigned)(32 * q) << 16);
+    const int nslots = gridDim.x * kTcSumEpi, slot = blockIdx.x * kTcSumEpi + ew;
+    const int n = g.len;
+    double nrm[3] = {0.0, 0.0, 0.0};
+    bool bad = false;
+    int norm_b = -1;
+    RingPos sl;
+    StrideWalk walk(g.len, LT, batch, kTcTS);
+    Chunk ch;
+    while (walk.next(ch, kTcTS)) {
+      if (ch.b != norm_b) {
+        if (norm_b >= 0) kb_warp_finish_f<MODE>(e, nrm, bad, norm_b, nslots, slot, lane);
+        nrm[0] = nrm[1] = nrm[2] = 0.0;
+        bad = false;
+        norm_b = ch.b;
+      }
+      const bool live = 32 * hh < ch.cnt;
+      float sum[32];
+      for (int term = 0; term < r; ++term, sl.advance(kTcSumSlots)) {
+        mbar_wait_lazy(&slot_full[sl.i], sl.phase, 2000);
+        __syncwarp();
+        tc_fence_after();
+        if (live) {
+          const unsigned col = lane_base + sl.i * 64 + 32 * hh;
+          float v[16];
+#pragma unroll
+          for (int p2 = 0; p2 < 2; ++p2) {
+            tc_ld16(col + 16 * p2, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) sum[16 * p2 + i] = term ? __fadd_rn(sum[16 * p2 + i], v[i]) : v[i];
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&slot_empty[sl.i]);
+      }
+      const int l = ch.lt * 128 + 32 * q + lane;
+      if (live && l < g.other && !(g.dbg & 2)) {
+        float Lb = 0.f, db = 1.f, rd = 1.f;
+        double vs = 1.0;
+        if constexpr (MODE == EPI_UPDATE) {
+          Lb = (float)e.L[ch.b];
+          db = (float)e.denom[ch.b];
+          rd = 1.f / db;
+        }
+        if constexpr (MODE == EPI_POWER) vs = e.vnw2 ? sqrt(e.vnw2[ch.b]) : 1.0;
+        const long long row = (long long)ch.b * e.bstride + (long long)l * n + ch.s0 + 32 * hh;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = ch.cnt - 32 * hh - 8 * j;
+          if (c <= 0) break;
+          const float v8[8] = {sum[8 * j], sum[8 * j + 1], sum[8 * j + 2], sum[8 * j + 3],
+                               sum[8 * j + 4], sum[8 * j + 5], sum[8 * j + 6], sum[8 * j + 7]};
+          tc_sum_epi8<MODE>(v8, e, row + 8 * j, min(8, c), Lb, db, rd, vs, nrm, bad);
+        }
+      }
+    }
+    if (norm_b >= 0) kb_warp_finish_f<MODE>(e, nrm, bad, norm_b, nslots, slot, lane);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Roofline denominator for the tcgen05 passes (kb_fma_peak, KB_PEAK_TC_TF32): two warps per CTA
+// each issue `iters` kind::tf32 MMAs of M = 128, N = 256, K = 8 (A and B from shared memory,
+// K-major INTERLEAVE) into their own 256-column accumulator; one CTA per SM.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128, 1) kb_tc_burn(int iters, float* out) {
+  __shared__ __align__(1024) float ops[3 * 1024];  // A: 4 KB, B: 8 KB
+  __shared__ unsigned long long done;
+  __shared__ unsigned tmem_base;
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  for (int i = tid; i < 3 * 1024; i += 128) ops[i] = 1.f + 1e-3f * (float)((i * 37) & 255);
+  if (tid == 0) {
+    mbar_init(&done, 2);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const unsigned tmem = __shfl_sync(0xffffffffu, tmem_base, 0);
+  if (warp < 2) {
+    const unsigned long long ad = tc_desc(smem_u32(ops), 128, 256, 0), bd = tc_desc(smem_u32(ops + 1024), 128, 256, 0);
+    constexpr unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | (32u << 17) | (8u << 24);
+    const unsigned d = tmem + 256 * warp;
+    for (int i = 0; i < iters; ++i)
+      asm volatile(
+          "{\n.reg .pred p, q;\nsetp.ne.b32 q, %4, 0;\nelect.sync _|p, 0xffffffff;\n"
+          "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, q;\n}" ::"r"(d),
+          "l"(ad), "l"(bd), "r"(idesc), "r"(i));
+    tc_commit_elect(&done);
+  }
+  mbar_wait(&done, 0);
+  tc_fence_after();
+  if (warp == 0) {
+    float v[16];
+    tc_ld16(tmem, v);  // keep the result observable
+    if (tid == 0 && blockIdx.x == 0) out[0] = v[0];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }

@@ -20,10 +20,14 @@ from .psf import bc_name
 from .structured import factor_band, kind_name
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkb_b200.so")
+# KB_LIB_PATH: load another build of the same library (compile-time variants in experiments)
+LIB_PATH = os.environ.get("KB_LIB_PATH") or os.path.join(_HERE, "libkb_b200.so")
 
 KB_OK, KB_ERR_ARGUMENT, KB_ERR_CUDA, KB_ERR_NUMERIC = 0, 2, 3, 4
 KB_F64, KB_F32 = 0, 1
+KB_PEAK_TC_TF32 = 2
+# pass engines (kb_last_engines)
+ENGINES = {0: "generic", 1: "ffma", 2: "dmma", 3: "mma_tf32", 4: "tcgen05_tf32"}
 KB_BC_ZERO, KB_BC_REFLECTIVE = 0, 1
 INT_MAX = 2**31 - 1
 
@@ -61,6 +65,7 @@ EXPORTS = {
     "kb_block_residual": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
     "kb_fma_peak": (_c_int, [_c_int, ctypes.POINTER(ctypes.c_float), _vp]),
     "kb_debug_trace": (_c_int, [ctypes.POINTER(ctypes.c_ulonglong), _c_int]),
+    "kb_last_engines": (_c_int, [_vp, ctypes.POINTER(ctypes.c_int)]),
     "kb_time_passes": (
         _c_int,
         [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_dp, _c_double, _vp,
@@ -285,6 +290,12 @@ class DeviceOperator:
         _check(rc, "kb_time_passes")
         return [float(v) for v in ms]
 
+    def last_engines(self) -> list:
+        """Engine names of the four phases of the latest time_passes (kb_last_engines)."""
+        out = (ctypes.c_int * 4)()
+        _check(load_library().kb_last_engines(self._handle, out), "kb_last_engines")
+        return [ENGINES.get(int(v), str(int(v))) for v in out]
+
     def power_iter(self, v, iters: int):
         """Device power iteration; returns the device history [iters][2][batch] (rho, ||w||^2)."""
         torch = _torch()
@@ -298,9 +309,11 @@ class DeviceOperator:
 
 
 def fma_peak(dtype: str = "float64") -> float:
-    """Measured FMA throughput (TFLOP/s) of the current GPU for dtype."""
+    """Measured tensor-instruction throughput (TFLOP/s) of the current GPU: "float64" DMMA,
+    "float32" TF32 mma.sync, "tcgen05_tf32" tcgen05.mma kind::tf32."""
     out = ctypes.c_float()
-    _check(load_library().kb_fma_peak(_code(dtype), ctypes.byref(out), _stream_handle()), "kb_fma_peak")
+    code = KB_PEAK_TC_TF32 if dtype == "tcgen05_tf32" else _code(dtype)
+    _check(load_library().kb_fma_peak(code, ctypes.byref(out), _stream_handle()), "kb_fma_peak")
     return float(out.value)
 
 

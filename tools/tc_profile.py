@@ -21,10 +21,19 @@ for _ in range(3):
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * (2 * 1024 * 8))()
 assert load_library().kb_debug_trace(buf, 2 * 1024 * 8) == 0
-a = np.frombuffer(buf, dtype=np.uint64).reshape(2, 1024, 8)[0].astype(np.float64)
+allk = np.frombuffer(buf, dtype=np.uint64).reshape(2, 1024, 8).astype(np.float64)
+a = allk[0]
 a = a[a[:, 7] > 0]
 names = ["converter convert+st", "converter a_free wait", "converter full wait", "converter bricks",
          "epilogue busy", "converter wait::st", "issuer a_ready wait", "converter total"]
 print(f"{name} m={m}: {len(a)} blocks")
 for i, nm in enumerate(names):
     print(f"  {nm:24s} mean {a[:, i].mean() / 1e3:9.1f} kcyc  max {a[:, i].max() / 1e3:9.1f}")
+s = allk[1]
+s = s[s[:, 7] > 0]
+names1 = ["converter convert+st", "converter a_free wait", "converter full wait", "converter bricks (+bfree)",
+          "issuer a_ready wait", "issuer slot/bready wait", "converter wait::st", "converter total"]
+print(f"sum pass: {len(s)} blocks")
+for i, nm in enumerate(names1):
+    if len(s):
+        print(f"  {nm:26s} mean {s[:, i].mean() / 1e3:9.1f} kcyc  max {s[:, i].max() / 1e3:9.1f}")
