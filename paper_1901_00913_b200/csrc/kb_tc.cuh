@@ -736,7 +736,7 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
     const unsigned lane_base = tmem + ((unsigned)(32 * q) << 16);
     RingPos a, t;
     int tg = 0;
-    TcProf p0(g, wt == 0), p1(g, wt == 0), p2(g, wt == 0), p6(g, wt == 0), p7(g, wt == 0);
+    TcProf p0(g, wt == 0), p1(g, wt == 0), p2(g, wt == 0), p3(g, wt == 0), p6(g, wt == 0), p7(g, wt == 0);
     p7.start();
     StrideWalk walk(g.len, LT, batch, kTcTS);
     Chunk ch;
@@ -781,6 +781,7 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
           p6.start();
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           p6.stop();
+          p3.start();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
@@ -788,6 +789,7 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
             if (st1 >= 0) mbar_arrive(&a_ready[st1]);
             mbar_arrive(&sfree[t.i]);  // shared tile read: TMA may refill it
           }
+          p3.stop();
         }
       }
     }
@@ -795,6 +797,7 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
     p0.put(0, 1);
     p1.put(1, 1);
     p2.put(2, 1);
+    p3.put(3, 1);
     p6.put(6, 1);
     p7.put(7, 1);
   } else {

@@ -1,6 +1,6 @@
 """Per-kernel duration and DRAM traffic of one iteration's four pass kernels from an ncu report.
 
-usage: ncu_traffic.py REPORT DTYPE [OUT_JSON]
+usage: ncu_traffic.py REPORT DTYPE [OUT_JSON [CONFIG]]
 The report is `ncu --set full --cache-control none --clock-control none -k regex:kb_pass_ -s 4
 -c 4 python tools/one_iter.py DTYPE` (the second iteration, warm L2 as inside a solve). With
 OUT_JSON the iteration's bytes are merged into that file under DTYPE (bench.py reads it as the
@@ -44,7 +44,8 @@ if len(sys.argv) > 3:
             cur = json.load(f)
     cur[dtype] = total
     cur.setdefault("_per_kernel", {})[dtype] = out
+    cfgname = sys.argv[4] if len(sys.argv) > 4 else "cfg2"
     cur["_source"] = ("ncu --set full --cache-control none --clock-control none, tools/one_iter.py "
-                      "(second iteration of cfg2), dram__bytes_read.sum + dram__bytes_write.sum")
+                      f"(second iteration of {cfgname}), dram__bytes_read.sum + dram__bytes_write.sum")
     with open(path, "w") as f:
         json.dump(cur, f, indent=1)

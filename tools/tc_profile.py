@@ -31,7 +31,7 @@ for i, nm in enumerate(names):
     print(f"  {nm:24s} mean {a[:, i].mean() / 1e3:9.1f} kcyc  max {a[:, i].max() / 1e3:9.1f}")
 s = allk[1]
 s = s[s[:, 7] > 0]
-names1 = ["converter convert+st", "converter a_free wait", "converter full wait", "converter bricks (+bfree)",
+names1 = ["converter convert+st", "converter a_free wait", "converter full wait", "converter fence+arrives",
           "issuer a_ready wait", "issuer slot/bready wait", "converter wait::st", "converter total"]
 print(f"sum pass: {len(s)} blocks")
 for i, nm in enumerate(names1):
