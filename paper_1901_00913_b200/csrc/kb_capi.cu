@@ -159,16 +159,20 @@ bool use_tma_f32(const kb_op* op) { return op->dtype == KB_F32 && op->m % 4 == 0
 // they take the wide bands where they measured faster than the mma.sync kernels on the box
 // (tools/time_kernels.py): split from Kw >= 64, sum from Kw >= 128, and only with
 // enough 64 x 128 chunks to occupy the SMs (a 256^2 image has 8).
-int tc_policy() {
+// (KB_FP32_TC=split / sum force one pass only.)
+int tc_policy(int pass) {  // pass: 1 split, 2 sum
   static const int p = [] {
     const char* v = std::getenv("KB_FP32_TC");
-    return v ? (v[0] == '1' ? 1 : 0) : -1;
+    if (!v) return -1;
+    const std::string s(v);
+    return s == "1" ? 3 : s == "split" ? 1 : s == "sum" ? 2 : 0;
   }();
-  return p;
+  return p < 0 ? -1 : (p & pass) ? 1 : 0;
 }
 bool use_tc(const kb_op* op, const kb::AxisGeom& g, int min_kw) {
-  if (!use_tma_f32(op) || tc_policy() == 0) return false;
-  if (tc_policy() == 1) return true;
+  const int pol = tc_policy(min_kw == 64 ? 1 : 2);
+  if (!use_tma_f32(op) || pol == 0) return false;
+  if (pol == 1) return true;
   const long long chunks = (long long)((g.len + kb::kTcTS - 1) / kb::kTcTS) * ((g.other + 127) / 128) * op->batch;
   return g.Kw >= min_kw && chunks >= 128;
 }
@@ -181,9 +185,7 @@ const unsigned* brick_table(const kb_op* op, const void* tin) {
   return nullptr;
 }
 
-bool use_tc_split(const kb_op* op, const kb::AxisGeom& g, int mirror_h) {
-  return use_tc(op, g, 64) && !g.fill && mirror_h == 0;
-}
+bool use_tc_split(const kb_op* op, const kb::AxisGeom& g) { return use_tc(op, g, 64); }
 // fp32 arithmetic of the persistent kernels: 3xTF32 tensor-core MMA (kb_tf32.cuh, default) or
 // FFMA register windows (kb_ffma.cuh; KB_FP32_PATH=ffma)
 bool use_tf32(const kb_op* op) {
@@ -394,7 +396,7 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
     return launch_a_g<T, kGmaxF64>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
   } else {
     const unsigned* btab = brick_table(op, tin);
-    if (btab && use_tc_split(op, g, mirror_h) && z_bs == (long long)op->r * z_ps) {
+    if (btab && use_tc_split(op, g) && z_bs == (long long)op->r * z_ps) {
       const int nbr = kb::tc_bricks(g.Kw);
       // bricks of up to kTcG terms first, then as deep a tile ring as the rest of shared memory
       // holds (at least 3 stages)
@@ -405,12 +407,23 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
       }();
       int G = std::min(op->r, gmax);
       while (G > 1 && (size_t)G * nbr * 1024 + 3 * kb::kTcStageBytes > avail) --G;
+      // sign-uniform term groups of <= G terms: the runs of equal fill sign of the pass' groups,
+      // each cut into near-equal pieces
+      kb::Groups tg{};
+      for (int i = 0; i < grp.n;) {
+        int j = i + 1, count = grp.count[i];
+        while (j < grp.n && grp.sign[j] == grp.sign[i] && grp.start[j] == grp.start[i] + count) count += grp.count[j++];
+        add_groups(tg, grp.start[i], count, G, grp.sign[i]);
+        i = j;
+      }
+      G = 0;
+      for (int i = 0; i < tg.n; ++i) G = std::max(G, tg.count[i]);
       const size_t fixed = (size_t)G * nbr * 1024;
       const int nst = std::min<int>(kb::kTcRingMax, (int)((avail - std::min(fixed, avail)) / kb::kTcStageBytes));
       const size_t smem = std::max<size_t>(1024 + kb::kTcStoreBytes + (size_t)nst * kb::kTcStageBytes + fixed,
                                            116 * 1024);  // one CTA per SM
       CUtensorMap mapt, mapz;
-      if (nst >= 3 &&
+      if (nst >= 3 && tg.n <= kb::kMaxGroups &&
           make_tmap(&mapt, in_map, g.other, in_rows, op->batch, g.other, in_bs, kb::kTcRB, 4, 128) &&
           make_tmap(&mapz, z, g.len, g.other, (long long)op->batch * op->r, g.len, z_ps, 32, 4, 32,
                     CU_TENSOR_MAP_SWIZZLE_128B)) {
@@ -430,7 +443,9 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
         cfg.numAttrs = use_pdl() ? 1 : 0;
         op->last_engine = KB_ENGINE_TC_TF32;
         KB_CUDA(cudaLaunchKernelEx(&cfg, kern, mapt, mapz, z, z_ps, z_bs, btab, g, nw2, op->r, op->batch, parts,
-                                   G, nst));
+                                   tg, G, nst, reinterpret_cast<const float*>(in), in_bs, mirror_h,
+                                   reinterpret_cast<const float*>(msign)));
+        op->last_mirror = mirror_h > 0;
         return KB_OK;
       }
     }
@@ -510,7 +525,7 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
       return op->last_engine = KB_ENGINE_DMMA, launch(kb::kb_pass_sum_dmma<MODE>, smem, bps, map);
   } else {
     const unsigned* btab = brick_table(op, tin);
-    if (btab && use_tc(op, g, 128) && persistent_ok && !g_in.fill && !mirrored && e.foldH == 0) {
+    if (btab && use_tc(op, g, 128) && persistent_ok) {
       // tcgen05 sum pass (kb_tc.cuh): double-buffered bricks from the brick table, tile ring
       const int nbr = kb::tc_bricks(g.Kw);
       const size_t fixed = 2 * (size_t)nbr * 1024;
@@ -684,6 +699,7 @@ template <typename T>
 int apply_t(const kb_op* op, int adjoint, const T* X, T* Y, const Work& w, const RowBlock& rb,
             cudaStream_t s) {
   KB_TRY(stage_a<T>(op, adjoint, X, w, rb, nullptr, s));
+  if (debug_mode() & 1024) return KB_OK;  // profiling / debugging: pass A only (Z^T left in the workspace)
   kb::Epi<T> e = epi_base<T>(op, kb::EPI_PLAIN);
   e.out = Y;
   return stage_b<T, kb::EPI_PLAIN>(op, adjoint, e, w, s);
@@ -817,7 +833,7 @@ int upload_tables(kb_op* op, int dlo, int w, const double* taps, const std::vect
 int build_brick_tables(kb_op* op, int H, int Wp, const void* conv, const void* corr, unsigned** bconv,
                        unsigned** bcorr) {
   const int Kw = (2 * H + 1 + 3) / 4 * 4;
-  if (Kw < 64 && tc_policy() != 1) return KB_OK;
+  if (Kw < 64 && tc_policy(3) != 1) return KB_OK;
   const int nbr = kb::tc_bricks(Kw);
   const long long bt = (long long)op->batch * op->r;
   const size_t bytes = (size_t)bt * nbr * 1024;

@@ -1,25 +1,23 @@
-// kb_tc.cuh — fp32 split pass on the 5th-generation tensor cores (tcgen05.mma kind::tf32, 3xTF32).
+// kb_tc.cuh — fp32 passes on the 5th-generation tensor cores (tcgen05.mma kind::tf32, 3xTF32).
 //
-// The same banded GEMM as the other split passes, Z_i^T[l][s] = sum_t X[t][l] c_i[t - s] for a
+// The same banded GEMM as the other passes, Z_i^T[l][s] = sum_t X[t][l] c_i[t - s] for a
 // 128-column L-tile (M = 128) and 16-output N-blocks, accumulated in tensor memory:
 //   A = X^T from tensor memory: the natural [rows][cols] input tile is streamed by TMA in 32-row
-//       blocks; worker warps (lane = column) split each value into tf32 hi + lo and store them to an
-//       A stage in tensor memory (lane = column, column = K). With A read from shared memory the
-//       operand traffic of 16-wide MMAs bounds the tensor core at ~1/4 of its rate (ncu: 57% of the
-//       shared-memory bandwidth at 9% tensor activity).
+//       blocks; converter warps (lane = column) split each value into tf32 hi + lo and store them
+//       to an A stage in tensor memory (lane = column, column = K; 2 K-steps per stage). With A
+//       read from shared memory the operand traffic of 16-wide MMAs bounds the tensor core at ~1/4
+//       of its rate (ncu: 57% of the shared-memory bandwidth at 9% tensor activity).
 //   B = Toeplitz bricks: for N-block nb and K-step k the 16 x 8 operand B[n][kk] = taps[8k + kk -
-//       16nb - n] depends only on o = 8k - 16nb, so each term keeps (Kw+14)/8 + 1 bricks (hi and lo,
-//       K-major INTERLEAVE core matrices) in shared memory.
-//   D = tensor memory: one 16-column accumulator per (term, N-block) of the chunk; every term
-//       accumulates only its own K-range (the 3xTF32 products of one output stay in one accumulator,
-//       33-35 K-steps at the widest BASELINE band).
-// Warp roles: warp 0 streams the tile (TMA); warps 1-12 each issue the MMAs of one (term, N-block)
-// accumulator (one thread each: a single issuing thread serialises its MMAs, ~120 cycles each on
-// the box, so twelve streams feed the tensor core; warp 1 owns the tensor memory); warps 13-16
-// (converters) split the tiles into A stages and rebuild the bricks when the image or term group
-// changes; warps 17-20 run the epilogue (tcgen05.ld -> swizzled staging -> TMA store of Z^T) on
-// the other of two accumulator sets while the next chunk's MMAs run. Zero boundary conditions
-// only (no edge folds); the reflect-filled split takes the mma.sync kernels.
+//       16nb - n] depends only on o = 8k - 16nb, so each term needs (Kw+14)/8 + 1 bricks (hi and
+//       lo, K-major INTERLEAVE core matrices), built once per operator (kb_build_bricks) and
+//       bulk-copied into shared memory.
+//   D = tensor memory: 16-column accumulators per (term, N-block); each term accumulates only
+//       its own K-range (the 3xTF32 products of one output stay in one accumulator, 33-35 K-steps
+//       at the widest BASELINE band).
+// Warp roles: warp 0 streams tiles (TMA) [and, in the sum pass, bricks]; warps 1-4 issue the MMAs
+// of one N-block each (a converged warp issues from uniform registers; warp 1 owns the tensor
+// memory); two sets of four converter warps own alternate tiles and fill the A stages; the last
+// warps run the epilogue on one accumulator set while the MMAs fill the other.
 #pragma once
 #ifndef KB_TC_SPIN_NS
 #define KB_TC_SPIN_NS 1000
@@ -212,7 +210,9 @@ __global__ void kb_build_bricks(const float* __restrict__ tin, int Wp, int Kw, i
 __global__ void __launch_bounds__(kTcThreads, 1)
 kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap zmap,
                  float* __restrict__ z, long long z_ps, long long z_bs, const unsigned* __restrict__ btab,
-                 AxisGeom g, const double* __restrict__ nw2, int r, int batch, int parts, int G, int nst) {
+                 AxisGeom g, const double* __restrict__ nw2, int r, int batch, int parts, Groups grp, int G,
+                 int nst, const float* __restrict__ in, long long in_bs, int mirror_h,
+                 const float* __restrict__ msign) {
   extern __shared__ __align__(1024) unsigned char kb_smem_tc[];
   __shared__ unsigned long long full[kTcRingMax], sfree[kTcRingMax], a_ready[kTcStagesMax],
       a_free[kTcStagesMax], acc_full[2], acc_empty[2], bready;
@@ -226,7 +226,7 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
   const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
   const int LT = (g.other + 127) / 128;
   const int nk = tc_ksteps(g.Kw), nrb = (nk + 3) / 4, na = (nk + 1) / 2, nbr = tc_bricks(g.Kw);
-  const int ngroups = (r + G - 1) / G;
+  const int ngroups = grp.n;  // sign-uniform term groups of <= G terms
   const int nas = tc_astages(G), acol = 128 * G;  // A stages at columns acol + 32 st
 
   if (tid == 0) {
@@ -287,7 +287,7 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     const unsigned long long b0 = tc_desc(smem_u32(bricks), 128, 256, 0);
     const int qmax = (g.Kw + 14) >> 3;
     for (int gr = 0; gr < ngroups; ++gr) {
-      const int g0 = gr * G, gc = min(G, r - g0);
+      const int gc = grp.count[gr];
       const bool live = !(g.dbg & 1);
       ChunkWalk walk(g.len, LT, parts, batch, 4);
       Chunk ch;
@@ -344,7 +344,8 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     RingPos a, t;
     int chunk = 0, bricks_key = -1, nbl = 0, tg = 0;
     for (int gr = 0; gr < ngroups; ++gr) {
-      const int g0 = gr * G, gc = min(G, r - g0);
+      const int g0 = grp.start[gr], gc = grp.count[gr];
+      const float fsign = grp.sign[gr] < 0 ? -1.f : 1.f;
       ChunkWalk walk(g.len, LT, parts, batch, 4);
       Chunk ch;
       while (walk.next(ch, kTcTS)) {
@@ -376,6 +377,8 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
           p2.stop();
           tc_fence_after();
           const float* tile = stages + t.i * (kTcStageBytes / 4) + 32 * q + lane;
+          const int row_lo = g.g0 + ch.s0 - g.H + kTcRB * rb;  // global row of tile row 0
+          const bool edge = g.fill && (row_lo < 0 || row_lo + kTcRB > g.Mg);
           int st0 = a.i, st1 = -1;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -389,7 +392,14 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
               unsigned hi[16], lo[16];
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
-                const float x = tile[(16 * h + i) * 128];
+                float x = tile[(16 * h + i) * 128];
+                if (edge) {  // reflect fill: sign * X[fold(row)] from global memory (edge tiles only)
+                  const int gr = row_lo + 16 * h + i;
+                  if (gr < 0 || gr >= g.Mg) {
+                    const int f = kb_fold(gr, g.Mg), col = ch.lt * 128 + 32 * q + lane;
+                    x = (f >= 0 && col < g.other) ? fsign * in[ch.b * in_bs + (long long)(f - g.g0) * g.other + col] : 0.f;
+                  }
+                }
                 hi[i] = __float_as_uint(x) & 0xffffe000u;
                 lo[i] = __float_as_uint(x - __uint_as_float(hi[i]));
               }
@@ -428,7 +438,7 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     TcProf p3(g, warp == kTcEpi && lane == 0), p4(g, warp == kTcEpi && lane == 0);
     int chunk = 0, nstore = 0;
     for (int gr = 0; gr < ngroups; ++gr) {
-      const int g0 = gr * G, gc = min(G, r - g0);
+      const int g0 = grp.start[gr], gc = grp.count[gr];
       ChunkWalk walk(g.len, LT, parts, batch, 4);
       Chunk ch;
       while (walk.next(ch, kTcTS)) {
@@ -472,7 +482,7 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
                     make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
               __syncwarp();
-              if (lane == 0) {
+              if (lane == 0 && l0 < g.other) {  // boxes wholly past the last row carry no data
                 tma_store_3d(&zmap, sb, ch.s0 + s, l0, ch.b * r + g0 + gg);
                 bulk_commit();
               }
@@ -481,6 +491,27 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
 #pragma unroll
               for (int i = 0; i < 32; ++i)
                 if (s + i < ch.cnt) zp[s + i] = v[i];
+            }
+            // reflected halo rows of Z^T for a reflect-filled sum pass (edge L-tiles only):
+            // row -1 - l and / or row 2 * other - 1 - l (both when the halo spans the plane),
+            // times the term's mirror sign
+            if (mirror_h > 0 && l < g.other && (l < mirror_h || l >= g.other - mirror_h)) {
+              const float sg = msign ? msign[(long long)ch.b * r + g0 + gg] : 1.f;
+#pragma unroll
+              for (int side = 0; side < 2; ++side) {
+                if (side == 0 ? l >= mirror_h : l < g.other - mirror_h) continue;
+                float* zm = zp + (long long)((side == 0 ? -1 - l : 2 * g.other - 1 - l) - l) * g.len;
+                if (s + 32 <= ch.cnt) {
+#pragma unroll
+                  for (int c = 0; c < 8; ++c)
+                    reinterpret_cast<float4*>(zm + s)[c] =
+                        make_float4(sg * v[4 * c], sg * v[4 * c + 1], sg * v[4 * c + 2], sg * v[4 * c + 3]);
+                } else {
+#pragma unroll
+                  for (int i = 0; i < 32; ++i)
+                    if (s + i < ch.cnt) zm[s + i] = sg * v[i];
+                }
+              }
             }
           }
         }
@@ -536,8 +567,9 @@ struct StrideWalk {
 // issuer / converter pipeline as kb_pass_split_tc; the bricks of consecutive terms alternate
 // between two shared-memory buffers: the producer bulk-copies term t's bricks from the
 // operator's brick table (kb_build_bricks) once the MMAs of term t - 2 completed (bfree), and
-// the issuers wait for them (bready). Zero boundary conditions and no fold corrections;
-// epilogue operands move as 16-byte vectors per lane row.
+// the issuers wait for them (bready). Reflective axes read the reflected halo rows the split
+// pass stored (TMA boxes over the padded planes) and add the adjoint's fold corrections in the
+// epilogue; epilogue operands move as 16-byte vectors per lane row.
 // ------------------------------------------------------------------------------------------
 constexpr int kTcSumSlots = 4;                       // per-term accumulator slots (64 columns each)
 constexpr int kTcSumEpi = 8;                         // epilogue warps
@@ -850,12 +882,23 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
         }
         if constexpr (MODE == EPI_POWER) vs = e.vnw2 ? sqrt(e.vnw2[ch.b]) : 1.0;
         const long long row = (long long)ch.b * e.bstride + (long long)l * n + ch.s0 + 32 * hh;
+        const bool fold_edge = e.foldH > 0 && (ch.s0 < e.foldH || ch.s0 + kTcTS > n - e.foldH);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int c = ch.cnt - 32 * hh - 8 * j;
           if (c <= 0) break;
-          const float v8[8] = {sum[8 * j], sum[8 * j + 1], sum[8 * j + 2], sum[8 * j + 3],
-                               sum[8 * j + 4], sum[8 * j + 5], sum[8 * j + 6], sum[8 * j + 7]};
+          float v8[8] = {sum[8 * j], sum[8 * j + 1], sum[8 * j + 2], sum[8 * j + 3],
+                         sum[8 * j + 4], sum[8 * j + 5], sum[8 * j + 6], sum[8 * j + 7]};
+          if (fold_edge) {  // exact adjoint fold corrections of the reflective axis (edge chunks)
+            const int FH = e.foldH;
+            const float* f = e.fold + ((long long)ch.b * g.other + l) * (2 * FH);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int qi = ch.s0 + 32 * hh + 8 * j + i;
+              if (qi < FH) v8[i] += f[qi];
+              else if (qi >= n - FH && qi < n) v8[i] += f[qi - (n - 2 * FH)];
+            }
+          }
           tc_sum_epi8<MODE>(v8, e, row + 8 * j, min(8, c), Lb, db, rd, vs, nrm, bad);
         }
       }
