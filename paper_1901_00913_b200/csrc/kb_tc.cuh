@@ -213,7 +213,7 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
                  AxisGeom g, const double* __restrict__ nw2, int r, int batch, int parts, Groups grp, int G,
                  int nst, const float* __restrict__ in, long long in_bs, int mirror_h,
                  const float* __restrict__ msign) {
-  extern __shared__ __align__(1024) unsigned char kb_smem_tc[];
+  extern __shared__ __align__(16) unsigned char kb_smem_tc[];
   __shared__ unsigned long long full[kTcRingMax], sfree[kTcRingMax], a_ready[kTcStagesMax],
       a_free[kTcStagesMax], acc_full[2], acc_empty[2], bready;
   __shared__ unsigned tmem_base;
@@ -647,7 +647,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kTcSumThreads, 1)
 kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* __restrict__ btab, AxisGeom g,
                Epi<float> e, int batch, int nst) {
-  extern __shared__ __align__(1024) unsigned char kb_smem_tc[];
+  extern __shared__ __align__(16) unsigned char kb_smem_tc[];
   __shared__ unsigned long long full[kTcRingMax], sfree[kTcRingMax], a_ready[kTcStagesMax],
       a_free[kTcStagesMax], slot_full[kTcSumSlots], slot_empty[kTcSumSlots], bready[2], bfree[2];
   __shared__ unsigned tmem_base;
