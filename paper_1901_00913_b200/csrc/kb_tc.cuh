@@ -96,6 +96,21 @@ struct RingPos {
   }
 };
 
+// reflect fill of 16 consecutive tile rows starting at global row r0 (edge tiles of a reflective
+// axis only; the interior tiles load all 16 rows before this branch):
+// out-of-domain rows take sign * X[fold(row)] from global memory
+__device__ __forceinline__ void tc_reflect_fill(float* xv, int r0, const AxisGeom& g, const float* __restrict__ in,
+                                             long long img, int col, float fsign) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int gr = r0 + i;
+    if (gr < 0 || gr >= g.Mg) {
+      const int f = kb_fold(gr, g.Mg);
+      xv[i] = (f >= 0 && col < g.other) ? fsign * in[img + (long long)(f - g.g0) * g.other + col] : 0.f;
+    }
+  }
+}
+
 // one 3xTF32 K-step, issued by one elected lane of a converged warp: D (+)= lo*hi + hi*lo + hi*hi
 __device__ __forceinline__ void tc_mma3(unsigned d, unsigned ahi, unsigned alo, unsigned long long bh,
                                         unsigned long long bl, unsigned acc) {
@@ -390,18 +405,14 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
             pc.start();
             if (!(g.dbg & 4)) {
               unsigned hi[16], lo[16];
+              float xv[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) xv[i] = tile[(16 * h + i) * 128];
+              if (edge) tc_reflect_fill(xv, row_lo + 16 * h, g, in, ch.b * in_bs, ch.lt * 128 + 32 * q + lane, fsign);
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
-                float x = tile[(16 * h + i) * 128];
-                if (edge) {  // reflect fill: sign * X[fold(row)] from global memory (edge tiles only)
-                  const int gr = row_lo + 16 * h + i;
-                  if (gr < 0 || gr >= g.Mg) {
-                    const int f = kb_fold(gr, g.Mg), col = ch.lt * 128 + 32 * q + lane;
-                    x = (f >= 0 && col < g.other) ? fsign * in[ch.b * in_bs + (long long)(f - g.g0) * g.other + col] : 0.f;
-                  }
-                }
-                hi[i] = __float_as_uint(x) & 0xffffe000u;
-                lo[i] = __float_as_uint(x - __uint_as_float(hi[i]));
+                hi[i] = __float_as_uint(xv[i]) & 0xffffe000u;
+                lo[i] = __float_as_uint(xv[i] - __uint_as_float(hi[i]));
               }
               const unsigned ahi = lane_base + acol + a.i * 32;
               tc_st16(ahi, hi);
