@@ -59,10 +59,15 @@ constexpr unsigned kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (2u << 17) | 
 // 0 producer waiting for free tiles, 1/2 converters waiting for A stages / tiles, 3 epilogue
 // waiting for the accumulators, 4 epilogue busy, 5/6 issuer 0 waiting for drained accumulators /
 // A stages, 7 converter-0 kernel cycles.
+// Compiled in only with -DKB_TC_PROF=1 (tools/tc_profile.py builds that variant): the runtime
+// checks alone cost ~8% of the sum pass' issued instructions.
+#ifndef KB_TC_PROF
+#define KB_TC_PROF 0
+#endif
 struct TcProf {
   bool on;
   unsigned long long acc = 0, t0 = 0;
-  __device__ TcProf(const AxisGeom& g, bool me) : on((g.dbg & 128) && me && blockIdx.x < kTraceBlocks) {}
+  __device__ TcProf(const AxisGeom& g, bool me) : on(KB_TC_PROF && (g.dbg & 128) && me && blockIdx.x < kTraceBlocks) {}
   __device__ __forceinline__ void start() { if (on) t0 = clock64(); }
   __device__ __forceinline__ void stop() { if (on) acc += clock64() - t0; }
   __device__ __forceinline__ void put(int slot, int kind = 0) { if (on) kb_trace[kind][blockIdx.x][slot] = acc; }
@@ -78,6 +83,30 @@ __device__ __forceinline__ void mbar_wait_lazy(unsigned long long* bar, unsigned
       "@!p bra WAITL_%=;\n}\n" ::"r"(smem_u32(bar)),
       "r"(parity), "r"(ns)
       : "memory");
+}
+
+// mbarrier wait that sleeps between probes: for the roles that are never on the critical path
+// (the TMA producer waiting for a free ring stage, the epilogue waiting for a finished term),
+// so their polling does not take issue slots from the converter and MMA warps of the same SM
+// sub-partition
+#ifndef KB_TC_SLEEP_NS
+#define KB_TC_SLEEP_NS 256
+#endif
+__device__ __forceinline__ bool mbar_test(unsigned long long* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_idle(unsigned long long* bar, unsigned parity, unsigned lazy_ns) {
+  if (KB_TC_SLEEP_NS > 0) {
+    while (!mbar_test(bar, parity)) __nanosleep(KB_TC_SLEEP_NS);
+  } else {
+    mbar_wait_lazy(bar, parity, lazy_ns);
+  }
 }
 
 // suspend-time hint of the tcgen05 kernels' barrier waits (KB_TC_SPIN_NS experiments)
@@ -282,7 +311,11 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
         while (walk.next(ch, kTcTS)) {
           for (int rb = 0; rb < nrb; ++rb, t.advance(nst)) {
             pw.start();
+#if KB_TC_SPLIT_PRODUCER_SPIN
             mbar_wait(&sfree[t.i], t.phase ^ 1);
+#else
+            mbar_wait_idle(&sfree[t.i], t.phase ^ 1, kTcSpinNs);
+#endif
             pw.stop();
             mbar_arrive_expect_tx(&full[t.i], kTcStageBytes);
             const int row0 = ch.s0 - g.H + g.halo_lo + kTcRB * rb;
@@ -712,11 +745,11 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
       while (walk.next(ch, kTcTS)) {
         for (int term = 0; term < r; ++term, ++tb) {
           const int bb = tb & 1;
-          if (tb >= 2) mbar_wait_lazy(&bfree[bb], ((tb >> 1) - 1) & 1, kTcSpinNs);
+          if (tb >= 2) mbar_wait_idle(&bfree[bb], ((tb >> 1) - 1) & 1, kTcSpinNs);
           mbar_arrive_expect_tx(&bready[bb], bbytes);
           bulk_g2s(bricks + bb * nbr * 256, btab + ((long long)ch.b * r + term) * nbr * 256, bbytes, &bready[bb]);
           for (int rb = 0; rb < nrb; ++rb, t.advance(nst)) {
-            mbar_wait_lazy(&sfree[t.i], t.phase ^ 1, kTcSpinNs);
+            mbar_wait_idle(&sfree[t.i], t.phase ^ 1, kTcSpinNs);
             mbar_arrive_expect_tx(&full[t.i], kTcStageBytes);
             const int row0 = ch.s0 - g.H + g.halo_lo + kTcRB * rb;
             tma_load_3d(stages + t.i * (kTcStageBytes / 4), &tmap, ch.lt * 128, row0, ch.b * r + term, &full[t.i]);
@@ -865,7 +898,7 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
       const bool live = 32 * hh < ch.cnt;
       float sum[32];
       for (int term = 0; term < r; ++term, sl.advance(kTcSumSlots)) {
-        mbar_wait_lazy(&slot_full[sl.i], sl.phase, 2000);
+        mbar_wait_idle(&slot_full[sl.i], sl.phase, 2000);
         __syncwarp();
         tc_fence_after();
         if (live) {

@@ -1,4 +1,4 @@
-"""Per-role stall cycles of the tcgen05 split kernel (KB_FP32_TC=1 KB_DEBUG_MODE=128).
+"""Per-role stall cycles of the tcgen05 split kernel (KB_FP32_TC=1 KB_DEBUG_MODE=128; needs a -DKB_TC_PROF=1 build, e.g. tools/variant.sh prof -DKB_TC_PROF=1).
 
 usage: tc_profile.py [cfg] [m]   -- prints the block-mean of each kb_tc.cuh TcProf slot (kcycles)
 """

@@ -103,8 +103,8 @@ int main(int argc, char** argv) {
   long long* dc;
   cudaMalloc(&dc, sms * sizeof(long long));
   cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  for (int amode : {3, 5}) {
-    for (int N : {16}) {
+  for (int amode : {0, 1, 2, 3}) {
+    for (int N : {16, 32, 64}) {
       for (int streams : {1, 4, 8}) {
         if (streams * N > 496 || (amode >= 3 && streams > 4)) continue;
         const int iters = 3078;
