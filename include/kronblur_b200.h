@@ -118,6 +118,21 @@ int kb_block_update(const kb_op* op, const void* Rh, void* X, void* Y, void* wor
                     double lam, int project, int* nonfinite, void* stream);
 
 /*
+ * Exact blur of `batch` float64 images — psf.py:170-193 (blur_direct), the `exact_apply` of
+ * solvers.py:182 / pipeline.py:180,294 and the data generator of pipeline.py:88. Y gets, per
+ * pixel, the reference's own sequence: the products P[a][b] * X~[i+l-1-a][j+q-1-b] over the
+ * NONZERO PSF entries in row-major order, each product and each sum rounded separately, X~ the
+ * zero (bc = KB_BC_ZERO) or numpy-"symmetric" (KB_BC_REFLECTIVE) extension of X. The result is
+ * bit-identical to the reference. psf: device [batch or 1][rows][cols] float64 with 1-based
+ * centre (l, q); psf_batch_stride = 0 shares one PSF, rows*cols gives one PSF per image.
+ * Errors (KB_ERR_ARGUMENT) as the reference: PSF larger than the image; X and Y must not
+ * overlap. All-zero PSF borders may be cropped by the caller (they add nothing), so the centre
+ * may lie outside the passed block.
+ */
+int kb_blur_direct(const double* psf, long long psf_batch_stride, int rows, int cols, int l, int q,
+                   const double* X, double* Y, int m, int n, int batch, int bc, void* stream);
+
+/*
  * Measurement helpers used by bench.py (no reference counterpart).
  * kb_fma_peak: measured throughput (TFLOP/s) of the arithmetic instruction the pass kernels issue
  * for dtype - FP64 tensor-core DMMA (m8n8k4) for KB_F64, TF32 tensor-core mma.sync (m16n8k8)

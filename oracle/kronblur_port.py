@@ -252,3 +252,45 @@ def sfista(op, B, L: float, lam: float, iters: int, X0=None, project: bool = Fal
     pop = op if isinstance(op, PortOperator) else PortOperator(op)
     return engine(lambda Y: kron_apply(pop, Y), lambda Y: kron_apply_adjoint(pop, Y), B, L, lam,
                   iters, X0, project, record_iterates)
+
+
+# ---------------------------------------------------------------- exact blur
+def blur_direct(values, center, X, bc: str) -> np.ndarray:
+    """Shifted-copy blur, psf.py:170-193: pad by ((rows-l, l-1), (cols-q, q-1)) with zeros or
+    numpy "symmetric" mode (:184-186), then Y += P[a0, b0] * Xp[rows-1-a0 : +m, cols-1-b0 : +n] over
+    np.nonzero(P) in row-major order (:187-192)."""
+    P = np.asarray(values, dtype=float)
+    X = np.asarray(X, dtype=float)
+    m, n = X.shape
+    rows, cols = P.shape
+    l, q = int(center[0]), int(center[1])
+    pad = ((rows - l, l - 1), (cols - q, q - 1))
+    Xp = np.pad(X, pad, mode="constant" if bc == "zero" else "symmetric")
+    Y = np.zeros_like(X)
+    for a0, b0 in zip(*np.nonzero(P)):
+        r0, c0 = rows - 1 - a0, cols - 1 - b0
+        Y += P[a0, b0] * Xp[r0 : r0 + m, c0 : c0 + n]
+    return Y
+
+
+def blur_direct_pixel(values, center, X, bc: str, i: int, j: int) -> float:
+    """One output pixel of blur_direct by the same per-pixel sequence (separately rounded products
+    and sums over the nonzeros in row-major order): for sampled checks at sizes where the whole
+    image would take hours in numpy."""
+    P = np.asarray(values, dtype=float)
+    m, n = X.shape
+    l, q = int(center[0]), int(center[1])
+
+    def ext(t, M):
+        if 0 <= t < M:
+            return t
+        if bc == "zero":
+            return -1
+        return -1 - t if t < 0 else 2 * M - 1 - t
+
+    y = 0.0
+    for a0, b0 in zip(*np.nonzero(P)):
+        gi, gj = ext(i + l - 1 - a0, m), ext(j + q - 1 - b0, n)
+        x = float(X[gi, gj]) if gi >= 0 and gj >= 0 else 0.0
+        y = y + float(P[a0, b0]) * x
+    return y

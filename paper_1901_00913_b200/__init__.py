@@ -2,11 +2,12 @@
 
 Drop-in entry points (same names, signatures and error behaviour as the reference package
 ``kronblur``): ``sfista``, ``kron_apply``, ``kron_apply_adjoint``, ``estimate_lipschitz``,
-``objective_matrix``, ``decompose``. The arithmetic of the first four runs in the sm_100a kernels of
+``objective_matrix``, ``decompose``, ``blur_direct``. The arithmetic of the first four runs in the sm_100a kernels of
 ``libkb_b200.so`` (C ABI: include/kronblur_b200.h); ``decompose`` is the one-time host setup.
 ``install()`` reroutes an imported ``kronblur`` to these functions.
 """
 
+from .blur import blur_direct, blur_direct_batch
 from .errors import ArgumentError, CapacityError, FormatError, KronblurError, NumericError
 from .kron import (
     KronOperator,

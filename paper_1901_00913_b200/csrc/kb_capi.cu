@@ -24,6 +24,7 @@
 #include "kb_ffma.cuh"
 #include "kb_tf32.cuh"
 #include "kb_tc.cuh"
+#include "kb_blur.cuh"
 
 namespace {
 
@@ -1314,6 +1315,32 @@ int kb_power_iter(const kb_op* op, void* v, void* wb, void* work, int iters, dou
   if (op->dtype == KB_F64)
     return power_t<double>(op, static_cast<double*>(v), static_cast<double*>(wb), w, iters, hist, s);
   return power_t<float>(op, static_cast<float*>(v), static_cast<float*>(wb), w, iters, hist, s);
+}
+
+int kb_blur_direct(const double* psf, long long psf_batch_stride, int rows, int cols, int l, int q,
+                   const double* X, double* Y, int m, int n, int batch, int bc, void* stream) {
+  if (!psf || !X || !Y) return fail(KB_ERR_ARGUMENT, "null pointer");
+  if (m < 1 || n < 1 || batch < 1) return fail(KB_ERR_ARGUMENT, "invalid image shape");
+  if (rows < 1 || cols < 1) return fail(KB_ERR_ARGUMENT, "PSF must be a nonempty 2-D array");
+  if (rows > m || cols > n)
+    return fail(KB_ERR_ARGUMENT, "PSF of shape (" + std::to_string(rows) + ", " + std::to_string(cols) +
+                                     ") larger than image (" + std::to_string(m) + ", " + std::to_string(n) + ")");
+  // (l, q) may lie outside a PSF whose all-zero borders the caller cropped (blur.py); the
+  // extension stays a single fold as long as the uncropped PSF fits the image
+  if (l < 1 - m || l > rows + m || q < 1 - n || q > cols + n) return fail(KB_ERR_ARGUMENT, "PSF center too far outside the array");
+  if (bc != KB_BC_ZERO && bc != KB_BC_REFLECTIVE) return fail(KB_ERR_ARGUMENT, "unknown boundary condition");
+  if (psf_batch_stride < 0) return fail(KB_ERR_ARGUMENT, "negative PSF batch stride");
+  const size_t img = (size_t)m * n * sizeof(double) * batch;
+  const char* xb = reinterpret_cast<const char*>(X);
+  const char* yb = reinterpret_cast<const char*>(Y);
+  if (xb < yb + img && yb < xb + img) return fail(KB_ERR_ARGUMENT, "X and Y overlap");
+  const size_t smem = kb::kb_blur_smem(cols);
+  KB_TRY(allow_smem(kb::kb_blur_direct_k, smem));
+  dim3 grid((n + kb::kBlTW - 1) / kb::kBlTW, (m + kb::kBlTH - 1) / kb::kBlTH, batch);
+  kb::kb_blur_direct_k<<<grid, kb::kBlThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+      psf, psf_batch_stride, rows, cols, l, q, X, Y, m, n, bc == KB_BC_REFLECTIVE);
+  KB_CUDA(cudaGetLastError());
+  return KB_OK;
 }
 
 int kb_fma_peak(int dtype, float* tflops, void* stream) {

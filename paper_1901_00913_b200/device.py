@@ -64,6 +64,11 @@ EXPORTS = {
     "kb_apply_block": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
     "kb_block_residual": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
     "kb_fma_peak": (_c_int, [_c_int, ctypes.POINTER(ctypes.c_float), _vp]),
+    "kb_blur_direct": (
+        _c_int,
+        [_vp, ctypes.c_longlong, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _c_int,
+         _c_int, _vp],
+    ),
     "kb_debug_trace": (_c_int, [ctypes.POINTER(ctypes.c_ulonglong), _c_int]),
     "kb_last_engines": (_c_int, [_vp, ctypes.POINTER(ctypes.c_int)]),
     "kb_time_passes": (

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import importlib
 
+from . import blur as _blur
 from . import kron as _kron
 from . import solvers as _solvers
 
@@ -20,6 +21,8 @@ PATCH_SITES = {
     "kron_apply": ("", "kron", "solvers", "pipeline"),
     "kron_apply_adjoint": ("", "kron", "solvers", "pipeline"),
     "estimate_lipschitz": ("", "solvers", "pipeline"),
+    # exact blur (psf.py:170-193): by-name imports in pipeline.py:26 and imaging.py:26
+    "blur_direct": ("", "psf", "pipeline", "imaging"),
 }
 
 
@@ -44,6 +47,7 @@ def install(kronblur_module=None, options: _solvers.SolveOptions | None = None):
         "kron_apply": _kron.kron_apply,
         "kron_apply_adjoint": _kron.kron_apply_adjoint,
         "estimate_lipschitz": _solvers.estimate_lipschitz,
+        "blur_direct": _blur.blur_direct,
     }
     saved = []
     for name, mods in PATCH_SITES.items():

@@ -161,10 +161,16 @@ def make_psf(cfg: Config, index: int = 0, seed: int = 0) -> Psf:
 
 # ------------------------------------------------------------------------------ data
 def blur_exact(X, psf: Psf, bc: str):
-    """blur_direct (psf.py:170-193) for a torch float64 image: symmetric / zero padding, then a
-    correlation with the flipped PSF (torch conv2d; setup only)."""
+    """blur_direct (psf.py:170-193) for a torch float64 image. On the GPU this is the native
+    kb_blur_direct kernel (bit-identical to the reference); CPU tensors (CPU-only tests of this
+    harness) take symmetric / zero padding plus a torch conv2d correlation with the flipped PSF."""
     import torch
     import torch.nn.functional as F
+
+    if X.is_cuda:
+        from .blur import blur_direct
+
+        return blur_direct(psf, X, bc)
 
     rows, cols = psf.values.shape
     l, q = psf.center

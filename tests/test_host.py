@@ -235,6 +235,10 @@ def test_install_patches_every_by_name_binding(monkeypatch):
         assert pipeline.estimate_lipschitz is kb.estimate_lipschitz
         assert pipeline.kron_apply is kb.kron_apply and solvers.kron_apply is kb.kron_apply
         assert kronblur.kron_apply_adjoint is kb.kron_apply_adjoint
+        from kronblur import imaging, psf as ref_psf
+
+        for mod in (kronblur, ref_psf, pipeline, imaging):
+            assert mod.blur_direct is kb.blur_direct
     finally:
         undo()
     assert (solvers.sfista, pipeline.sfista, pipeline.estimate_lipschitz, pipeline.kron_apply) == orig
