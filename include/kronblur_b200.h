@@ -133,6 +133,17 @@ int kb_blur_direct(const double* psf, long long psf_batch_stride, int rows, int 
                    const double* X, double* Y, int m, int n, int batch, int bc, void* stream);
 
 /*
+ * History reductions of one sFISTA iteration with record_history (solvers.py:133-141, :181):
+ * out2 (device double[2]) = { ||AX - B||^2, ||X - truth||^2 } over `count` elements of dtype
+ * (truth may be NULL: out2[1] = 0). With ||x_k||^2 from kb_sfista_run's norms this gives the
+ * objective 1/2 ||A x - b||^2 + lam^2/2 ||x||^2 and eta. work: device scratch of at least
+ * KB_RESID_NORMS_WORK bytes. Deterministic (fixed reduction order), fp64 accumulation.
+ */
+#define KB_RESID_NORMS_WORK (2 * 8 * 296)
+int kb_resid_norms(int dtype, const void* AX, const void* B, const void* X, const void* truth,
+                   long long count, double* out2, void* work, void* stream);
+
+/*
  * Measurement helpers used by bench.py (no reference counterpart).
  * kb_fma_peak: measured throughput (TFLOP/s) of the arithmetic instruction the pass kernels issue
  * for dtype - FP64 tensor-core DMMA (m8n8k4) for KB_F64, TF32 tensor-core mma.sync (m16n8k8)

@@ -25,6 +25,7 @@
 #include "kb_tf32.cuh"
 #include "kb_tc.cuh"
 #include "kb_blur.cuh"
+#include "kb_norms.cuh"
 
 namespace {
 
@@ -1339,6 +1340,26 @@ int kb_blur_direct(const double* psf, long long psf_batch_stride, int rows, int 
   dim3 grid((n + kb::kBlTW - 1) / kb::kBlTW, (m + kb::kBlTH - 1) / kb::kBlTH, batch);
   kb::kb_blur_direct_k<<<grid, kb::kBlThreads, smem, static_cast<cudaStream_t>(stream)>>>(
       psf, psf_batch_stride, rows, cols, l, q, X, Y, m, n, bc == KB_BC_REFLECTIVE);
+  KB_CUDA(cudaGetLastError());
+  return KB_OK;
+}
+
+int kb_resid_norms(int dtype, const void* AX, const void* B, const void* X, const void* truth,
+                   long long count, double* out2, void* work, void* stream) {
+  if (!AX || !B || !out2 || !work || (truth && !X) || count < 0)
+    return fail(KB_ERR_ARGUMENT, "bad kb_resid_norms arguments");
+  if (dtype != KB_F64 && dtype != KB_F32) return fail(KB_ERR_ARGUMENT, "unknown dtype");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* partial = static_cast<double*>(work);
+  if (dtype == KB_F64)
+    kb::kb_resid_norms_k<double><<<kb::kNormBlocks, kb::kNormThreads, 0, s>>>(
+        static_cast<const double*>(AX), static_cast<const double*>(B), static_cast<const double*>(X),
+        static_cast<const double*>(truth), count, partial);
+  else
+    kb::kb_resid_norms_k<float><<<kb::kNormBlocks, kb::kNormThreads, 0, s>>>(
+        static_cast<const float*>(AX), static_cast<const float*>(B), static_cast<const float*>(X),
+        static_cast<const float*>(truth), count, partial);
+  kb::kb_resid_norms_finish<<<1, 32, 0, s>>>(partial, kb::kNormBlocks, out2);
   KB_CUDA(cudaGetLastError());
   return KB_OK;
 }

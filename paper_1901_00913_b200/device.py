@@ -29,6 +29,7 @@ KB_PEAK_TC_TF32 = 2
 # pass engines (kb_last_engines)
 ENGINES = {0: "generic", 1: "ffma", 2: "dmma", 3: "mma_tf32", 4: "tcgen05_tf32"}
 KB_BC_ZERO, KB_BC_REFLECTIVE = 0, 1
+KB_RESID_NORMS_WORK = 2 * 8 * 296  # include/kronblur_b200.h
 INT_MAX = 2**31 - 1
 
 # Band trimming threshold relative to max|c|: removes the ~1e-16 leakage that the reference's
@@ -64,6 +65,7 @@ EXPORTS = {
     "kb_apply_block": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
     "kb_block_residual": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
     "kb_fma_peak": (_c_int, [_c_int, ctypes.POINTER(ctypes.c_float), _vp]),
+    "kb_resid_norms": (_c_int, [_c_int, _vp, _vp, _vp, _vp, ctypes.c_longlong, _vp, _vp, _vp]),
     "kb_blur_direct": (
         _c_int,
         [_vp, ctypes.c_longlong, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _c_int,
@@ -214,6 +216,7 @@ class DeviceOperator:
         self.work = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self.lock = threading.Lock()
         self._stage = {}
+        self._norm_work = None
 
     def info(self) -> dict:
         """Device layout facts (kb_op_info)."""
@@ -260,6 +263,19 @@ class DeviceOperator:
         _check(fn(self._handle, _ptr(X), _ptr(out), _ptr(self.work), _stream_handle()),
                "kb_apply_adjoint" if adjoint else "kb_apply")
         return out
+
+    def resid_norms(self, AX, B, X, truth, out2):
+        """out2 (device double[2]) = ||AX - B||^2, ||X - truth||^2 (kb_resid_norms; truth may be None)."""
+        torch = _torch()
+        if self._norm_work is None:
+            self._norm_work = torch.empty(KB_RESID_NORMS_WORK // 8, dtype=torch.float64, device=self.device)
+        AX, B, X = self._as_plane(AX, "AX"), self._as_plane(B, "data"), self._as_plane(X, "x")
+        if truth is not None:
+            truth = self._as_plane(truth, "truth")
+        rc = load_library().kb_resid_norms(
+            _code(self.dtype), _ptr(AX), _ptr(B), _ptr(X), _ptr(truth) if truth is not None else None,
+            int(AX.numel()), _ptr(out2), _ptr(self._norm_work), _stream_handle())
+        _check(rc, "kb_resid_norms")
 
     def sfista_run(self, B, X, Y, beta: np.ndarray, k0: int, iters: int, L, lam: float,
                    project: bool, nonfinite, norms=None, use_graph: bool = False):

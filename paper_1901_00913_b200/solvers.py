@@ -290,39 +290,65 @@ def sfista(op, B, cfg: SolveConfig, X0=None, truth=None, exact_apply=None, *,
             x = hX.numpy().astype(np.float64, copy=True)
             return SolveRun(x=x, iterations=K, solve_ms=float(start.elapsed_time(stop)))
 
+        # History / iterate / rel_tol path, one native iteration per step. Per iteration k the
+        # device holds hist[k-1] = (||x_k - x_{k-1}||^2, ||x_{k-1}||^2, ||x_k||^2, -, from the
+        # update epilogue; ||A x_k - b||^2, ||x_k - truth||^2 from one extra forward application
+        # plus kb_resid_norms). Nothing comes back to the host per iteration unless a host-side
+        # quantity needs it (rel_tol stopping, record_iterates, a host exact_apply callable);
+        # otherwise one synchronisation at the end. solve_ms / ms time only the iteration's own
+        # kernels (solvers.py:169-174), bracketed by events on the stream.
         norm_b = _norm(B)
         norm_truth = _norm(truth) if truth is not None else 0.0
-        norms = torch.zeros((1, 4, 1), dtype=torch.float64, device=dev.device)
-        history, iterates = [], []
-        elapsed = 0.0
+        hist = torch.zeros((K, 8), dtype=torch.float64, device=dev.device)
+        truth_d = None
+        if cfg.record_history and truth is not None:
+            truth_d = torch.from_numpy(np.ascontiguousarray(truth, dtype=np.float64)).to(dev.device, dev.tdtype)
+        Ax = dev.staging("ax") if cfg.record_history else None
+        per_iter_host = cfg.rel_tol > 0 or cfg.record_iterates or (cfg.record_history and exact_apply is not None)
+        marks = []
+        gammas, iterates = [], []
         iterations = 0
         for k in range(1, K + 1):
-            start.record(stream)
-            dev.sfista_run(Bd, Xd, Yd, beta, k - 1, 1, L, lam, opts.project, flag, norms=norms,
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dev.sfista_run(Bd, Xd, Yd, beta, k - 1, 1, L, lam, opts.project, flag, norms=hist[k - 1, :4],
                            use_graph=False)
-            stop.record(stream)
-            stop.synchronize()
-            elapsed += float(start.elapsed_time(stop))
+            e1.record(stream)
+            marks.append((e0, e1))
+            if cfg.record_history:
+                dev.apply(Xd, out=Ax)
+                dev.resid_norms(Ax, Bd, Xd, truth_d, hist[k - 1, 4:6])
+            iterations = k
+            if not per_iter_host:
+                continue
+            e1.synchronize()
             if int(flag.item()) <= k:
                 raise NumericError(f"non-finite iterate at iteration {k}")
-            iterations = k
-            nr = norms[0, :, 0].cpu().numpy()
-            step, base = float(np.sqrt(nr[0])), float(np.sqrt(nr[1]))
-            if cfg.record_history or cfg.record_iterates:
+            if cfg.record_iterates or (cfg.record_history and exact_apply is not None):
                 x = _host(Xd)
+                if cfg.record_iterates:
+                    iterates.append(x.copy())
+                if cfg.record_history and exact_apply is not None:
+                    gammas.append(_norm(exact_apply(x) - B) / norm_b if norm_b > 0 else None)
+            if cfg.rel_tol > 0:
+                step, base = np.sqrt(hist[k - 1, :2].cpu().numpy())
+                if step < cfg.rel_tol * (base if base > 0 else 1.0):
+                    break
+        torch.cuda.current_stream().synchronize()
+        bad = int(flag.item())
+        if bad <= iterations:
+            raise NumericError(f"non-finite iterate at iteration {bad}")
+        h = hist[:iterations].cpu().numpy()
+        elapsed, history = 0.0, []
+        for k in range(1, iterations + 1):
+            elapsed += float(marks[k - 1][0].elapsed_time(marks[k - 1][1]))
             if cfg.record_history:
-                Ax = _host(dev.apply(Xd))
-                eta = _norm(x - truth) / norm_truth if truth is not None and norm_truth > 0 else None
-                gamma = (_norm(exact_apply(x) - B) / norm_b
-                         if exact_apply is not None and norm_b > 0 else None)
-                r = Ax - B
-                phi = 0.5 * float(np.dot(r.ravel(), r.ravel())) + 0.5 * lam**2 * float(np.dot(x.ravel(), x.ravel()))
+                r2, x2, e2 = h[k - 1, 4], h[k - 1, 2], h[k - 1, 5]
+                phi = 0.5 * float(r2) + 0.5 * lam**2 * float(x2)
+                eta = float(np.sqrt(e2)) / norm_truth if truth is not None and norm_truth > 0 else None
+                gamma = gammas[k - 1] if exact_apply is not None else None
                 history.append(IterationRecord(k=k, t=float(ts[k - 1]), objective=phi, eta=eta,
                                                gamma=gamma, ms=elapsed))
-            if cfg.record_iterates:
-                iterates.append(x.copy())
-            if cfg.rel_tol > 0 and step < cfg.rel_tol * (base if base > 0 else 1.0):
-                break
         return SolveRun(x=_host(Xd), iterations=iterations, solve_ms=elapsed, history=history,
                         iterates=iterates)
 
