@@ -187,7 +187,10 @@ __device__ __forceinline__ void kb_fill_tile(T* __restrict__ xs, const T* __rest
 //        group's sign (adjoint of (anti)symmetric generators: see kb_capi.cu)
 // nw2  : optional per-image ||in||^2; outputs are divided by sqrt(nw2) (power iteration)
 // ------------------------------------------------------------------------------------------
-constexpr int kMaxGroups = 16;
+#ifndef KB_MAX_GROUPS
+#define KB_MAX_GROUPS 160
+#endif
+constexpr int kMaxGroups = KB_MAX_GROUPS;  // up to 318 (fp64) / 636 (fp32) terms: full-rank restore() operators
 struct Groups {
   int n;
   int start[kMaxGroups];

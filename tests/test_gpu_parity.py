@@ -340,3 +340,25 @@ def test_misaligned_device_buffers(dtype):
         assert rel(got, want) <= tol
         dev.apply(xa, out=ov, adjoint=adjoint)  # aligned operand, misaligned result
         assert rel(ov.double().cpu().numpy(), want) <= tol
+
+
+# ----------------------------------------------------------------- full-rank operators
+@pytest.mark.parametrize("bc", [ZERO, REFL])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_full_rank_operator_matches_oracle(rng, bc, dtype):
+    """restore(s=None) decomposes the padded PSF at full rank (pipeline.py:169, rank up to the PSF
+    size): 41 terms here, beyond the BASELINE r <= 10 configs."""
+    psf = random_psf(rng, 41)
+    op = kb.decompose(psf, bc, shape=(96, 96))
+    assert len(op.terms) == 41
+    pop = port.PortOperator(op)
+    X = rng.standard_normal((96, 96))
+    tol = 1e-12 if dtype == "float64" else 1e-5
+    if dtype == "float64":
+        assert rel(kb.kron_apply(op, X), port.kron_apply(pop, X)) <= tol
+        assert rel(kb.kron_apply_adjoint(op, X), port.kron_apply_adjoint(pop, X)) <= tol
+    B = port.kron_apply(pop, np.abs(X))
+    cfg = kb.SolveConfig(lam=0.05, lipschitz=1.05, max_iter=20, record_history=False)
+    run = kb.sfista(op, B, cfg, options=kb.SolveOptions(dtype=dtype))
+    want, _ = port.sfista(op, B, 1.05, 0.05, 20)
+    assert rel(run.x, want) <= (1e-10 if dtype == "float64" else 1e-4)
