@@ -91,6 +91,11 @@ int kb_apply_adjoint(const kb_op* op, const void* Y, void* X, void* work, void* 
 int kb_sfista_run(const kb_op* op, const void* B, void* X, void* Y, void* work,
                   const double* beta, int k0, int iters, const double* L, double lam,
                   int project, int* nonfinite, double* norms, int use_graph, void* stream);
+/* kb_sfista_run with a per-image lam (host array [batch]): the batched lambda probes of
+ * select_lambda (solvers.py:294-305), one image per candidate lambda. */
+int kb_sfista_run_lams(const kb_op* op, const void* B, void* X, void* Y, void* work,
+                       const double* beta, int k0, int iters, const double* L, const double* lam,
+                       int project, int* nonfinite, double* norms, int use_graph, void* stream);
 
 /*
  * Power iteration of solvers.py:104-130 on A^T A: v (device, normalised start vector drawn on

@@ -32,6 +32,7 @@ from .solvers import (
     momentum_table,
     objective,
     objective_matrix,
+    select_lambda,
     sfista,
     sfista_batch,
 )

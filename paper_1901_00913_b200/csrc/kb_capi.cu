@@ -1237,9 +1237,32 @@ int kb_block_update(const kb_op* op, const void* Rh, void* X, void* Y, void* wor
   return update_t<float>(op, static_cast<const float*>(Rh), static_cast<float*>(X), static_cast<float*>(Y), w, RowBlock{g0, m_global, halo_lo, halo_hi}, beta, k, w.scal, w.scal + 1, project, nonfinite, nullptr, s);
 }
 
+namespace {
+int sfista_run_impl(const kb_op* op, const void* B, void* X, void* Y, void* work, const double* beta, int k0,
+                    int iters, const double* L, const double* lam, int lam_per_image, int project,
+                    int* nonfinite, double* norms, int use_graph, void* stream);
+}  // namespace
+
 int kb_sfista_run(const kb_op* op, const void* B, void* X, void* Y, void* work,
                   const double* beta, int k0, int iters, const double* L, double lam,
                   int project, int* nonfinite, double* norms, int use_graph, void* stream) {
+  return sfista_run_impl(op, B, X, Y, work, beta, k0, iters, L, &lam, 0, project, nonfinite, norms, use_graph,
+                         stream);
+}
+
+int kb_sfista_run_lams(const kb_op* op, const void* B, void* X, void* Y, void* work,
+                       const double* beta, int k0, int iters, const double* L, const double* lam,
+                       int project, int* nonfinite, double* norms, int use_graph, void* stream) {
+  if (!lam) return fail(KB_ERR_ARGUMENT, "null argument");
+  return sfista_run_impl(op, B, X, Y, work, beta, k0, iters, L, lam, 1, project, nonfinite, norms, use_graph,
+                         stream);
+}
+}  // extern "C"
+
+namespace {
+int sfista_run_impl(const kb_op* op, const void* B, void* X, void* Y, void* work, const double* beta, int k0,
+                    int iters, const double* L, const double* lam, int lam_per_image, int project,
+                    int* nonfinite, double* norms, int use_graph, void* stream) {
   KB_TRY(check_op(op));
   if (!B || !X || !Y || !work || !beta || !L || !nonfinite) return fail(KB_ERR_ARGUMENT, "null argument");
   if (iters < 0 || k0 < 0) return fail(KB_ERR_ARGUMENT, "iters and k0 must be >= 0");
@@ -1248,8 +1271,9 @@ int kb_sfista_run(const kb_op* op, const void* B, void* X, void* Y, void* work,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   std::vector<double> host(2 * (size_t)op->batch);
   for (int b = 0; b < op->batch; ++b) {
+    const double lb = lam[lam_per_image ? b : 0];
     host[b] = L[b];
-    host[op->batch + b] = L[b] + lam * lam;
+    host[op->batch + b] = L[b] + lb * lb;
   }
   KB_CUDA(cudaMemcpyAsync(w.scal, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice, s));
   // cudaMemcpyAsync from pageable memory returns after staging, so `host` may go out of scope.
@@ -1306,6 +1330,9 @@ int kb_sfista_run(const kb_op* op, const void* B, void* X, void* Y, void* work,
   KB_CUDA(cudaGraphLaunch(gc->exec, s));
   return KB_OK;
 }
+}  // namespace
+
+extern "C" {
 
 int kb_power_iter(const kb_op* op, void* v, void* wb, void* work, int iters, double* hist,
                   void* stream) {

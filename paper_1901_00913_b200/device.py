@@ -61,6 +61,11 @@ EXPORTS = {
         [_vp, _vp, _vp, _vp, _vp, _c_dp, _c_int, _c_int, _c_dp, _c_double, _c_int, _vp, _vp,
          _c_int, _vp],
     ),
+    "kb_sfista_run_lams": (
+        _c_int,
+        [_vp, _vp, _vp, _vp, _vp, _c_dp, _c_int, _c_int, _c_dp, _c_dp, _c_int, _vp, _vp,
+         _c_int, _vp],
+    ),
     "kb_power_iter": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _vp, _vp]),
     "kb_apply_block": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
     "kb_block_residual": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
@@ -277,6 +282,22 @@ class DeviceOperator:
             int(AX.numel()), _ptr(out2), _ptr(self._norm_work), _stream_handle())
         _check(rc, "kb_resid_norms")
 
+    def resid_norms_images(self, AX, B) -> np.ndarray:
+        """||AX[k] - B[k]||^2 per image of a batched plane (kb_resid_norms per image)."""
+        torch = _torch()
+        AX, B = self._as_plane(AX, "AX"), self._as_plane(B, "data")
+        if self._norm_work is None:
+            self._norm_work = torch.empty(KB_RESID_NORMS_WORK // 8, dtype=torch.float64, device=self.device)
+        out = torch.zeros((self.batch, 2), dtype=torch.float64, device=self.device)
+        ax, bb = AX.reshape(self.batch, -1), B.reshape(self.batch, -1)
+        lib = load_library()
+        for k in range(self.batch):
+            rc = lib.kb_resid_norms(_code(self.dtype), _ptr(ax[k]), _ptr(bb[k]), None, None,
+                                    int(self.m * self.n), _ptr(out[k]), _ptr(self._norm_work),
+                                    _stream_handle())
+            _check(rc, "kb_resid_norms")
+        return out[:, 0].cpu().numpy()
+
     def sfista_run(self, B, X, Y, beta: np.ndarray, k0: int, iters: int, L, lam: float,
                    project: bool, nonfinite, norms=None, use_graph: bool = False):
         """Native loop of `iters` sFISTA iterations (kb_sfista_run)."""
@@ -287,13 +308,20 @@ class DeviceOperator:
         Ls = np.ascontiguousarray(np.broadcast_to(np.asarray(L, dtype=np.float64), (self.batch,)))
         if beta.size < k0 + iters:
             raise ArgumentError("momentum table shorter than the iteration range")
-        rc = load_library().kb_sfista_run(
+        if np.ndim(lam) == 0:
+            fn, lam_arg, what = load_library().kb_sfista_run, float(lam), "kb_sfista_run"
+        else:  # one lambda per image (select_lambda's batched probes)
+            lams = np.ascontiguousarray(lam, dtype=np.float64)
+            if lams.shape != (self.batch,):
+                raise ArgumentError(f"{lams.size} lambdas for a batch of {self.batch}")
+            fn, lam_arg, what = load_library().kb_sfista_run_lams, lams.ctypes.data_as(_c_dp), "kb_sfista_run_lams"
+        rc = fn(
             self._handle, _ptr(B), _ptr(X), _ptr(Y), _ptr(self.work), beta.ctypes.data_as(_c_dp),
-            int(k0), int(iters), Ls.ctypes.data_as(_c_dp), float(lam), int(bool(project)),
+            int(k0), int(iters), Ls.ctypes.data_as(_c_dp), lam_arg, int(bool(project)),
             _ptr(nonfinite), _ptr(norms) if norms is not None else None, int(bool(use_graph)),
             _stream_handle(),
         )
-        _check(rc, "kb_sfista_run")
+        _check(rc, what)
 
     def time_passes(self, Y, B, L: float, lam: float, reps: int = 20) -> list:
         """Average device ms of the four kernels of one iteration (kb_time_passes)."""

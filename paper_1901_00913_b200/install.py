@@ -23,6 +23,8 @@ PATCH_SITES = {
     "estimate_lipschitz": ("", "solvers", "pipeline"),
     # exact blur (psf.py:170-193): by-name imports in pipeline.py:26 and imaging.py:26
     "blur_direct": ("", "psf", "pipeline", "imaging"),
+    # lambda selection (solvers.py:255-306): by-name import in pipeline.py:33
+    "select_lambda": ("", "solvers", "pipeline"),
 }
 
 
@@ -48,6 +50,7 @@ def install(kronblur_module=None, options: _solvers.SolveOptions | None = None):
         "kron_apply_adjoint": _kron.kron_apply_adjoint,
         "estimate_lipschitz": _solvers.estimate_lipschitz,
         "blur_direct": _blur.blur_direct,
+        "select_lambda": _solvers.select_lambda,
     }
     saved = []
     for name, mods in PATCH_SITES.items():

@@ -353,6 +353,81 @@ def sfista(op, B, cfg: SolveConfig, X0=None, truth=None, exact_apply=None, *,
                         iterates=iterates)
 
 
+LAMBDA_DENSE_LIMIT = 1024  # solvers.py:47
+LAMBDA_PROBE_TERMS = 5     # solvers.py:50
+
+
+def select_lambda(op, B, noise_level: float, lipschitz: float, grid_points: int = 25,
+                  probe_iters: int = 50) -> float:
+    """Discrepancy-principle lambda over the reference's log grid (solvers.py:255-306).
+
+    Same validation, grid, target and argmin. Small problems (m n <= LAMBDA_DENSE_LIMIT) take the
+    reference's dense eigendecomposition route unchanged (host setup on <= 1024 unknowns). Larger
+    ones run the fixed sFISTA probes — 25 independent 50-iteration solves on the truncated
+    operator, one per candidate lambda — as ONE batched device solve (one image per lambda,
+    kb_sfista_run_lams; the batched cfg3 kernels), then one batched forward application and the
+    per-image residual norms on the device, instead of 25 sequential solves."""
+    from .kron import kron_to_dense
+    from .psf import vec
+
+    B = np.asarray(B, dtype=float)
+    if B.shape != tuple(op.shape):
+        raise ArgumentError(f"data shape {B.shape} does not match operator shape {tuple(op.shape)}")
+    if not (np.isfinite(noise_level) and noise_level >= 0):
+        raise ArgumentError(f"noise level must be >= 0, got {noise_level}")
+    if not (np.isfinite(lipschitz) and lipschitz > 0):
+        raise ArgumentError(f"Lipschitz constant must be positive, got {lipschitz}")
+    scale = np.sqrt(lipschitz)
+    grid = np.geomspace(1e-4 * scale, scale, int(grid_points))
+    b = vec(B)
+    target = noise_level * np.linalg.norm(b)
+    m, n = op.shape
+    if m * n <= LAMBDA_DENSE_LIMIT:
+        A = kron_to_dense(op)
+        w, Q = np.linalg.eigh(A.T @ A)
+        z = Q.T @ (A.T @ b)
+        bb = float(b @ b)
+        residuals = np.empty(grid.size)
+        for i, lam in enumerate(grid):
+            xh = z / (w + lam**2)
+            residuals[i] = np.sqrt(max(bb - 2.0 * float(z @ xh) + float((w * xh) @ xh), 0.0))
+        return float(grid[int(np.argmin(np.abs(residuals - target)))])
+    residuals = lambda_probe_residuals(op.truncate(min(LAMBDA_PROBE_TERMS, len(op.terms))), B, grid,
+                                       lipschitz, int(probe_iters))
+    return float(grid[int(np.argmin(np.abs(residuals - target)))])
+
+
+def lambda_probe_residuals(probe, B, grid, lipschitz: float, iters: int) -> np.ndarray:
+    """||A_s x(lam) - B||_F of the 50-iteration sFISTA probe from X0 = 0 for every lam of the grid
+    (solvers.py:296-305), batched over the grid on the device (chunked to the free memory)."""
+    import torch
+
+    from .device import INT_MAX, DeviceOperator
+
+    m, n = probe.shape
+    _, beta = momentum_table(int(iters))
+    free = torch.cuda.mem_get_info()[0]
+    per_image = (len(probe.terms) + 8) * m * n * 8  # Z planes + halo, R, B, X, Y, AX (fp64)
+    chunk = int(max(1, min(len(grid), (free // 2) // per_image)))
+    out = np.empty(len(grid))
+    for c0 in range(0, len(grid), chunk):
+        lams = np.asarray(grid[c0:c0 + chunk], dtype=np.float64)
+        G = lams.size
+        dev = DeviceOperator([probe] * G, "float64")
+        Bd = torch.from_numpy(np.ascontiguousarray(B)).to(dev.device).expand(G, m, n).contiguous()
+        Xd = torch.zeros_like(Bd)
+        Yd = torch.zeros_like(Bd)
+        flag = torch.full((1,), INT_MAX, dtype=torch.int32, device=dev.device)
+        dev.sfista_run(Bd, Xd, Yd, beta, 0, int(iters), lipschitz, lams, False, flag, use_graph=False)
+        AX = dev.apply(Xd)
+        r2 = dev.resid_norms_images(AX, Bd)
+        bad = int(flag.item())
+        if bad <= iters:
+            raise NumericError(f"non-finite iterate at iteration {bad}")
+        out[c0:c0 + G] = np.sqrt(r2)
+    return out
+
+
 def sfista_batch(ops, B, lipschitz, lam: float, iters: int, *, options: SolveOptions | None = None,
                  X0=None):
     """Batch of independent solves (BASELINE cfg3): one batched operator, per-image L, shared lam

@@ -184,3 +184,16 @@ def test_port_blur_direct_reproduces_reference_bit_for_bit():
                 m, n = X.shape
                 for i, j in [(0, 0), (m - 1, n - 1), (0, n - 1)] + [tuple(rng.integers(0, (m, n))) for _ in range(5)]:
                     assert port.blur_direct_pixel(P, c, X, bc, i, j) == ref[i, j], (ci, bc, i, j)
+
+
+# ------------------------------------------------------------------ solvers.py select_lambda
+def test_port_select_lambda_reproduces_reference():
+    """Both routes (dense eigen, m n <= 1024; sFISTA probes otherwise) pick the reference's lambda."""
+    g = load("lambda.npz")
+    for ci in range(int(g["ncases"])):
+        psf = kb.Psf(g[f"l{ci}_psf"], tuple(int(v) for v in g[f"l{ci}_center"]))
+        B = g[f"l{ci}_B"]
+        noise, L = (float(v) for v in g[f"l{ci}_noise_L"])
+        op = kb.decompose(psf, kb.BoundaryCondition(str(g[f"l{ci}_bc"])), shape=B.shape)
+        lam, _ = port.select_lambda(op, B, noise, L)
+        assert lam == float(g[f"l{ci}_lam"]), ci
