@@ -249,7 +249,7 @@ def run_b200(args):
     units = cfg.batch if batched else world
     value = units * mpix_it / (ms / 1e3)
 
-    # ---- e2e: public API with host buffers (H2D of B and X0, D2H of x inside the region)
+    # ---- e2e: public API with host buffers (H2D of B, D2H of x inside the region; X0 = None)
     cfgsolve = kb.SolveConfig(lam=cfg.lam, lipschitz=float(np.max(L)), max_iter=iters, record_history=False)
     opts = kb.SolveOptions(dtype=args.dtype, project=True, use_graph=True)
     esz = 8 if args.dtype == "float64" else 4
@@ -275,7 +275,7 @@ def run_b200(args):
     e2e_s = max_over_ranks(sum(e2e_t) / len(e2e_t))
     nimg = len(ops)
     e2e = {"value": units * mpix_it / e2e_s, "unit": "Mpixel*iterations/s",
-           "h2d_bytes_per_step": (1 if batched else 2) * nimg * m * m * esz,
+           "h2d_bytes_per_step": nimg * m * m * esz,  # B (X0 = None is zeroed on the device)
            "d2h_bytes_per_step": nimg * m * m * esz}
 
     # ---- roofline of the dominant pass kernel (CUDA events on the launching stream)

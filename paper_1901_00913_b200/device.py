@@ -153,6 +153,44 @@ def _stream_handle():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+_PIECE_BYTES = 2 << 20  # host <-> device transfers move in 2 MiB pieces
+
+
+def upload_pieces(dst, src: np.ndarray, stage) -> None:
+    """dst (device tensor) <- src (host array) through the pinned staging tensor `stage` (same
+    element count): the host copy (and dtype conversion) of each piece overlaps the DMA of the
+    previous one on the current stream. The caller keeps `stage` untouched until the stream
+    has passed these copies (every public call synchronises before returning)."""
+    flat = np.ascontiguousarray(src).reshape(-1)
+    hs, hn, dflat = stage.view(-1), stage.view(-1).numpy(), dst.view(-1)
+    step = max(1, _PIECE_BYTES // stage.element_size())
+    for a in range(0, flat.size, step):
+        b = min(flat.size, a + step)
+        hn[a:b] = flat[a:b]
+        dflat[a:b].copy_(hs[a:b], non_blocking=True)
+
+
+def download_pieces(src, stage, out: np.ndarray) -> np.ndarray:
+    """out (host array) <- src (device tensor) through the pinned `stage`: every piece's DMA is
+    queued at once and each is copied (and converted) into `out` as soon as it has landed."""
+    torch = _torch()
+    sflat, hs, hn = src.view(-1), stage.view(-1), stage.view(-1).numpy()
+    oflat = out.reshape(-1)
+    step = max(1, _PIECE_BYTES // stage.element_size())
+    marks = []
+    stream = torch.cuda.current_stream()
+    for a in range(0, sflat.numel(), step):
+        b = min(sflat.numel(), a + step)
+        hs[a:b].copy_(sflat[a:b], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        marks.append((a, b, ev))
+    for a, b, ev in marks:
+        ev.synchronize()
+        oflat[a:b] = hn[a:b]
+    return out
+
+
 def _axis_bands(factors, tol: float):
     """Unified band (dlo, [batch*r, w] taps, kind) over one axis of all terms."""
     kinds = {kind_name(f) for f in factors}

@@ -247,15 +247,14 @@ def sfista(op, B, cfg: SolveConfig, X0=None, truth=None, exact_apply=None, *,
     """Accelerated solve of the matrix model against a KronOperator, on the B200."""
     import torch
 
-    from .device import INT_MAX, device_operator
+    from .device import INT_MAX, device_operator, download_pieces, upload_pieces
 
     opts = options or SolveOptions()
     B = np.asarray(B, dtype=float)
-    if X0 is None:
-        X0 = np.zeros_like(B)
-    X0 = np.array(X0, dtype=float)
-    if X0.shape != B.shape:
-        raise ArgumentError(f"x0 shape {X0.shape} does not match data shape {B.shape}")
+    if X0 is not None:  # None: x_0 = 0 (solvers.py:218-219), zeroed on the device
+        X0 = np.asarray(X0, dtype=float)
+        if X0.shape != B.shape:
+            raise ArgumentError(f"x0 shape {X0.shape} does not match data shape {B.shape}")
     if B.shape != tuple(op.shape):
         raise ArgumentError(f"image shape {B.shape} does not match operator shape {tuple(op.shape)}")
     K = int(cfg.max_iter)
@@ -269,10 +268,11 @@ def sfista(op, B, cfg: SolveConfig, X0=None, truth=None, exact_apply=None, *,
         stream = torch.cuda.current_stream()
         hB, hX = dev.staging("host_b", pinned=True), dev.staging("host_x", pinned=True)
         Bd, Xd, Yd = dev.staging("b"), dev.staging("x"), dev.staging("y")
-        hB.numpy()[...] = B
-        hX.numpy()[...] = X0
-        Bd.copy_(hB, non_blocking=True)
-        Xd.copy_(hX, non_blocking=True)
+        upload_pieces(Bd, B, hB)
+        if X0 is None:
+            Xd.zero_()
+        else:
+            upload_pieces(Xd, X0, hX)
         Yd.copy_(Xd)
         flag = torch.full((1,), INT_MAX, dtype=torch.int32, device=dev.device)
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -281,13 +281,11 @@ def sfista(op, B, cfg: SolveConfig, X0=None, truth=None, exact_apply=None, *,
             start.record(stream)
             dev.sfista_run(Bd, Xd, Yd, beta, 0, K, L, lam, opts.project, flag, use_graph=use_graph)
             stop.record(stream)
-            hX.copy_(Xd, non_blocking=True)
-            stop.synchronize()
+            x = download_pieces(Xd, hX, np.empty(B.shape))
             torch.cuda.current_stream().synchronize()
             bad = int(flag.item())
             if bad <= K:
                 raise NumericError(f"non-finite iterate at iteration {bad}")
-            x = hX.numpy().astype(np.float64, copy=True)
             return SolveRun(x=x, iterations=K, solve_ms=float(start.elapsed_time(stop)))
 
         # History / iterate / rel_tol path, one native iteration per step. Per iteration k the
@@ -434,13 +432,17 @@ def sfista_batch(ops, B, lipschitz, lam: float, iters: int, *, options: SolveOpt
     and momentum. B: (batch, m, n) numpy or CUDA tensor. Returns (x, solve_ms) with x like B."""
     import torch
 
-    from .device import INT_MAX, DeviceOperator
+    from .device import INT_MAX, DeviceOperator, download_pieces, upload_pieces
 
     opts = options or SolveOptions()
     dev = ops if isinstance(ops, DeviceOperator) else DeviceOperator(list(ops), opts.dtype)
     _, beta = momentum_table(int(iters))
     on_device = isinstance(B, torch.Tensor) and B.is_cuda
-    Bd = B.to(dev.tdtype).contiguous() if on_device else torch.from_numpy(np.ascontiguousarray(B)).to(dev.device, dev.tdtype)
+    if on_device:
+        Bd = B.to(dev.tdtype).contiguous()
+    else:  # host arrays move in pinned pieces (device.upload_pieces), converted on the way
+        Bd = dev.staging("b")
+        upload_pieces(Bd, np.asarray(B), dev.staging("host_b", pinned=True))
     if X0 is None:
         Xd = torch.zeros_like(Bd)
     else:
@@ -457,5 +459,5 @@ def sfista_batch(ops, B, lipschitz, lam: float, iters: int, *, options: SolveOpt
     bad = int(flag.item())
     if bad <= iters:
         raise NumericError(f"non-finite iterate at iteration {bad}")
-    x = Xd if on_device else _host(Xd)
+    x = Xd if on_device else download_pieces(Xd, dev.staging("host_x", pinned=True), np.empty(tuple(Xd.shape)))
     return x, float(start.elapsed_time(stop))
