@@ -153,41 +153,64 @@ def _stream_handle():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-_PIECE_BYTES = 2 << 20  # host <-> device transfers move in 2 MiB pieces
+_PIECE_BYTES = 1 << 20  # host <-> device transfers move in 1 MiB pieces
+_copy_pool = None
+
+
+def _pool():
+    """Host-copy workers: numpy releases the GIL for large contiguous copies, so the pieces'
+    host copies (and dtype conversions) run in parallel with each other and with the DMAs."""
+    global _copy_pool
+    if _copy_pool is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _copy_pool = ThreadPoolExecutor(max_workers=max(1, min(8, os.cpu_count() or 1)),
+                                        thread_name_prefix="kb-copy")
+    return _copy_pool
 
 
 def upload_pieces(dst, src: np.ndarray, stage) -> None:
     """dst (device tensor) <- src (host array) through the pinned staging tensor `stage` (same
-    element count): the host copy (and dtype conversion) of each piece overlaps the DMA of the
-    previous one on the current stream. The caller keeps `stage` untouched until the stream
-    has passed these copies (every public call synchronises before returning)."""
+    element count). Pieces are copied (and converted) into `stage` by the copy workers; each
+    piece's DMA is queued on the current stream as soon as its host copy is done. The caller
+    keeps `stage` untouched until the stream has passed these copies (every public call
+    synchronises before returning)."""
     flat = np.ascontiguousarray(src).reshape(-1)
     hs, hn, dflat = stage.view(-1), stage.view(-1).numpy(), dst.view(-1)
     step = max(1, _PIECE_BYTES // stage.element_size())
-    for a in range(0, flat.size, step):
-        b = min(flat.size, a + step)
+    spans = [(a, min(flat.size, a + step)) for a in range(0, flat.size, step)]
+
+    def put(a, b):
         hn[a:b] = flat[a:b]
+
+    futs = [_pool().submit(put, a, b) for a, b in spans]
+    for (a, b), f in zip(spans, futs):
+        f.result()
         dflat[a:b].copy_(hs[a:b], non_blocking=True)
 
 
 def download_pieces(src, stage, out: np.ndarray) -> np.ndarray:
     """out (host array) <- src (device tensor) through the pinned `stage`: every piece's DMA is
-    queued at once and each is copied (and converted) into `out` as soon as it has landed."""
+    queued at once; the copy workers move (and convert) each piece into `out` once it landed."""
     torch = _torch()
     sflat, hs, hn = src.view(-1), stage.view(-1), stage.view(-1).numpy()
     oflat = out.reshape(-1)
     step = max(1, _PIECE_BYTES // stage.element_size())
-    marks = []
     stream = torch.cuda.current_stream()
+    marks = []
     for a in range(0, sflat.numel(), step):
         b = min(sflat.numel(), a + step)
         hs[a:b].copy_(sflat[a:b], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(stream)
         marks.append((a, b, ev))
-    for a, b, ev in marks:
+
+    def get(a, b, ev):
         ev.synchronize()
         oflat[a:b] = hn[a:b]
+
+    for f in [_pool().submit(get, a, b, ev) for a, b, ev in marks]:
+        f.result()
     return out
 
 
