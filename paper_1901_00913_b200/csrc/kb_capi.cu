@@ -171,12 +171,15 @@ int tc_policy(int pass) {  // pass: 1 split, 2 sum
   }();
   return p < 0 ? -1 : (p & pass) ? 1 : 0;
 }
+int sm_count();
 bool use_tc(const kb_op* op, const kb::AxisGeom& g, int min_kw) {
   const int pol = tc_policy(min_kw == 64 ? 1 : 2);
   if (!use_tma_f32(op) || pol == 0) return false;
   if (pol == 1) return true;
   const long long chunks = (long long)((g.len + kb::kTcTS - 1) / kb::kTcTS) * ((g.other + 127) / 128) * op->batch;
-  return g.Kw >= min_kw && chunks >= 128;
+  // wide bands with enough chunks to occupy the SMs, or any band from 32 taps once there are
+  // >= 8 chunks per SM (cfg3's 512-image batch, cfg5's 16384^2: 2x the mma.sync passes there)
+  return (g.Kw >= min_kw && chunks >= 128) || (g.Kw >= 32 && chunks >= 8LL * sm_count());
 }
 // the brick table built from tap table `tin`, or null
 const unsigned* brick_table(const kb_op* op, const void* tin) {
@@ -835,7 +838,7 @@ int upload_tables(kb_op* op, int dlo, int w, const double* taps, const std::vect
 int build_brick_tables(kb_op* op, int H, int Wp, const void* conv, const void* corr, unsigned** bconv,
                        unsigned** bcorr) {
   const int Kw = (2 * H + 1 + 3) / 4 * 4;
-  if (Kw < 64 && tc_policy(3) != 1) return KB_OK;
+  if (Kw < 32 && tc_policy(3) != 1) return KB_OK;
   const int nbr = kb::tc_bricks(Kw);
   const long long bt = (long long)op->batch * op->r;
   const size_t bytes = (size_t)bt * nbr * 1024;

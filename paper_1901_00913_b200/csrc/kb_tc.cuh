@@ -85,6 +85,9 @@ __device__ __forceinline__ void mbar_wait_lazy(unsigned long long* bar, unsigned
       : "memory");
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 // mbarrier wait that sleeps between probes: for the roles that are never on the critical path
 // (the TMA producer waiting for a free ring stage, the epilogue waiting for a finished term),
 // so their polling does not take issue slots from the converter and MMA warps of the same SM
@@ -615,6 +618,9 @@ struct StrideWalk {
 // pass stored (TMA boxes over the padded planes) and add the adjoint's fold corrections in the
 // epilogue; epilogue operands move as 16-byte vectors per lane row.
 // ------------------------------------------------------------------------------------------
+#ifndef KB_TC_V8
+#define KB_TC_V8 1  // 256-bit epilogue loads / stores (sm_100: LDG/STG.256)
+#endif
 constexpr int kTcSumSlots = 4;                       // per-term accumulator slots (64 columns each)
 constexpr int kTcSumEpi = 8;                         // epilogue warps
 constexpr int kTcSumThreads = 32 * (kTcEpi + kTcSumEpi);
@@ -626,7 +632,11 @@ __device__ __forceinline__ void tc_sum_epi8(const float (&v)[8], const Epi<float
   float u[8], w[8];
   const bool full8 = cnt == 8;
   auto ld8 = [&](const float* a, float (&o)[8]) {
-    if (full8) {
+    if (full8 && KB_TC_V8 && !(reinterpret_cast<unsigned long long>(a + at) & 31)) {  // one 32-byte sector
+      asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=f"(o[0]), "=f"(o[1]), "=f"(o[2]), "=f"(o[3]), "=f"(o[4]), "=f"(o[5]), "=f"(o[6]), "=f"(o[7])
+                   : "l"(a + at));
+    } else if (full8) {
       const float4 p0 = *reinterpret_cast<const float4*>(a + at), p1 = *reinterpret_cast<const float4*>(a + at + 4);
       o[0] = p0.x, o[1] = p0.y, o[2] = p0.z, o[3] = p0.w, o[4] = p1.x, o[5] = p1.y, o[6] = p1.z, o[7] = p1.w;
     } else {
@@ -635,7 +645,11 @@ __device__ __forceinline__ void tc_sum_epi8(const float (&v)[8], const Epi<float
     }
   };
   auto st8 = [&](float* a, const float (&o)[8]) {
-    if (full8) {
+    if (full8 && KB_TC_V8 && !(reinterpret_cast<unsigned long long>(a + at) & 31)) {
+      asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(a + at), "f"(o[0]), "f"(o[1]), "f"(o[2]),
+                   "f"(o[3]), "f"(o[4]), "f"(o[5]), "f"(o[6]), "f"(o[7])
+                   : "memory");
+    } else if (full8) {
       *reinterpret_cast<float4*>(a + at) = make_float4(o[0], o[1], o[2], o[3]);
       *reinterpret_cast<float4*>(a + at + 4) = make_float4(o[4], o[5], o[6], o[7]);
     } else {
@@ -652,28 +666,31 @@ __device__ __forceinline__ void tc_sum_epi8(const float (&v)[8], const Epi<float
     for (int i = 0; i < 8; ++i) u[i] = __fsub_rn(v[i], u[i]);
     st8(e.out, u);
   } else if constexpr (MODE == EPI_UPDATE) {
+    // in place (u: y_k -> x_k, w: x_{k-1} -> y_{k+1}): the epilogue warps share the kernel's
+    // register budget with the sum[32] accumulators
     ld8(e.y, u);
     ld8(e.x, w);
-    float xv[8], yv[8];
+    const float beta = (float)e.beta;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const float a = __fsub_rn(__fmul_rn(Lb, u[i]), v[i]);
       const float q0 = __fmul_rn(a, rd);
-      xv[i] = fmaf(fmaf(-db, q0, a), rd, q0);
-      if (e.project) xv[i] = (xv[i] > 0.f || xv[i] != xv[i]) ? xv[i] : 0.f;
-      const float d = __fsub_rn(xv[i], w[i]);
-      yv[i] = __fadd_rn(xv[i], __fmul_rn((float)e.beta, d));
+      float x = fmaf(fmaf(-db, q0, a), rd, q0);
+      if (e.project) x = (x > 0.f || x != x) ? x : 0.f;
+      const float d = __fsub_rn(x, w[i]);
       if (i < cnt) {
-        bad |= !isfinite(xv[i]);
+        bad |= !isfinite(x);
         if (e.want_norms) {
           nrm[0] += (double)d * d;
           nrm[1] += (double)w[i] * w[i];
-          nrm[2] += (double)xv[i] * xv[i];
+          nrm[2] += (double)x * x;
         }
       }
+      u[i] = x;
+      w[i] = __fadd_rn(x, __fmul_rn(beta, d));
     }
-    st8(e.x, xv);
-    st8(e.y, yv);
+    st8(e.x, u);
+    st8(e.y, w);
   } else {  // EPI_POWER
     ld8(e.vin, u);
 #pragma unroll
@@ -896,6 +913,21 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
         norm_b = ch.b;
       }
       const bool live = 32 * hh < ch.cnt;
+#if !KB_TC_NO_PREFETCH
+      {  // this chunk's epilogue operand rows go to L2 now, while its r terms accumulate: the
+         // epilogue's own loads then wait for L2, not DRAM (short-band batches are bound by them)
+        const int lp = ch.lt * 128 + 32 * q + lane;
+        if (live && lp < g.other) {
+          const long long at = (long long)ch.b * e.bstride + (long long)lp * n + ch.s0 + 32 * hh;
+          if constexpr (MODE == EPI_RESID) prefetch_l2(e.bsub + at);
+          if constexpr (MODE == EPI_UPDATE) {
+            prefetch_l2(e.y + at);
+            prefetch_l2(e.x + at);
+          }
+          if constexpr (MODE == EPI_POWER) prefetch_l2(e.vin + at);
+        }
+      }
+#endif
       float sum[32];
       for (int term = 0; term < r; ++term, sl.advance(kTcSumSlots)) {
         mbar_wait_idle(&slot_full[sl.i], sl.phase, 2000);
