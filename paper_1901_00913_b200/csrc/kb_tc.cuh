@@ -913,6 +913,13 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
         norm_b = ch.b;
       }
       const bool live = 32 * hh < ch.cnt;
+      // the image's scalars, loaded now so their latency hides behind the term accumulation
+      double sc_L = 0.0, sc_d = 1.0;
+      if constexpr (MODE == EPI_UPDATE) {
+        sc_L = e.L[ch.b];
+        sc_d = e.denom[ch.b];
+      }
+      if constexpr (MODE == EPI_POWER) sc_L = e.vnw2 ? e.vnw2[ch.b] : 1.0;
 #if !KB_TC_NO_PREFETCH
       {  // this chunk's epilogue operand rows go to L2 now, while its r terms accumulate: the
          // epilogue's own loads then wait for L2, not DRAM (short-band batches are bound by them)
@@ -949,14 +956,8 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
       }
       const int l = ch.lt * 128 + 32 * q + lane;
       if (live && l < g.other && !(g.dbg & 2)) {
-        float Lb = 0.f, db = 1.f, rd = 1.f;
-        double vs = 1.0;
-        if constexpr (MODE == EPI_UPDATE) {
-          Lb = (float)e.L[ch.b];
-          db = (float)e.denom[ch.b];
-          rd = 1.f / db;
-        }
-        if constexpr (MODE == EPI_POWER) vs = e.vnw2 ? sqrt(e.vnw2[ch.b]) : 1.0;
+        const float Lb = (float)sc_L, db = (float)sc_d, rd = 1.f / db;
+        const double vs = MODE == EPI_POWER && e.vnw2 ? sqrt(sc_L) : 1.0;
         const long long row = (long long)ch.b * e.bstride + (long long)l * n + ch.s0 + 32 * hh;
         const bool fold_edge = e.foldH > 0 && (ch.s0 < e.foldH || ch.s0 + kTcTS > n - e.foldH);
 #pragma unroll
