@@ -69,12 +69,15 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, u
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-// Profiling timeline (KB_DEBUG_MODE bit 7): thread 0 of block b stamps %globaltimer into
-// kb_trace[kind][b][slot] (kind 0 split, 1 sum; read back with kb_debug_trace).
+// Profiling timeline (KB_DEBUG_MODE bit 7 in a -DKB_TRACE=1 build): thread 0 of block b stamps
+// %globaltimer into kb_trace[kind][b][slot] (kind 0 split, 1 sum; read back with kb_debug_trace).
+#ifndef KB_TRACE
+#define KB_TRACE 0
+#endif
 constexpr int kTraceBlocks = 1024;
 __device__ unsigned long long kb_trace[2][kTraceBlocks][8];
 __device__ __forceinline__ void kb_stamp(const AxisGeom& g, int kind, int slot) {
-  if ((g.dbg & 128) && threadIdx.x == 0 && threadIdx.y == 0 && blockIdx.x < kTraceBlocks) {
+  if (KB_TRACE && (g.dbg & 128) && threadIdx.x == 0 && threadIdx.y == 0 && blockIdx.x < kTraceBlocks) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     kb_trace[kind][blockIdx.x][slot] = t;

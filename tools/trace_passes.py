@@ -1,6 +1,7 @@
 """Per-block timeline of the fp64 pass kernels (KB_DEBUG_MODE bit 7, kb_debug_trace).
 
 usage: KB_DEBUG_MODE=128 python tools/trace_passes.py [m] [float64|float32]
+(from a -DKB_TRACE=1 build: tools/variant.sh trace -DKB_TRACE=1, run in tmp_variants/trace)
 Runs kb_apply (forward: split + plain sum) and one sFISTA iteration (last kernels: adjoint split
 + update sum) on cfg2 and prints, per kernel, the distribution over blocks of each stamp
 relative to the kernel's earliest start (us).
