@@ -71,6 +71,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, u
 }
 // Profiling timeline (KB_DEBUG_MODE bit 7 in a -DKB_TRACE=1 build): thread 0 of block b stamps
 // %globaltimer into kb_trace[kind][b][slot] (kind 0 split, 1 sum; read back with kb_debug_trace).
+#ifndef KB_DMMA_EARLY_SCALARS
+#define KB_DMMA_EARLY_SCALARS 1
+#endif
 #ifndef KB_TRACE
 #define KB_TRACE 0
 #endif
@@ -647,8 +650,7 @@ template <int MODE>
 __device__ __forceinline__ void kb_sum_epilogue_regs(const double (&D)[2][4][2], const AxisGeom& g,
                                                      const Epi<double>& e, const Chunk& ch,
                                                      int s_off, int ar, int ac, double (&nrm)[3],
-                                                     bool& bad) {
-  const EpiScalars sc = kb_epi_scalars<MODE>(e, ch.b);
+                                                     bool& bad, const EpiScalars& sc) {
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) {
     double u[4][2], w[4][2];
@@ -811,6 +813,10 @@ kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* 
       for (int j = 0; j < 4; ++j) D[mt][j][0] = D[mt][j][1] = 0.0;
     const bool active = s_off < ch.cnt;  // warp-uniform
     const bool two = s_off + 8 < ch.cnt;
+#if KB_DMMA_EARLY_SCALARS
+    // the image's epilogue scalars (and the reciprocal's division) now, off the chunk's tail
+    const EpiScalars sc = kb_epi_scalars<MODE>(e, ch.b);
+#endif
     for (int term = 0; term < r; ++term, ++t) {
       issue();
       const int st = t % kStages;
@@ -823,7 +829,10 @@ kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* 
       if (lane == 0) mbar_arrive(&empty[st]);
     }
     if (t == r) kb_stamp(g, 1, 4);
-    if (active && !(g.dbg & 2)) kb_sum_epilogue_regs<MODE>(D, g, e, ch, s_off, ar, ac, nrm, bad);
+#if !KB_DMMA_EARLY_SCALARS
+    const EpiScalars sc = kb_epi_scalars<MODE>(e, ch.b);
+#endif
+    if (active && !(g.dbg & 2)) kb_sum_epilogue_regs<MODE>(D, g, e, ch, s_off, ar, ac, nrm, bad, sc);
     if (t == r) kb_stamp(g, 1, 5);
   }
   if (norm_b >= 0) kb_warp_finish<MODE>(e, nrm, bad, norm_b, nslots, slot, lane);
