@@ -110,3 +110,28 @@ def test_full_size_operator_properties(name):
     assert float(torch.linalg.norm(ATY32 - ATY) / torch.linalg.norm(ATY)) <= 1e-5
     del d64, d32
     torch.cuda.empty_cache()
+
+
+def test_cfg3_style_batch_on_tensor_core_passes():
+    """A batch large enough for the >= 8 chunks-per-SM rule (160 x 256^2, cfg3's w = 31 band) runs
+    on the tcgen05 passes; sampled images match the per-image oracle at the fp32 tolerance."""
+    from paper_1901_00913_b200.device import DeviceOperator
+
+    cfg = W.CONFIGS["cfg3"]
+    m, nb, iters = 256, 160, 30
+    ops, Bs, Xs = [], [], []
+    for i in range(nb):
+        X, psf, B = W.make_image_data(cfg, seed=1, index=i, m=m, counts=(20, 10), device="cuda")
+        ops.append(kb.decompose(psf, kb.BoundaryCondition(cfg.bc), s=cfg.r, shape=(m, m)))
+        Bs.append(B.astype(np.float32).astype(np.float64))
+        Xs.append(X)
+    Ls = np.array([kb.lipschitz(op, iters=20, seed=0) for op in ops])
+    dev = DeviceOperator(ops, "float32")
+    B32 = torch.from_numpy(np.stack(Bs)).to("cuda", torch.float32)
+    dev.time_passes(B32, B32, Ls, cfg.lam, reps=1)
+    assert dev.last_engines() == ["tcgen05_tf32"] * 4
+    x, _ = kb.sfista_batch(dev, np.stack(Bs), Ls, cfg.lam, iters, options=kb.SolveOptions(project=True))
+    for i in (0, 77, nb - 1):
+        want, _ = port.sfista(ops[i], Bs[i], Ls[i], cfg.lam, iters, project=True)
+        assert rel(x[i], want) <= 1e-4
+        assert abs(psnr(x[i], Xs[i]) - psnr(want, Xs[i])) <= 0.01
