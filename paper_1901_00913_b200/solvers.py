@@ -250,27 +250,40 @@ def sfista(op, B, cfg: SolveConfig, X0=None, truth=None, exact_apply=None, *,
     from .device import INT_MAX, device_operator, download_pieces, upload_pieces
 
     opts = options or SolveOptions()
-    B = np.asarray(B, dtype=float)
+    fast = not cfg.record_history and not cfg.record_iterates and cfg.rel_tol == 0
+    # optional extension: CUDA tensors in skip the host copies on the fast path
+    # and x comes back as a float64 CUDA tensor; elsewhere they are brought to the host
+    on_device = isinstance(B, torch.Tensor) and B.is_cuda
+    if on_device and not fast:
+        B, on_device = B.detach().to("cpu", torch.float64).numpy(), False
+    if isinstance(X0, torch.Tensor) and not on_device:
+        X0 = X0.detach().to("cpu", torch.float64).numpy()
+    if not on_device:
+        B = np.asarray(B, dtype=float)
     if X0 is not None:  # None: x_0 = 0 (solvers.py:218-219), zeroed on the device
-        X0 = np.asarray(X0, dtype=float)
+        X0 = X0 if isinstance(X0, torch.Tensor) else np.asarray(X0, dtype=float)
         if X0.shape != B.shape:
             raise ArgumentError(f"x0 shape {X0.shape} does not match data shape {B.shape}")
-    if B.shape != tuple(op.shape):
-        raise ArgumentError(f"image shape {B.shape} does not match operator shape {tuple(op.shape)}")
+    if tuple(B.shape) != tuple(op.shape):
+        raise ArgumentError(f"image shape {tuple(B.shape)} does not match operator shape {tuple(op.shape)}")
     K = int(cfg.max_iter)
     L, lam = float(cfg.lipschitz), float(cfg.lam)
     ts, beta = momentum_table(K)
     dev = device_operator(op, opts.dtype)
-    fast = not cfg.record_history and not cfg.record_iterates and cfg.rel_tol == 0
     use_graph = opts.use_graph if opts.use_graph is not None else (fast and K >= 8)
 
     with dev.lock:
         stream = torch.cuda.current_stream()
         hB, hX = dev.staging("host_b", pinned=True), dev.staging("host_x", pinned=True)
         Bd, Xd, Yd = dev.staging("b"), dev.staging("x"), dev.staging("y")
-        upload_pieces(Bd, B, hB)
+        if on_device:
+            Bd.copy_(B)
+        else:
+            upload_pieces(Bd, B, hB)
         if X0 is None:
             Xd.zero_()
+        elif isinstance(X0, torch.Tensor):
+            Xd.copy_(X0)
         else:
             upload_pieces(Xd, X0, hX)
         Yd.copy_(Xd)
@@ -281,7 +294,7 @@ def sfista(op, B, cfg: SolveConfig, X0=None, truth=None, exact_apply=None, *,
             start.record(stream)
             dev.sfista_run(Bd, Xd, Yd, beta, 0, K, L, lam, opts.project, flag, use_graph=use_graph)
             stop.record(stream)
-            x = download_pieces(Xd, hX, np.empty(B.shape))
+            x = Xd.to(torch.float64, copy=True) if on_device else download_pieces(Xd, hX, np.empty(B.shape))
             torch.cuda.current_stream().synchronize()
             bad = int(flag.item())
             if bad <= K:

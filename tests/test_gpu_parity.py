@@ -362,3 +362,18 @@ def test_full_rank_operator_matches_oracle(rng, bc, dtype):
     run = kb.sfista(op, B, cfg, options=kb.SolveOptions(dtype=dtype))
     want, _ = port.sfista(op, B, 1.05, 0.05, 20)
     assert rel(run.x, want) <= (1e-10 if dtype == "float64" else 1e-4)
+
+
+def test_sfista_accepts_cuda_tensors(rng):
+    """Optional extension: device tensors in skip the host copies; same result."""
+    psf = random_psf(rng, 7)
+    op = kb.decompose(psf, REFL, s=3, shape=(64, 64))
+    B = rng.random((64, 64))
+    X0 = 0.1 * rng.random((64, 64))
+    cfg = kb.SolveConfig(lam=0.05, lipschitz=1.2, max_iter=20, record_history=False)
+    host = kb.sfista(op, B, cfg, X0=X0).x
+    dev = kb.sfista(op, torch.from_numpy(B).cuda(), cfg, X0=torch.from_numpy(X0).cuda()).x
+    assert isinstance(dev, torch.Tensor) and dev.is_cuda and dev.dtype == torch.float64
+    assert np.array_equal(dev.cpu().numpy(), host)
+    hist = kb.sfista(op, torch.from_numpy(B).cuda(), kb.SolveConfig(lam=0.05, lipschitz=1.2, max_iter=5))
+    assert isinstance(hist.x, np.ndarray) and len(hist.history) == 5
