@@ -527,7 +527,11 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
     CUtensorMap map;
     if (use_dmma(op) && persistent_ok && bps > 0 &&
         make_tmap(&map, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, tb.box_rows))
-      return op->last_engine = KB_ENGINE_DMMA, launch(kb::kb_pass_sum_dmma<MODE>, smem, bps, map);
+    {
+      op->last_engine = KB_ENGINE_DMMA;
+      if (MODE == kb::EPI_UPDATE && !e.want_norms) return launch(kb::kb_pass_sum_dmma<MODE, false>, smem, bps, map);
+      return launch(kb::kb_pass_sum_dmma<MODE>, smem, bps, map);
+    }
   } else {
     const unsigned* btab = brick_table(op, tin);
     if (btab && use_tc(op, g, 128) && persistent_ok) {
@@ -543,7 +547,7 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
       CUtensorMap mapt;
       if (nst >= 3 && nb * kb::kTcSumEpi <= sum_blocks(op) &&
           make_tmap(&mapt, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, kb::kTcRB, 4, 128)) {
-        auto kern = kb::kb_pass_sum_tc<MODE>;
+        auto kern = MODE == kb::EPI_UPDATE && !e.want_norms ? kb::kb_pass_sum_tc<MODE, false> : kb::kb_pass_sum_tc<MODE>;
         KB_TRY(allow_smem(kern, smem));
         if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // warps skip untouched images
           KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kTcSumEpi, s));

@@ -581,7 +581,7 @@ __device__ __forceinline__ void kb_epi_load(const AxisGeom& g, const Epi<double>
   }
 }
 
-template <int MODE>
+template <int MODE, bool NORMS = true>
 __device__ __forceinline__ void kb_epi_apply(const double (&D)[4][2], const AxisGeom& g, const Epi<double>& e,
                                              const EpiScalars& sc, const Chunk& ch, int so, int ar, int ac,
                                              const double (&u)[4][2], const double (&w)[4][2], double (&nrm)[3],
@@ -622,7 +622,7 @@ __device__ __forceinline__ void kb_epi_apply(const double (&D)[4][2], const Axis
         yv[i] = __dadd_rn(xv[i], __dmul_rn(e.beta, d));
         if (i == 0 || both) {
           bad |= !isfinite(xv[i]);
-          if (e.want_norms) {
+          if (NORMS && e.want_norms) {
             nrm[0] += d * d;
             nrm[1] += w[j][i] * w[j][i];
             nrm[2] += xv[i] * xv[i];
@@ -646,7 +646,7 @@ __device__ __forceinline__ void kb_epi_apply(const double (&D)[4][2], const Axis
 }
 
 // two S-tiles (the 16-row warps of kb_pass_sum_dmma): loads of a tile before its arithmetic
-template <int MODE>
+template <int MODE, bool NORMS = true>
 __device__ __forceinline__ void kb_sum_epilogue_regs(const double (&D)[2][4][2], const AxisGeom& g,
                                                      const Epi<double>& e, const Chunk& ch,
                                                      int s_off, int ar, int ac, double (&nrm)[3],
@@ -655,7 +655,7 @@ __device__ __forceinline__ void kb_sum_epilogue_regs(const double (&D)[2][4][2],
   for (int mt = 0; mt < 2; ++mt) {
     double u[4][2], w[4][2];
     kb_epi_load<MODE>(g, e, ch, s_off + 8 * mt, ar, ac, u, w);
-    kb_epi_apply<MODE>(D[mt], g, e, sc, ch, s_off + 8 * mt, ar, ac, u, w, nrm, bad);
+    kb_epi_apply<MODE, NORMS>(D[mt], g, e, sc, ch, s_off + 8 * mt, ar, ac, u, w, nrm, bad);
   }
 }
 
@@ -718,7 +718,9 @@ __device__ __forceinline__ void kb_sum_mma(double (&D)[2][4][2], const double* _
 // runs the fused epilogue from its registers. Norm partials are per warp:
 // partials[b][block*kNW + warp].
 // ------------------------------------------------------------------------------------------
-template <int MODE>
+// NORMS = false: the update epilogue without the history norm partials (fewer registers: the
+// norms' accumulators made the update kernel spill)
+template <int MODE, bool NORMS = true>
 __global__ void __launch_bounds__(32 * kNW, 2)
 kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* __restrict__ tin,
                  long long t_bs, AxisGeom g, Epi<double> e, int batch, int parts) {
@@ -832,7 +834,7 @@ kb_pass_sum_dmma(const __grid_constant__ CUtensorMap tmap, int r, const double* 
 #if !KB_DMMA_EARLY_SCALARS
     const EpiScalars sc = kb_epi_scalars<MODE>(e, ch.b);
 #endif
-    if (active && !(g.dbg & 2)) kb_sum_epilogue_regs<MODE>(D, g, e, ch, s_off, ar, ac, nrm, bad, sc);
+    if (active && !(g.dbg & 2)) kb_sum_epilogue_regs<MODE, NORMS>(D, g, e, ch, s_off, ar, ac, nrm, bad, sc);
     if (t == r) kb_stamp(g, 1, 5);
   }
   if (norm_b >= 0) kb_warp_finish<MODE>(e, nrm, bad, norm_b, nslots, slot, lane);

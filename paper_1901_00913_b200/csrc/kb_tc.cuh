@@ -624,7 +624,7 @@ struct StrideWalk {
 constexpr int kTcSumSlots = 4;                       // per-term accumulator slots (64 columns each)
 constexpr int kTcSumEpi = 8;                         // epilogue warps
 constexpr int kTcSumThreads = 32 * (kTcEpi + kTcSumEpi);
-template <int MODE>
+template <int MODE, bool NORMS = true>
 __device__ __forceinline__ void tc_sum_epi8(const float (&v)[8], const Epi<float>& e, long long at, int cnt,
                                             float Lb, float db, float rd, double vs, double (&nrm)[3],
                                             bool& bad) {
@@ -680,7 +680,7 @@ __device__ __forceinline__ void tc_sum_epi8(const float (&v)[8], const Epi<float
       const float d = __fsub_rn(x, w[i]);
       if (i < cnt) {
         bad |= !isfinite(x);
-        if (e.want_norms) {
+        if (NORMS && e.want_norms) {
           nrm[0] += (double)d * d;
           nrm[1] += (double)w[i] * w[i];
           nrm[2] += (double)x * x;
@@ -704,7 +704,7 @@ __device__ __forceinline__ void tc_sum_epi8(const float (&v)[8], const Epi<float
   }
 }
 
-template <int MODE>
+template <int MODE, bool NORMS = true>  // NORMS = false: update without the history norms
 __global__ void __launch_bounds__(kTcSumThreads, 1)
 kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* __restrict__ btab, AxisGeom g,
                Epi<float> e, int batch, int nst) {
@@ -976,7 +976,7 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
               else if (qi >= n - FH && qi < n) v8[i] += f[qi - (n - 2 * FH)];
             }
           }
-          tc_sum_epi8<MODE>(v8, e, row + 8 * j, min(8, c), Lb, db, rd, vs, nrm, bad);
+          tc_sum_epi8<MODE, NORMS>(v8, e, row + 8 * j, min(8, c), Lb, db, rd, vs, nrm, bad);
         }
       }
     }
