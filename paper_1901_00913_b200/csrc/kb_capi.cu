@@ -576,7 +576,11 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
       CUtensorMap mapx;
       if (bps > 0 && make_tmap(&mapx, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps,
                                tx.box_rows, 4, kb::kXF))
-        return op->last_engine = KB_ENGINE_MMA_TF32, launch(kb::kb_pass_sum_x<MODE>, smem, bps, mapx, nst);
+      {
+        op->last_engine = KB_ENGINE_MMA_TF32;
+        if (MODE == kb::EPI_UPDATE && !e.want_norms) return launch(kb::kb_pass_sum_x<MODE, false>, smem, bps, mapx, nst);
+        return launch(kb::kb_pass_sum_x<MODE>, smem, bps, mapx, nst);
+      }
     }
     const kb::TileBoxesF tb = kb::tile_boxes_f(kb::kNW * 16 + g.Wp);
     const size_t smem = sizeof(float) * ((size_t)kb::kStages * tb.stage_elems + (size_t)op->r * g.Wp);

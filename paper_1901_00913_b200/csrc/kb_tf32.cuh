@@ -366,7 +366,7 @@ kb_pass_split_x(const __grid_constant__ CUtensorMap tmap, float* __restrict__ z,
 // sum pass epilogue: lane (g, q) holds, for N-tile n (8 S rows) and M-tile m (16 columns),
 // Y[p = l0 + 16m + 8h + g][q' = s0 + s_off + 8n + 2q + {0,1}] in D[n][m][2h + {0,1}].
 // ------------------------------------------------------------------------------------------
-template <int MODE>
+template <int MODE, bool NORMS = true>
 __device__ __forceinline__ void kb_sum_epilogue_x(const float (&D)[2][2][4], const AxisGeom& g,
                                                   const Epi<float>& e, const Chunk& ch, int s_off, int lane,
                                                   double (&nrm)[3], bool& bad) {
@@ -446,7 +446,7 @@ __device__ __forceinline__ void kb_sum_epilogue_x(const float (&D)[2][2][4], con
             yv[i] = __fadd_rn(xv[i], __fmul_rn((float)e.beta, d));
             if (i == 0 || both) {
               bad |= !isfinite(xv[i]);
-              if (e.want_norms) {
+              if (NORMS && e.want_norms) {
                 nrm[0] += (double)d * d;
                 nrm[1] += (double)w[m][h][i] * w[m][h][i];
                 nrm[2] += (double)xv[i] * xv[i];
@@ -520,7 +520,7 @@ __device__ __forceinline__ void kb_sum_mma_x(float (&D)[2][2][4], const float* _
 // sum pass: warp w owns S rows [16w, 16w+16) (two N-tiles) x 32 L of a chunk; the (chunk,
 // term) tiles stream through the mbarrier ring; fused epilogue from the accumulators.
 // ------------------------------------------------------------------------------------------
-template <int MODE>
+template <int MODE, bool NORMS = true>  // NORMS = false: update without the history norms
 __global__ void __launch_bounds__(32 * kNW, 2)
 kb_pass_sum_x(const __grid_constant__ CUtensorMap tmap, int r, const float* __restrict__ tin, long long t_bs,
               AxisGeom g, Epi<float> e, int batch, int parts, int nst) {
@@ -638,7 +638,7 @@ kb_pass_sum_x(const __grid_constant__ CUtensorMap tmap, int r, const float* __re
       if (lane == 0) mbar_arrive(&empty[st]);
     }
     if (t == r) kb_stamp(g, 1, 4);
-    if (active && !(g.dbg & 2)) kb_sum_epilogue_x<MODE>(D, g, e, ch, s_off, lane, nrm, bad);
+    if (active && !(g.dbg & 2)) kb_sum_epilogue_x<MODE, NORMS>(D, g, e, ch, s_off, lane, nrm, bad);
     if (t == r) kb_stamp(g, 1, 5);
   }
   if (norm_b >= 0) kb_warp_finish_f<MODE>(e, nrm, bad, norm_b, nslots, slot, lane);
