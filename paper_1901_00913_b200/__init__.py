@@ -4,7 +4,7 @@ Drop-in entry points (same names, signatures and error behaviour as the referenc
 ``kronblur``): ``sfista``, ``kron_apply``, ``kron_apply_adjoint``, ``estimate_lipschitz``,
 ``objective_matrix``, ``decompose``, ``blur_direct``. The arithmetic of the first four runs in the sm_100a kernels of
 ``libkb_b200.so`` (C ABI: include/kronblur_b200.h); ``decompose`` is the one-time host setup.
-``install()`` reroutes an imported ``kronblur`` to these functions.
+``install(kronblur, options=None)`` reroutes an imported ``kronblur`` to these functions.
 """
 
 from .blur import blur_direct, blur_direct_batch
@@ -41,8 +41,4 @@ from .structured import FactorKind, StructuredFactor, factor_band, factor_to_den
 __version__ = "0.1.0"
 
 
-def install(kronblur_module=None):
-    """Patch an imported ``kronblur`` so its solver path runs here (see install.py)."""
-    from .install import install as _install
-
-    return _install(kronblur_module)
+from .dropin import install  # noqa: E402  (patches an imported kronblur; see dropin.py)

@@ -84,10 +84,8 @@ struct kb_op {
   unsigned* br_b_conv = nullptr;
   unsigned* br_b_corr = nullptr;
   GraphCache* graph = nullptr;
-  mutable int last_mirror = 0;  // the latest split pass stored Z^T's reflected halo rows
-  mutable int last_slots = 0;  // norm partial slots per image written by the latest sum pass
-  mutable int last_engine = 0;  // KB_ENGINE_* of the latest pass launch
-  mutable int phase_engine[4] = {0, 0, 0, 0};  // engines of the latest kb_time_passes phases
+  // engines of the latest kb_time_passes phases (reporting only; written under g_phase_mu)
+  mutable int phase_engine[4] = {0, 0, 0, 0};
 };
 
 namespace {
@@ -100,8 +98,18 @@ long long z_plane(const kb_op* op) { return (long long)(op->n + 2 * op->Hb) * op
 template <typename T>
 T* z_row0(const kb_op* op, void* z) { return static_cast<T*>(z) + (long long)op->Hb * op->m; }
 
+// Per-call launch state: what the latest pass launch of THIS call did. It lives in the call's
+// Work (never in the shared kb_op), so concurrent calls on one operator from several host
+// threads (each with its own workspace) do not see each other's launches.
+struct Ctx {
+  int mirror = 0;  // the latest split pass stored Z^T's reflected halo rows
+  int slots = 0;   // norm partial slots per image written by the latest sum pass
+  int engine = 0;  // KB_ENGINE_* of the latest pass launch
+};
+
 // workspace: [Z: batch*r planes][R: batch planes][partials][scalars]
 struct Work {
+  mutable Ctx ctx;
   void* z;
   void* rp;
   void* fold;  // [batch][m][2*Hb] adjoint column-fold corrections
@@ -112,12 +120,11 @@ struct Work {
 
 // Resident blocks for the persistent fp64 kernels: two per SM.
 int persistent_blocks() {
-  static int nb = 0;
-  if (!nb) {
+  static const int nb = [] {  // thread-safe one-time init (C++11 magic static)
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    nb = 2 * sms;
-  }
+    return 2 * sms;
+  }();
   return nb;
 }
 
@@ -127,16 +134,14 @@ int persistent_blocks() {
 bool make_tmap(CUtensorMap* map, const void* base, long long cols, long long rows, long long planes,
                long long row_stride, long long plane_stride, int box_rows, int esize = 8,
                int box_cols = 0, CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_NONE) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {  // thread-safe one-time lookup
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+  }();
   if (!encode) return false;
   if (reinterpret_cast<uintptr_t>(base) % 16 || (row_stride * esize) % 16 || (plane_stride * esize) % 16)
     return false;
@@ -257,6 +262,7 @@ void add_groups(kb::Groups& g, int start, int count, int gmax, int sign) {
 // Opt a kernel into the full 227 KB of shared memory (minus its static shared memory). Keyed by
 // the kernel's address: instantiations that differ only in a template value share a type.
 std::mutex g_smem_mu;
+std::mutex g_phase_mu;
 std::unordered_map<const void*, int> g_smem_limit;
 
 template <typename K>
@@ -359,13 +365,13 @@ int sm_count() { return persistent_blocks() / 2; }
 
 // Pass A into the Z^T planes (z: row 0 of image 0, term 0). mirror_h > 0 asks the persistent
 // kernels to also store the reflected halo rows (times msign[b][i]) for a reflect-filled pass B;
-// op->last_mirror records whether they did.
+// c.mirror records whether they did.
 template <typename T>
-int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeom& g,
+int launch_a(const kb_op* op, Ctx& c, const T* in, T* z, const T* tin, const kb::AxisGeom& g,
              const kb::Groups& grp, const double* nw2, int mirror_h, const T* msign, cudaStream_t s) {
   const long long in_bs = (long long)plane_elems(op);
   const long long z_ps = z_plane(op);
-  op->last_mirror = 0;
+  c.mirror = 0;
   const long long z_bs = z_ps * op->r;
   const long long t_bs = (long long)op->r * g.Wp;
   const T* in_map = in - (long long)g.halo_lo * g.other;
@@ -391,13 +397,13 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
       KB_TRY(allow_smem(kern, smem));
       int parts, nb, eparts;
       plan(bps, parts, nb, eparts);
-      op->last_engine = sizeof(T) == 8 ? KB_ENGINE_DMMA : KB_ENGINE_FFMA;
+      c.engine = sizeof(T) == 8 ? KB_ENGINE_DMMA : KB_ENGINE_FFMA;
       KB_CUDA(launch_persistent(kern, nb, smem, s, map, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r, op->batch,
                                 parts, eparts, mirror_h, msign));
-      op->last_mirror = mirror_h > 0;
+      c.mirror = mirror_h > 0;
       return KB_OK;
     }
-    op->last_engine = KB_ENGINE_GENERIC;
+    c.engine = KB_ENGINE_GENERIC;
     return launch_a_g<T, kGmaxF64>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
   } else {
     const unsigned* btab = brick_table(op, tin);
@@ -446,11 +452,11 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = use_pdl() ? 1 : 0;
-        op->last_engine = KB_ENGINE_TC_TF32;
+        c.engine = KB_ENGINE_TC_TF32;
         KB_CUDA(cudaLaunchKernelEx(&cfg, kern, mapt, mapz, z, z_ps, z_bs, btab, g, nw2, op->r, op->batch, parts,
                                    tg, G, nst, reinterpret_cast<const float*>(in), in_bs, mirror_h,
                                    reinterpret_cast<const float*>(msign)));
-        op->last_mirror = mirror_h > 0;
+        c.mirror = mirror_h > 0;
         return KB_OK;
       }
     }
@@ -466,10 +472,10 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
         KB_TRY(allow_smem(kern, smem));
         int parts, nb, eparts;
         plan(bps, parts, nb, eparts);
-        op->last_engine = KB_ENGINE_MMA_TF32;
+        c.engine = KB_ENGINE_MMA_TF32;
         KB_CUDA(launch_persistent(kern, nb, smem, s, mapx, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r,
                                   op->batch, parts, eparts, mirror_h, msign, nst));
-        op->last_mirror = mirror_h > 0;
+        c.mirror = mirror_h > 0;
         return KB_OK;
       }
     }
@@ -483,13 +489,13 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
       KB_TRY(allow_smem(kern, smem));
       int parts, nb, eparts;
       plan(bps, parts, nb, eparts);
-      op->last_engine = sizeof(T) == 8 ? KB_ENGINE_DMMA : KB_ENGINE_FFMA;
+      c.engine = sizeof(T) == 8 ? KB_ENGINE_DMMA : KB_ENGINE_FFMA;
       KB_CUDA(launch_persistent(kern, nb, smem, s, map, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->r, op->batch,
                                 parts, eparts, mirror_h, msign));
-      op->last_mirror = mirror_h > 0;
+      c.mirror = mirror_h > 0;
       return KB_OK;
     }
-    op->last_engine = KB_ENGINE_GENERIC;
+    c.engine = KB_ENGINE_GENERIC;
     return launch_a_g<T, kGmaxF32>(in, in_bs, z, z_ps, z_bs, tin, t_bs, g, grp, nw2, op->batch, s);
   }
 }
@@ -498,10 +504,10 @@ int launch_a(const kb_op* op, const T* in, T* z, const T* tin, const kb::AxisGeo
 // reflect-filled pass's out-of-domain rows from the halo rows the split pass stored (the TMA
 // map then spans them: halo_lo = Hb); without them the generic kernel folds at read time.
 template <typename T, int MODE>
-int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in, const T* tsign,
+int launch_b(const kb_op* op, Ctx& c, const T* z, const T* tin, const kb::AxisGeom& g_in, const T* tsign,
              const kb::Epi<T>& e, cudaStream_t s) {
   const long long z_ps = z_plane(op);
-  const bool mirrored = g_in.fill && op->last_mirror;
+  const bool mirrored = g_in.fill && c.mirror;
   kb::AxisGeom g = g_in;
   if (mirrored) g.halo_lo = g.halo_hi = op->Hb;
   const T* zmap = z - (long long)g.halo_lo * g.other;
@@ -514,7 +520,7 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
     kb::plan_items(g.len, (g.other + 31) / 32, op->batch, sm_count() * bps, parts, nb);
     if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // warps skip untouched images
       KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kNW, s));
-    op->last_slots = nb * kb::kNW;
+    c.slots = nb * kb::kNW;
     KB_CUDA(launch_persistent(kern, nb, smem, s, map, op->r, tin, (long long)op->r * g.Wp, g, e, op->batch,
                               parts, extra...));
     return KB_OK;
@@ -528,7 +534,7 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
     if (use_dmma(op) && persistent_ok && bps > 0 &&
         make_tmap(&map, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, tb.box_rows))
     {
-      op->last_engine = KB_ENGINE_DMMA;
+      c.engine = KB_ENGINE_DMMA;
       if (MODE == kb::EPI_UPDATE && !e.want_norms) return launch(kb::kb_pass_sum_dmma<MODE, false>, smem, bps, map);
       return launch(kb::kb_pass_sum_dmma<MODE>, smem, bps, map);
     }
@@ -551,7 +557,7 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
         KB_TRY(allow_smem(kern, smem));
         if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // warps skip untouched images
           KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kTcSumEpi, s));
-        op->last_slots = nb * kb::kTcSumEpi;
+        c.slots = nb * kb::kTcSumEpi;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(nb);
         cfg.blockDim = dim3(kb::kTcSumThreads);
@@ -562,7 +568,7 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = use_pdl() ? 1 : 0;
-        op->last_engine = KB_ENGINE_TC_TF32;
+        c.engine = KB_ENGINE_TC_TF32;
         KB_CUDA(cudaLaunchKernelEx(&cfg, kern, mapt, op->r, btab, g, e, op->batch, nst));
         return KB_OK;
       }
@@ -577,7 +583,7 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
       if (bps > 0 && make_tmap(&mapx, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps,
                                tx.box_rows, 4, kb::kXF))
       {
-        op->last_engine = KB_ENGINE_MMA_TF32;
+        c.engine = KB_ENGINE_MMA_TF32;
         if (MODE == kb::EPI_UPDATE && !e.want_norms) return launch(kb::kb_pass_sum_x<MODE, false>, smem, bps, mapx, nst);
         return launch(kb::kb_pass_sum_x<MODE>, smem, bps, mapx, nst);
       }
@@ -588,7 +594,7 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
     CUtensorMap map;
     if (use_tma_f32(op) && persistent_ok && bps > 0 &&
         make_tmap(&map, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, tb.box_rows, 4))
-      return op->last_engine = KB_ENGINE_FFMA, launch(kb::kb_pass_sum_f<MODE>, smem, bps, map);
+      return c.engine = KB_ENGINE_FFMA, launch(kb::kb_pass_sum_f<MODE>, smem, bps, map);
   }
   constexpr int TS = kb::kNW * kRB;
   const size_t smem = sizeof(T) * (2 * (size_t)(TS + g.Wp) * 32 + 2 * (size_t)g.Wp);
@@ -599,8 +605,8 @@ int launch_b(const kb_op* op, const T* z, const T* tin, const kb::AxisGeom& g_in
   const long long t_bs = (long long)op->r * g.Wp;
   dim3 grid((g.other + 31) / 32, (g.len + TS - 1) / TS, op->batch);
   dim3 block(32, kb::kNW);
-  op->last_slots = (int)(grid.x * grid.y);
-  op->last_engine = KB_ENGINE_GENERIC;
+  c.slots = (int)(grid.x * grid.y);
+  c.engine = KB_ENGINE_GENERIC;
   kern<<<grid, block, smem, s>>>(z, z_ps, z_bs, op->r, tin, t_bs, g, tsign, e);
   KB_CUDA(cudaGetLastError());
   return KB_OK;
@@ -612,11 +618,10 @@ struct RowBlock {
 };
 
 int debug_mode() {
-  static int mode = -1;
-  if (mode < 0) {
+  static const int mode = [] {
     const char* v = std::getenv("KB_DEBUG_MODE");
-    mode = v ? std::atoi(v) : 0;
-  }
+    return v ? std::atoi(v) : 0;
+  }();
   return mode;
 }
 
@@ -673,7 +678,7 @@ int stage_a(const kb_op* op, int adjoint, const T* in, const Work& w, const RowB
   const T* msign = (adjoint && op->sym_b) ? static_cast<const T*>(op->sign_b) : nullptr;
   if (mirror_h > op->n)  // folds leaving the domain: those halo rows must read as zero
     KB_CUDA(cudaMemsetAsync(w.z, 0, (size_t)z_plane(op) * op->r * op->batch * sizeof(T), s));
-  KB_TRY(launch_a<T>(op, in, z, static_cast<const T*>(adjoint ? op->ta_corr : op->ta_conv), ga,
+  KB_TRY(launch_a<T>(op, w.ctx, in, z, static_cast<const T*>(adjoint ? op->ta_corr : op->ta_conv), ga,
                      adjoint ? op->grp_adj : op->grp_fwd, nw2, mirror_h, msign, s));
   if (adjoint && op->bc_a == KB_BC_REFLECTIVE && !op->sym_a && op->Ha > 0) {
     const long long z_ps = z_plane(op);
@@ -681,7 +686,7 @@ int stage_a(const kb_op* op, int adjoint, const T* in, const Work& w, const RowB
     kb::kb_fold_split<T><<<grid, 128, 0, s>>>(in, (long long)plane_elems(op), z, z_ps, z_ps * op->r, op->r,
                                                static_cast<const T*>(op->ta_conv),
                                                (long long)op->r * op->Wpa, ga,
-                                               op->last_mirror ? mirror_h : 0, msign);
+                                               w.ctx.mirror ? mirror_h : 0, msign);
     KB_CUDA(cudaGetLastError());
   }
   return KB_OK;
@@ -703,7 +708,7 @@ int stage_b(const kb_op* op, int adjoint, kb::Epi<T> e, const Work& w, cudaStrea
     e.foldH = op->Hb;
   }
   const T* tsign = (adjoint && op->sym_b) ? static_cast<const T*>(op->sign_b) : nullptr;
-  return launch_b<T, MODE>(op, z, static_cast<const T*>(adjoint ? op->tb_corr : op->tb_conv), gb,
+  return launch_b<T, MODE>(op, w.ctx, z, static_cast<const T*>(adjoint ? op->tb_corr : op->tb_conv), gb,
                            tsign, e, s);
 }
 
@@ -754,7 +759,7 @@ int update_t(const kb_op* op, const T* R, T* X, T* Y, const Work& w, const RowBl
   KB_TRY((stage_b<T, kb::EPI_UPDATE>(op, 1, update_epi<T>(op, X, Y, w, beta, k, Ldev, ddev, project,
                                                           nonfinite, norms_out != nullptr), w, s)));
   if (norms_out) {
-    kb::kb_reduce_partials<<<op->batch, 256, 0, s>>>(w.partials, op->last_slots, 3, norms_out,
+    kb::kb_reduce_partials<<<op->batch, 256, 0, s>>>(w.partials, w.ctx.slots, 3, norms_out,
                                                       op->batch, 1);
     KB_CUDA(cudaGetLastError());
   }
@@ -796,7 +801,7 @@ int power_t(const kb_op* op, T* v, T* wbuf, const Work& w, int iters, double* hi
     e2.vnw2 = nw2;
     e2.partials = w.partials;
     KB_TRY((stage_b<T, kb::EPI_POWER>(op, 1, e2, w, s)));
-    kb::kb_reduce_partials<<<op->batch, 256, 0, s>>>(w.partials, op->last_slots, 2,
+    kb::kb_reduce_partials<<<op->batch, 256, 0, s>>>(w.partials, w.ctx.slots, 2,
                                                       hist + (size_t)k * 2 * op->batch,
                                                       op->batch, 1);
     KB_CUDA(cudaGetLastError());
@@ -1047,7 +1052,10 @@ int time_passes_t(const kb_op* op, const T* Y, const T* B, T* R, T* X, T* Yio, c
         default: rc = stage_b<T, kb::EPI_UPDATE>(op, 1, eu, w, s); break;
       }
     }
-    op->phase_engine[phase] = op->last_engine;
+    {
+      std::lock_guard<std::mutex> lock(g_phase_mu);
+      op->phase_engine[phase] = w.ctx.engine;
+    }
     cudaError_t ce = cudaStreamEndCapture(s, &graph);
     if (rc == KB_OK && ce == cudaSuccess) ce = cudaGraphInstantiate(&exec, graph, 0);
     if (rc == KB_OK && ce == cudaSuccess) ce = cudaGraphLaunch(exec, s);  // warm-up
@@ -1412,6 +1420,7 @@ int kb_fma_peak(int dtype, float* tflops, void* stream) {
 int kb_last_engines(const kb_op* op, int* engines4) {
   KB_TRY(check_op(op));
   if (!engines4) return fail(KB_ERR_ARGUMENT, "null output");
+  std::lock_guard<std::mutex> lock(g_phase_mu);
   for (int i = 0; i < 4; ++i) engines4[i] = op->phase_engine[i];
   return KB_OK;
 }

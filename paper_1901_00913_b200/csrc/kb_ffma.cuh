@@ -140,6 +140,7 @@ kb_pass_split_f(const __grid_constant__ CUtensorMap tmap, float* __restrict__ z,
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();  // launched with programmatic serialization: the previous kernel's outputs are read below
 
   ChunkWalk fill_walk(g.len, LT, parts, batch, 4, eparts), use_walk(g.len, LT, parts, batch, 4, eparts);
   Chunk fc, ch;
@@ -358,6 +359,7 @@ kb_pass_sum_f(const __grid_constant__ CUtensorMap tmap, int r, const float* __re
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();  // launched with programmatic serialization: the previous kernel's outputs are read below
 
   ChunkWalk fill_walk(g.len, LT, parts, batch, 4), use_walk(g.len, LT, parts, batch, 4);
   Chunk fc;

@@ -8,6 +8,7 @@ missing or no GPU is present, every entry point raises.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 import threading
@@ -235,8 +236,10 @@ class DeviceOperator:
     """Immutable device copy of one KronOperator (or a batch of equal-shape operators).
 
     Holds the kb_op handle, the device workspace, and reusable pinned/device staging buffers for
-    the host-facing API. Thread safety: the handle is immutable; the staging buffers are guarded
-    by ``self.lock``.
+    the host-facing API. Thread safety: the native handle is immutable (per-launch state lives in
+    each call's context, kb_capi.cu ``Ctx``); the shared workspace and the staging buffers are
+    guarded by ``self.lock`` (re-entrant), which every device-path method takes, so host threads
+    sharing a cached operator serialise on it instead of racing on the workspace.
     """
 
     def __init__(self, ops, dtype: str = "float64", band_tol: float = BAND_REL_TOL):
@@ -280,9 +283,27 @@ class DeviceOperator:
         self._finalizer = weakref.finalize(self, lib.kb_op_destroy, handle)
         nbytes = int(lib.kb_workspace_bytes(handle))
         self.work = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
-        self.lock = threading.Lock()
+        self.lock = threading.RLock()
         self._stage = {}
         self._norm_work = None
+        self._ws_event = None  # recorded after the latest launch that used the workspace
+
+    @contextlib.contextmanager
+    def exclusive(self):
+        """Exclusive use of the shared workspace: the re-entrant host lock, plus stream ordering
+        on the device - the caller's stream first waits for the previous user of the workspace
+        (which may have run on another stream), and marks its own use when done."""
+        torch = _torch()
+        with self.lock:
+            stream = torch.cuda.current_stream()
+            if self._ws_event is not None:
+                stream.wait_event(self._ws_event)
+            try:
+                yield
+            finally:
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                self._ws_event = ev
 
     def info(self) -> dict:
         """Device layout facts (kb_op_info)."""
@@ -323,82 +344,87 @@ class DeviceOperator:
     # -- kernels ---------------------------------------------------------------------------
     def apply(self, X, out=None, adjoint: bool = False):
         """out = A X (or A^T X) for device planes X (kron.py:218-235)."""
-        X = self._as_plane(X, "operand")
-        out = self.plane() if out is None else self._as_plane(out, "output")
-        fn = load_library().kb_apply_adjoint if adjoint else load_library().kb_apply
-        _check(fn(self._handle, _ptr(X), _ptr(out), _ptr(self.work), _stream_handle()),
-               "kb_apply_adjoint" if adjoint else "kb_apply")
-        return out
+        with self.exclusive():
+            X = self._as_plane(X, "operand")
+            out = self.plane() if out is None else self._as_plane(out, "output")
+            fn = load_library().kb_apply_adjoint if adjoint else load_library().kb_apply
+            _check(fn(self._handle, _ptr(X), _ptr(out), _ptr(self.work), _stream_handle()),
+                   "kb_apply_adjoint" if adjoint else "kb_apply")
+            return out
 
     def resid_norms(self, AX, B, X, truth, out2):
         """out2 (device double[2]) = ||AX - B||^2, ||X - truth||^2 (kb_resid_norms; truth may be None)."""
-        torch = _torch()
-        if self._norm_work is None:
-            self._norm_work = torch.empty(KB_RESID_NORMS_WORK // 8, dtype=torch.float64, device=self.device)
-        AX, B, X = self._as_plane(AX, "AX"), self._as_plane(B, "data"), self._as_plane(X, "x")
-        if truth is not None:
-            truth = self._as_plane(truth, "truth")
-        rc = load_library().kb_resid_norms(
-            _code(self.dtype), _ptr(AX), _ptr(B), _ptr(X), _ptr(truth) if truth is not None else None,
-            int(AX.numel()), _ptr(out2), _ptr(self._norm_work), _stream_handle())
-        _check(rc, "kb_resid_norms")
+        with self.exclusive():
+            torch = _torch()
+            if self._norm_work is None:
+                self._norm_work = torch.empty(KB_RESID_NORMS_WORK // 8, dtype=torch.float64, device=self.device)
+            AX, B, X = self._as_plane(AX, "AX"), self._as_plane(B, "data"), self._as_plane(X, "x")
+            if truth is not None:
+                truth = self._as_plane(truth, "truth")
+            rc = load_library().kb_resid_norms(
+                _code(self.dtype), _ptr(AX), _ptr(B), _ptr(X), _ptr(truth) if truth is not None else None,
+                int(AX.numel()), _ptr(out2), _ptr(self._norm_work), _stream_handle())
+            _check(rc, "kb_resid_norms")
 
     def resid_norms_images(self, AX, B) -> np.ndarray:
         """||AX[k] - B[k]||^2 per image of a batched plane (kb_resid_norms per image)."""
-        torch = _torch()
-        AX, B = self._as_plane(AX, "AX"), self._as_plane(B, "data")
-        if self._norm_work is None:
-            self._norm_work = torch.empty(KB_RESID_NORMS_WORK // 8, dtype=torch.float64, device=self.device)
-        out = torch.zeros((self.batch, 2), dtype=torch.float64, device=self.device)
-        ax, bb = AX.reshape(self.batch, -1), B.reshape(self.batch, -1)
-        lib = load_library()
-        for k in range(self.batch):
-            rc = lib.kb_resid_norms(_code(self.dtype), _ptr(ax[k]), _ptr(bb[k]), None, None,
-                                    int(self.m * self.n), _ptr(out[k]), _ptr(self._norm_work),
-                                    _stream_handle())
-            _check(rc, "kb_resid_norms")
-        return out[:, 0].cpu().numpy()
+        with self.exclusive():
+            torch = _torch()
+            AX, B = self._as_plane(AX, "AX"), self._as_plane(B, "data")
+            if self._norm_work is None:
+                self._norm_work = torch.empty(KB_RESID_NORMS_WORK // 8, dtype=torch.float64, device=self.device)
+            out = torch.zeros((self.batch, 2), dtype=torch.float64, device=self.device)
+            ax, bb = AX.reshape(self.batch, -1), B.reshape(self.batch, -1)
+            lib = load_library()
+            for k in range(self.batch):
+                rc = lib.kb_resid_norms(_code(self.dtype), _ptr(ax[k]), _ptr(bb[k]), None, None,
+                                        int(self.m * self.n), _ptr(out[k]), _ptr(self._norm_work),
+                                        _stream_handle())
+                _check(rc, "kb_resid_norms")
+            return out[:, 0].cpu().numpy()
 
     def sfista_run(self, B, X, Y, beta: np.ndarray, k0: int, iters: int, L, lam: float,
                    project: bool, nonfinite, norms=None, use_graph: bool = False):
         """Native loop of `iters` sFISTA iterations (kb_sfista_run)."""
-        B = self._as_plane(B, "data")
-        X = self._as_plane(X, "x")
-        Y = self._as_plane(Y, "y")
-        beta = np.ascontiguousarray(beta, dtype=np.float64)
-        Ls = np.ascontiguousarray(np.broadcast_to(np.asarray(L, dtype=np.float64), (self.batch,)))
-        if beta.size < k0 + iters:
-            raise ArgumentError("momentum table shorter than the iteration range")
-        if np.ndim(lam) == 0:
-            fn, lam_arg, what = load_library().kb_sfista_run, float(lam), "kb_sfista_run"
-        else:  # one lambda per image (select_lambda's batched probes)
-            lams = np.ascontiguousarray(lam, dtype=np.float64)
-            if lams.shape != (self.batch,):
-                raise ArgumentError(f"{lams.size} lambdas for a batch of {self.batch}")
-            fn, lam_arg, what = load_library().kb_sfista_run_lams, lams.ctypes.data_as(_c_dp), "kb_sfista_run_lams"
-        rc = fn(
-            self._handle, _ptr(B), _ptr(X), _ptr(Y), _ptr(self.work), beta.ctypes.data_as(_c_dp),
-            int(k0), int(iters), Ls.ctypes.data_as(_c_dp), lam_arg, int(bool(project)),
-            _ptr(nonfinite), _ptr(norms) if norms is not None else None, int(bool(use_graph)),
-            _stream_handle(),
-        )
-        _check(rc, what)
+        with self.exclusive():
+            B = self._as_plane(B, "data")
+            X = self._as_plane(X, "x")
+            Y = self._as_plane(Y, "y")
+            beta = np.ascontiguousarray(beta, dtype=np.float64)
+            Ls = np.ascontiguousarray(np.broadcast_to(np.asarray(L, dtype=np.float64), (self.batch,)))
+            if beta.size < k0 + iters:
+                raise ArgumentError("momentum table shorter than the iteration range")
+            if np.ndim(lam) == 0:
+                fn, lam_arg, what = load_library().kb_sfista_run, float(lam), "kb_sfista_run"
+            else:  # one lambda per image (select_lambda's batched probes)
+                lams = np.ascontiguousarray(lam, dtype=np.float64)
+                if lams.shape != (self.batch,):
+                    raise ArgumentError(f"{lams.size} lambdas for a batch of {self.batch}")
+                fn, lam_arg, what = load_library().kb_sfista_run_lams, lams.ctypes.data_as(_c_dp), "kb_sfista_run_lams"
+            rc = fn(
+                self._handle, _ptr(B), _ptr(X), _ptr(Y), _ptr(self.work), beta.ctypes.data_as(_c_dp),
+                int(k0), int(iters), Ls.ctypes.data_as(_c_dp), lam_arg, int(bool(project)),
+                _ptr(nonfinite), _ptr(norms) if norms is not None else None, int(bool(use_graph)),
+                _stream_handle(),
+            )
+            _check(rc, what)
 
     def time_passes(self, Y, B, L: float, lam: float, reps: int = 20) -> list:
         """Average device ms of the four kernels of one iteration (kb_time_passes)."""
-        torch = _torch()
-        Y = self._as_plane(Y, "y")
-        B = self._as_plane(B, "data")
-        R, X, Yio = torch.empty_like(Y), torch.zeros_like(Y), Y.clone()
-        flag = torch.full((1,), INT_MAX, dtype=torch.int32, device=self.device)
-        Ls = np.ascontiguousarray(np.broadcast_to(np.asarray(L, dtype=np.float64), (self.batch,)))
-        ms = (ctypes.c_float * 4)()
-        rc = load_library().kb_time_passes(self._handle, _ptr(Y), _ptr(B), _ptr(R), _ptr(X),
-                                           _ptr(Yio), _ptr(self.work), int(reps),
-                                           Ls.ctypes.data_as(_c_dp), float(lam), _ptr(flag), ms,
-                                           _stream_handle())
-        _check(rc, "kb_time_passes")
-        return [float(v) for v in ms]
+        with self.exclusive():
+            torch = _torch()
+            Y = self._as_plane(Y, "y")
+            B = self._as_plane(B, "data")
+            R, X, Yio = torch.empty_like(Y), torch.zeros_like(Y), Y.clone()
+            flag = torch.full((1,), INT_MAX, dtype=torch.int32, device=self.device)
+            Ls = np.ascontiguousarray(np.broadcast_to(np.asarray(L, dtype=np.float64), (self.batch,)))
+            ms = (ctypes.c_float * 4)()
+            rc = load_library().kb_time_passes(self._handle, _ptr(Y), _ptr(B), _ptr(R), _ptr(X),
+                                               _ptr(Yio), _ptr(self.work), int(reps),
+                                               Ls.ctypes.data_as(_c_dp), float(lam), _ptr(flag), ms,
+                                               _stream_handle())
+            _check(rc, "kb_time_passes")
+            return [float(v) for v in ms]
 
     def last_engines(self) -> list:
         """Engine names of the four phases of the latest time_passes (kb_last_engines)."""
@@ -408,14 +434,15 @@ class DeviceOperator:
 
     def power_iter(self, v, iters: int):
         """Device power iteration; returns the device history [iters][2][batch] (rho, ||w||^2)."""
-        torch = _torch()
-        v = self._as_plane(v, "start vector")
-        w = torch.empty_like(v)
-        hist = torch.zeros((iters, 2, self.batch), dtype=torch.float64, device=self.device)
-        rc = load_library().kb_power_iter(self._handle, _ptr(v), _ptr(w), _ptr(self.work),
-                                          int(iters), _ptr(hist), _stream_handle())
-        _check(rc, "kb_power_iter")
-        return hist
+        with self.exclusive():
+            torch = _torch()
+            v = self._as_plane(v, "start vector")
+            w = torch.empty_like(v)
+            hist = torch.zeros((iters, 2, self.batch), dtype=torch.float64, device=self.device)
+            rc = load_library().kb_power_iter(self._handle, _ptr(v), _ptr(w), _ptr(self.work),
+                                              int(iters), _ptr(hist), _stream_handle())
+            _check(rc, "kb_power_iter")
+            return hist
 
 
 def fma_peak(dtype: str = "float64") -> float:

@@ -201,7 +201,7 @@ def _apply(op, X, adjoint: bool, dtype: str | None):
         dev = device_operator(op, dt)
         return dev.apply(X.to(dev.tdtype).contiguous(), adjoint=adjoint)
     dev = device_operator(op, dtype or "float64")
-    with dev.lock:
+    with dev.exclusive():
         d_in = dev.staging("apply_in")
         d_in.copy_(torch.from_numpy(np.ascontiguousarray(X)).to(dev.tdtype), non_blocking=False)
         out = dev.apply(d_in, out=dev.staging("apply_out"), adjoint=adjoint)

@@ -281,7 +281,7 @@ def sfista(op, B, cfg: SolveConfig, X0=None, truth=None, exact_apply=None, *,
     dev = device_operator(op, opts.dtype)
     use_graph = opts.use_graph if opts.use_graph is not None else (fast and K >= 8)
 
-    with dev.lock:
+    with dev.exclusive():
         stream = torch.cuda.current_stream()
         hB, hX = dev.staging("host_b", pinned=True), dev.staging("host_x", pinned=True)
         Bd, Xd, Yd = dev.staging("b"), dev.staging("x"), dev.staging("y")

@@ -224,8 +224,93 @@ def test_blur_exact_matches_loop_oracle(rng):
         np.testing.assert_allclose(got, blur_loop(psf.values, psf.center, X, bc), rtol=0, atol=1e-12)
 
 
+def _stub_kronblur():
+    """A stand-in package with the reference's module layout and by-name bindings (no import of
+    kronblur itself), so install() is tested in every environment."""
+    import sys
+    import types
+    from dataclasses import dataclass, field
+
+    pkg = types.ModuleType("kbstub")
+    pkg.__path__ = []
+    mods = {name: types.ModuleType(f"kbstub.{name}") for name in ("solvers", "kron", "pipeline", "psf", "imaging")}
+
+    @dataclass(frozen=True)
+    class IterationRecord:
+        k: int
+        t: float
+        objective: float
+        eta: object
+        gamma: object
+        ms: float
+
+    @dataclass
+    class SolveRun:
+        x: object
+        iterations: int
+        solve_ms: float
+        history: list = field(default_factory=list)
+        iterates: list = field(default_factory=list)
+
+    orig = {name: (lambda *a, **k: "reference") for name in
+            ("sfista", "kron_apply", "kron_apply_adjoint", "estimate_lipschitz", "decompose", "_vec_ops",
+             "blur_direct", "select_lambda")}
+    mods["solvers"].IterationRecord, mods["solvers"].SolveRun = IterationRecord, SolveRun
+    for name in ("sfista", "kron_apply", "kron_apply_adjoint", "estimate_lipschitz", "select_lambda"):
+        setattr(mods["solvers"], name, orig[name])
+    for name in ("decompose", "kron_apply", "kron_apply_adjoint"):
+        setattr(mods["kron"], name, orig[name])
+    for name in orig:
+        setattr(mods["pipeline"], name, orig[name])
+    mods["psf"].blur_direct = orig["blur_direct"]
+    mods["imaging"].blur_direct = orig["blur_direct"]
+    for name in ("sfista", "kron_apply", "kron_apply_adjoint", "estimate_lipschitz", "decompose", "blur_direct"):
+        setattr(pkg, name, orig[name])
+    sys.modules["kbstub"] = pkg
+    for name, mod in mods.items():
+        sys.modules[f"kbstub.{name}"] = mod
+        setattr(pkg, name, mod)
+    return pkg, mods, orig
+
+
+def test_install_twice_with_options_on_a_stub_package():
+    import sys
+
+    pkg, mods, orig = _stub_kronblur()
+    try:
+        opts = kb.SolveOptions(dtype="float32", project=True)
+        undo1 = kb.install(pkg, options=opts)
+        assert callable(kb.install)  # the submodule import must not shadow the function
+        undo2 = kb.install(pkg, options=kb.SolveOptions(dtype="float64"))
+        pipe = mods["pipeline"]
+        assert pipe.kron_apply is kb.kron_apply and mods["solvers"].kron_apply is kb.kron_apply
+        assert pipe.decompose is kb.decompose and mods["kron"].decompose is kb.decompose
+        assert pipe.estimate_lipschitz is kb.estimate_lipschitz
+        assert pipe.sfista is not orig["sfista"] and mods["solvers"].sfista is not orig["sfista"]
+        assert pipe.blur_direct is kb.blur_direct and mods["imaging"].blur_direct is kb.blur_direct
+        # restore()'s vector-form closures are tagged for the device power iteration
+        op = kb.decompose(random_psf(np.random.default_rng(1), 5), kb.BoundaryCondition.ZERO, s=2, shape=(8, 8))
+        apply_vec, adjoint_vec = pipe._vec_ops(op)
+        assert apply_vec._kb_power == (op, "vector", "float64")
+        with pytest.raises(kb.ArgumentError):
+            kb.install(pkg, options="float32")
+        undo2()
+        assert pipe.kron_apply is kb.kron_apply  # the first install is still in place
+        undo1()
+        for name, fn in orig.items():
+            assert getattr(pipe, name) is fn
+        assert mods["kron"].decompose is orig["decompose"] and pkg.sfista is orig["sfista"]
+    finally:
+        for name in [k for k in sys.modules if k == "kbstub" or k.startswith("kbstub.")]:
+            del sys.modules[name]
+
+
 def test_install_patches_every_by_name_binding(monkeypatch):
-    kronblur = pytest.importorskip("kronblur")  # the reference, when importable (build container)
+    from conftest import reference_module
+
+    kronblur = reference_module()  # the reference, pip-installed into baseline/_ref by build()
+    if kronblur is None:
+        pytest.skip("reference not installed in baseline/_ref (run __graft_entry__.build() here)")
     from kronblur import pipeline, solvers
 
     orig = (solvers.sfista, pipeline.sfista, pipeline.estimate_lipschitz, pipeline.kron_apply)
@@ -239,6 +324,10 @@ def test_install_patches_every_by_name_binding(monkeypatch):
 
         for mod in (kronblur, ref_psf, pipeline, imaging):
             assert mod.blur_direct is kb.blur_direct
+        assert pipeline.decompose is kb.decompose and kronblur.kron.decompose is kb.decompose
+        assert pipeline._vec_ops is not None and hasattr(pipeline._vec_ops(
+            kb.decompose(random_psf(np.random.default_rng(2), 5), kb.BoundaryCondition.ZERO, s=1,
+                         shape=(8, 8)))[0], "_kb_power")
     finally:
         undo()
     assert (solvers.sfista, pipeline.sfista, pipeline.estimate_lipschitz, pipeline.kron_apply) == orig
