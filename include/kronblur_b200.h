@@ -118,9 +118,17 @@ int kb_apply_block(const kb_op* op, int adjoint, const void* X, void* Y, void* w
  * each on a local row block (same halo contract as kb_apply_block). */
 int kb_block_residual(const kb_op* op, const void* Yh, const void* B, void* R, void* work,
                       int g0, int m_global, int halo_lo, int halo_hi, void* stream);
+/* norms: optional device double[4] receiving this block's ||x_k - x_{k-1}||^2, ||x_{k-1}||^2,
+ * ||x_k||^2 (solvers.py:178-179); the sharded solver all-reduces them across ranks (sum) for
+ * history and rel_tol. NULL: no norms (the fast kernels). */
 int kb_block_update(const kb_op* op, const void* Rh, void* X, void* Y, void* work, int g0,
                     int m_global, int halo_lo, int halo_hi, double beta, int k, double L,
-                    double lam, int project, int* nonfinite, void* stream);
+                    double lam, int project, int* nonfinite, double* norms, void* stream);
+/* out2 (device double[2]) = { <a, b>, ||b||^2 } over `count` elements of dtype, fp64
+ * accumulation, deterministic; work: KB_RESID_NORMS_WORK bytes. The sharded power iteration's
+ * local reductions (solvers.py:124-125), all-reduced across ranks by the caller. */
+int kb_inner2(int dtype, const void* a, const void* b, long long count, double* out2, void* work,
+              void* stream);
 
 /*
  * Exact blur of `batch` float64 images — psf.py:170-193 (blur_direct), the `exact_apply` of
@@ -160,8 +168,10 @@ int kb_resid_norms(int dtype, const void* AX, const void* B, const void* X, cons
  * overwritten.
  */
 int kb_fma_peak(int dtype, float* tflops, void* stream);
-/* Arithmetic engine of each phase of the latest kb_time_passes on `op` (KB_ENGINE_*), so the
- * roofline of a phase divides by the peak of the instruction it actually issued. */
+/* Arithmetic engine (KB_ENGINE_*) of each phase {forward pass A, forward pass B, adjoint pass
+ * A, adjoint pass B} of the latest kb_sfista_run / kb_sfista_run_lams / kb_time_passes on `op`,
+ * so tests can assert which kernels ran and the roofline of a phase divides by the peak of the
+ * instruction it actually issued. */
 int kb_last_engines(const kb_op* op, int* engines4);
 /* Profiling timeline of the latest fp64 pass kernels launched with KB_DEBUG_MODE bit 7 set:
  * host[kind][block][slot] %globaltimer stamps (kind 0 split, 1 sum; 1024 blocks x 8 slots,

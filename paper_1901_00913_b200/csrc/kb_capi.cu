@@ -62,6 +62,7 @@ struct GraphCache {
   std::mutex mu;
   cudaGraphExec_t exec = nullptr;
   std::vector<unsigned char> key;
+  int engines[4] = {-1, -1, -1, -1};  // phase engines of the captured launches
 };
 
 }  // namespace
@@ -84,6 +85,10 @@ struct kb_op {
   unsigned* br_b_conv = nullptr;
   unsigned* br_b_corr = nullptr;
   GraphCache* graph = nullptr;
+  // > 1 for the strip / image-group views of an L2-blocked solve (sfista_blocked): engine
+  // selection then counts the chunks of the whole problem, not of one strip
+  long long chunk_scale = 1;
+  int slots_cap = 0;  // views: norm-partial slots of the parent's workspace (0: sum_blocks(op))
   // engines of the latest kb_time_passes phases (reporting only; written under g_phase_mu)
   mutable int phase_engine[4] = {0, 0, 0, 0};
 };
@@ -105,6 +110,7 @@ struct Ctx {
   int mirror = 0;  // the latest split pass stored Z^T's reflected halo rows
   int slots = 0;   // norm partial slots per image written by the latest sum pass
   int engine = 0;  // KB_ENGINE_* of the latest pass launch
+  int phase[4] = {-1, -1, -1, -1};  // engines of the call's four phases (split/sum fwd, adj)
 };
 
 // workspace: [Z: batch*r planes][R: batch planes][partials][scalars]
@@ -181,7 +187,8 @@ bool use_tc(const kb_op* op, const kb::AxisGeom& g, int min_kw) {
   const int pol = tc_policy(min_kw == 64 ? 1 : 2);
   if (!use_tma_f32(op) || pol == 0) return false;
   if (pol == 1) return true;
-  const long long chunks = (long long)((g.len + kb::kTcTS - 1) / kb::kTcTS) * ((g.other + 127) / 128) * op->batch;
+  const long long chunks =
+      (long long)((g.len + kb::kTcTS - 1) / kb::kTcTS) * ((g.other + 127) / 128) * op->batch * op->chunk_scale;
   // wide bands with enough chunks to occupy the SMs, or any band from 32 taps once there are
   // >= 8 chunks per SM (cfg3's 512-image batch, cfg5's 16384^2: 2x the mma.sync passes there)
   return (g.Kw >= min_kw && chunks >= 128) || (g.Kw >= 32 && chunks >= 8LL * sm_count());
@@ -551,7 +558,7 @@ int launch_b(const kb_op* op, Ctx& c, const T* z, const T* tin, const kb::AxisGe
       const long long nch = (long long)((g.len + kb::kTcTS - 1) / kb::kTcTS) * ((g.other + 127) / 128) * op->batch;
       const int nb = (int)std::min<long long>(sm_count(), nch);
       CUtensorMap mapt;
-      if (nst >= 3 && nb * kb::kTcSumEpi <= sum_blocks(op) &&
+      if (nst >= 3 && nb * kb::kTcSumEpi <= (op->slots_cap ? op->slots_cap : sum_blocks(op)) &&
           make_tmap(&mapt, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, kb::kTcRB, 4, 128)) {
         auto kern = MODE == kb::EPI_UPDATE && !e.want_norms ? kb::kb_pass_sum_tc<MODE, false> : kb::kb_pass_sum_tc<MODE>;
         KB_TRY(allow_smem(kern, smem));
@@ -680,6 +687,7 @@ int stage_a(const kb_op* op, int adjoint, const T* in, const Work& w, const RowB
     KB_CUDA(cudaMemsetAsync(w.z, 0, (size_t)z_plane(op) * op->r * op->batch * sizeof(T), s));
   KB_TRY(launch_a<T>(op, w.ctx, in, z, static_cast<const T*>(adjoint ? op->ta_corr : op->ta_conv), ga,
                      adjoint ? op->grp_adj : op->grp_fwd, nw2, mirror_h, msign, s));
+  w.ctx.phase[adjoint ? 2 : 0] = w.ctx.engine;
   if (adjoint && op->bc_a == KB_BC_REFLECTIVE && !op->sym_a && op->Ha > 0) {
     const long long z_ps = z_plane(op);
     dim3 grid((op->n + 127) / 128, 2 * op->Ha * op->r, op->batch);
@@ -708,8 +716,10 @@ int stage_b(const kb_op* op, int adjoint, kb::Epi<T> e, const Work& w, cudaStrea
     e.foldH = op->Hb;
   }
   const T* tsign = (adjoint && op->sym_b) ? static_cast<const T*>(op->sign_b) : nullptr;
-  return launch_b<T, MODE>(op, w.ctx, z, static_cast<const T*>(adjoint ? op->tb_corr : op->tb_conv), gb,
-                           tsign, e, s);
+  const int rc = launch_b<T, MODE>(op, w.ctx, z, static_cast<const T*>(adjoint ? op->tb_corr : op->tb_conv), gb,
+                                   tsign, e, s);
+  w.ctx.phase[adjoint ? 3 : 1] = w.ctx.engine;
+  return rc;
 }
 
 // ---- operator application (one direction) ------------------------------------------------
@@ -766,11 +776,173 @@ int update_t(const kb_op* op, const T* R, T* X, T* Y, const Work& w, const RowBl
   return KB_OK;
 }
 
+// ---- L2-blocked schedule of the fast path ------------------------------------------------
+// The two-sweep iteration writes r Z_i^T planes in pass A and reads them back in pass B. When
+// they do not fit in L2 (cfg3's 512-image batch: 2.2 GB; cfg5's 16384^2: 11 GB) that round trip
+// dominates DRAM traffic. The blocked schedule runs the same kernels on L2-sized pieces so each
+// piece's Z^T is consumed while it is still in L2:
+//  * batches: groups of whole images; per group residual then update (images are independent);
+//  * one image: row strips [r0, r0+S) viewed as row blocks (the multi-GPU halo machinery, the
+//    neighbouring strips' rows are the halo); strip s's update needs R of strip s+1 (axis-0 halo
+//    of the adjoint), so the order is res(0), res(1), upd(0), res(2), upd(1), ..., upd(N-1).
+// A piece is a shallow view of the operator (same device tables, offset per image group).
+struct BlockPlanC {
+  int pieces = 1;  // image groups or row strips
+  int size = 0;    // images per group / rows per strip
+  bool strips = false;
+};
+
+// Rows per strip / images per group: env KB_L2_STRIP / KB_L2_GROUP (0 = off; "auto" = the
+// largest piece whose Z^T set fits in the L2 budget, only when the whole set does not). OFF by
+// default: measured on the B200 (tools/l2_blocking_exp.py, profiles/README.md) the smaller
+// launches lose more to ramp/tail and wave quantisation than the L2 round trip saves
+// (cfg5: 14.6 -> 16.2-19.8 ms per iteration; cfg3: 3.14 -> 3.56-6.14 ms).
+BlockPlanC blocked_plan(const kb_op* op) {
+  BlockPlanC p;
+  const size_t zrow = (size_t)op->r * (op->n + 2 * op->Hb) * elem(op);  // Z^T bytes per image row
+  const size_t zimg = zrow * op->m;
+  static const long long budget = [] {
+    const char* v = std::getenv("KB_L2_BUDGET_MB");
+    return (v ? std::atoll(v) : 48LL) << 20;
+  }();
+  const char* es = std::getenv("KB_L2_STRIP");
+  const char* eg = std::getenv("KB_L2_GROUP");
+  if (op->batch > 1) {
+    if (!eg) return p;
+    int g = std::atoi(eg);
+    if (std::string(eg) == "auto") {
+      if (zimg * op->batch <= (size_t)budget * 2) return p;
+      g = (int)std::max<long long>(1, budget / (long long)zimg);
+    }
+    if (g <= 0 || g >= op->batch) return p;
+    p.size = g;
+    p.pieces = (op->batch + g - 1) / g;
+    return p;
+  }
+  if (!es) return p;
+  int S = std::atoi(es);
+  if (std::string(es) == "auto") {
+    if (zimg <= (size_t)budget * 2) return p;
+    S = (int)(budget / (long long)zrow) / 128 * 128;
+    if (S < 128) S = 128;
+  }
+  if (S <= 0 || S >= op->m || S < op->Ha) return p;
+  p.size = S;
+  p.pieces = (op->m + S - 1) / S;
+  p.strips = true;
+  return p;
+}
+
+// view of images [b0, b0+gb) of a batched operator
+kb_op group_view(const kb_op* op, int b0, int gb, long long scale) {
+  kb_op v = *op;
+  v.graph = nullptr;
+  v.slots_cap = sum_blocks(op);
+  v.batch = gb;
+  v.chunk_scale = scale;
+  const size_t e = elem(op);
+  auto off = [&](void* p, long long per_image_elems, size_t esz) -> void* {
+    return p ? static_cast<unsigned char*>(p) + (size_t)b0 * per_image_elems * esz : nullptr;
+  };
+  v.ta_conv = off(op->ta_conv, (long long)op->r * op->Wpa, e);
+  v.ta_corr = off(op->ta_corr, (long long)op->r * op->Wpa, e);
+  v.tb_conv = off(op->tb_conv, (long long)op->r * op->Wpb, e);
+  v.tb_corr = off(op->tb_corr, (long long)op->r * op->Wpb, e);
+  v.sign_b = off(op->sign_b, op->r, e);
+  const long long ka = (2 * op->Ha + 1 + 3) / 4 * 4, kbw = (2 * op->Hb + 1 + 3) / 4 * 4;
+  const long long bra = (long long)op->r * kb::tc_bricks((int)ka) * 256;
+  const long long brb = (long long)op->r * kb::tc_bricks((int)kbw) * 256;
+  v.br_a_conv = static_cast<unsigned*>(off(op->br_a_conv, bra, sizeof(unsigned)));
+  v.br_a_corr = static_cast<unsigned*>(off(op->br_a_corr, bra, sizeof(unsigned)));
+  v.br_b_conv = static_cast<unsigned*>(off(op->br_b_conv, brb, sizeof(unsigned)));
+  v.br_b_corr = static_cast<unsigned*>(off(op->br_b_corr, brb, sizeof(unsigned)));
+  return v;
+}
+
+// view of a row strip of height S of a single-image operator
+kb_op strip_view(const kb_op* op, int S, long long scale) {
+  kb_op v = *op;
+  v.graph = nullptr;
+  v.slots_cap = sum_blocks(op);
+  v.m = S;
+  v.chunk_scale = scale;
+  return v;
+}
+
+template <typename T>
+int sfista_blocked(const kb_op* op, const BlockPlanC& p, const T* B, T* X, T* Y, const Work& w,
+                   const double* beta, int k0, int iters, int project, int* nonfinite, cudaStream_t s) {
+  T* R = static_cast<T*>(w.rp);
+  const long long pe = (long long)plane_elems(op);
+  if (!p.strips) {
+    for (int it = 0; it < iters; ++it) {
+      const int k = k0 + it + 1;
+      for (int g = 0; g < p.pieces; ++g) {
+        const int b0 = g * p.size, gb = std::min(p.size, op->batch - b0);
+        const kb_op v = group_view(op, b0, gb, p.pieces);
+        Work wv = w;
+        const long long o = (long long)b0 * pe;
+        const RowBlock rb{0, op->m, 0, 0};
+        KB_TRY(residual_t<T>(&v, Y + o, B + o, R + o, wv, rb, s));
+        KB_TRY(update_t<T>(&v, R + o, X + o, Y + o, wv, rb, beta[k - 1], k, w.scal + b0,
+                           w.scal + op->batch + b0, project, nonfinite, nullptr, s));
+        for (int i = 0; i < 4; ++i) w.ctx.phase[i] = wv.ctx.phase[i];
+      }
+    }
+    return KB_OK;
+  }
+  const int N = p.pieces, S = p.size;
+  auto piece = [&](int i, int& r0, int& rows, RowBlock& rb) {
+    r0 = i * S;
+    rows = std::min(S, op->m - r0);
+    rb = RowBlock{r0, op->m, r0 > 0 ? op->Ha : 0, r0 + rows < op->m ? op->Ha : 0};
+  };
+  auto res = [&](int i) -> int {
+    int r0, rows;
+    RowBlock rb;
+    piece(i, r0, rows, rb);
+    const kb_op v = strip_view(op, rows, N);
+    Work wv = w;
+    const long long o = (long long)r0 * op->n;
+    const int rc = residual_t<T>(&v, Y + o, B + o, R + o, wv, rb, s);
+    w.ctx.phase[0] = wv.ctx.phase[0];
+    w.ctx.phase[1] = wv.ctx.phase[1];
+    return rc;
+  };
+  auto upd = [&](int i, int k) -> int {
+    int r0, rows;
+    RowBlock rb;
+    piece(i, r0, rows, rb);
+    const kb_op v = strip_view(op, rows, N);
+    Work wv = w;
+    const long long o = (long long)r0 * op->n;
+    const int rc = update_t<T>(&v, R + o, X + o, Y + o, wv, rb, beta[k - 1], k, w.scal, w.scal + 1, project,
+                               nonfinite, nullptr, s);
+    w.ctx.phase[2] = wv.ctx.phase[2];
+    w.ctx.phase[3] = wv.ctx.phase[3];
+    return rc;
+  };
+  for (int it = 0; it < iters; ++it) {
+    const int k = k0 + it + 1;
+    KB_TRY(res(0));
+    for (int i = 0; i + 1 < N; ++i) {
+      KB_TRY(res(i + 1));
+      KB_TRY(upd(i, k));
+    }
+    KB_TRY(upd(N - 1, k));
+  }
+  return KB_OK;
+}
+
 template <typename T>
 int sfista_launches(const kb_op* op, const T* B, T* X, T* Y, const Work& w, const double* beta,
                     int k0, int iters, int project, int* nonfinite, double* norms,
                     cudaStream_t s) {
   T* R = static_cast<T*>(w.rp);
+  if (!norms) {
+    const BlockPlanC p = blocked_plan(op);
+    if (p.pieces > 1) return sfista_blocked<T>(op, p, B, X, Y, w, beta, k0, iters, project, nonfinite, s);
+  }
   const RowBlock rb{0, op->m, 0, 0};
   for (int it = 0; it < iters; ++it) {
     const int k = k0 + it + 1;
@@ -1242,7 +1414,7 @@ int kb_block_residual(const kb_op* op, const void* Yh, const void* B, void* R, v
 
 int kb_block_update(const kb_op* op, const void* Rh, void* X, void* Y, void* work, int g0,
                     int m_global, int halo_lo, int halo_hi, double beta, int k, double L,
-                    double lam, int project, int* nonfinite, void* stream) {
+                    double lam, int project, int* nonfinite, double* norms, void* stream) {
   KB_TRY(check_op(op));
   if (op->batch != 1) return fail(KB_ERR_ARGUMENT, "row-block update needs batch == 1");
   if (g0 < 0 || g0 + op->m > m_global || halo_lo < 0 || halo_hi < 0)
@@ -1252,8 +1424,8 @@ int kb_block_update(const kb_op* op, const void* Rh, void* X, void* Y, void* wor
   const double host[2] = {L, L + lam * lam};
   KB_CUDA(cudaMemcpyAsync(w.scal, host, sizeof(host), cudaMemcpyHostToDevice, s));
   if (op->dtype == KB_F64)
-    return update_t<double>(op, static_cast<const double*>(Rh), static_cast<double*>(X), static_cast<double*>(Y), w, RowBlock{g0, m_global, halo_lo, halo_hi}, beta, k, w.scal, w.scal + 1, project, nonfinite, nullptr, s);
-  return update_t<float>(op, static_cast<const float*>(Rh), static_cast<float*>(X), static_cast<float*>(Y), w, RowBlock{g0, m_global, halo_lo, halo_hi}, beta, k, w.scal, w.scal + 1, project, nonfinite, nullptr, s);
+    return update_t<double>(op, static_cast<const double*>(Rh), static_cast<double*>(X), static_cast<double*>(Y), w, RowBlock{g0, m_global, halo_lo, halo_hi}, beta, k, w.scal, w.scal + 1, project, nonfinite, norms, s);
+  return update_t<float>(op, static_cast<const float*>(Rh), static_cast<float*>(X), static_cast<float*>(Y), w, RowBlock{g0, m_global, halo_lo, halo_hi}, beta, k, w.scal, w.scal + 1, project, nonfinite, norms, s);
 }
 
 namespace {
@@ -1303,7 +1475,16 @@ int sfista_run_impl(const kb_op* op, const void* B, void* X, void* Y, void* work
     return sfista_launches<float>(op, static_cast<const float*>(B), static_cast<float*>(X),
                                   static_cast<float*>(Y), w, beta, k0, iters, project, nonfinite, norms, cs);
   };
-  if (!use_graph) return body(s);
+  auto publish = [&](const int* eng) {
+    std::lock_guard<std::mutex> lock(g_phase_mu);
+    for (int i = 0; i < 4; ++i)
+      if (eng[i] >= 0) op->phase_engine[i] = eng[i];
+  };
+  if (!use_graph) {
+    const int rc = body(s);
+    if (rc == KB_OK) publish(w.ctx.phase);
+    return rc;
+  }
 
   // graph path: key = every pointer and scalar the captured launches bake in
   std::vector<unsigned char> key;
@@ -1345,8 +1526,10 @@ int sfista_run_impl(const kb_op* op, const void* B, void* X, void* Y, void* work
       return fail(KB_ERR_CUDA, std::string("instantiate: ") + cudaGetErrorString(ce));
     }
     gc->key = key;
+    for (int i = 0; i < 4; ++i) gc->engines[i] = w.ctx.phase[i];
   }
   KB_CUDA(cudaGraphLaunch(gc->exec, s));
+  publish(gc->engines);
   return KB_OK;
 }
 }  // namespace
@@ -1405,6 +1588,23 @@ int kb_resid_norms(int dtype, const void* AX, const void* B, const void* X, cons
     kb::kb_resid_norms_k<float><<<kb::kNormBlocks, kb::kNormThreads, 0, s>>>(
         static_cast<const float*>(AX), static_cast<const float*>(B), static_cast<const float*>(X),
         static_cast<const float*>(truth), count, partial);
+  kb::kb_resid_norms_finish<<<1, 32, 0, s>>>(partial, kb::kNormBlocks, out2);
+  KB_CUDA(cudaGetLastError());
+  return KB_OK;
+}
+
+int kb_inner2(int dtype, const void* a, const void* b, long long count, double* out2, void* work,
+              void* stream) {
+  if (!a || !b || !out2 || !work || count < 0) return fail(KB_ERR_ARGUMENT, "bad kb_inner2 arguments");
+  if (dtype != KB_F64 && dtype != KB_F32) return fail(KB_ERR_ARGUMENT, "unknown dtype");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* partial = static_cast<double*>(work);
+  if (dtype == KB_F64)
+    kb::kb_inner2_k<double><<<kb::kNormBlocks, kb::kNormThreads, 0, s>>>(
+        static_cast<const double*>(a), static_cast<const double*>(b), count, partial);
+  else
+    kb::kb_inner2_k<float><<<kb::kNormBlocks, kb::kNormThreads, 0, s>>>(
+        static_cast<const float*>(a), static_cast<const float*>(b), count, partial);
   kb::kb_resid_norms_finish<<<1, 32, 0, s>>>(partial, kb::kNormBlocks, out2);
   KB_CUDA(cudaGetLastError());
   return KB_OK;

@@ -53,4 +53,34 @@ __global__ void kb_resid_norms_finish(const double* __restrict__ partial, int nb
   }
 }
 
+// <a, b> and ||b||^2 over `count` elements, fp64 accumulation, deterministic (the sharded power
+// iteration's local reductions, solvers.py:124-125, all-reduced across ranks by the caller).
+template <typename T>
+__global__ void __launch_bounds__(kNormThreads)
+kb_inner2_k(const T* __restrict__ a, const T* __restrict__ b, long long count, double* __restrict__ partial) {
+  double s0 = 0.0, s1 = 0.0;
+  for (long long i = (long long)blockIdx.x * kNormThreads + threadIdx.x; i < count;
+       i += (long long)gridDim.x * kNormThreads) {
+    const double bv = (double)b[i];
+    s0 += (double)a[i] * bv;
+    s1 += bv * bv;
+  }
+  __shared__ double red[kNormThreads / 32][2];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5][0] = s0;
+    red[threadIdx.x >> 5][1] = s1;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double s = 0.0;
+    for (int w = 0; w < kNormThreads / 32; ++w) s += red[w][threadIdx.x];
+    partial[2 * blockIdx.x + threadIdx.x] = s;
+  }
+}
+
 }  // namespace kb

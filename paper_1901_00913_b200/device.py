@@ -87,8 +87,9 @@ EXPORTS = {
     "kb_block_update": (
         _c_int,
         [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _c_double,
-         _c_double, _c_int, _vp, _vp],
+         _c_double, _c_int, _vp, _vp, _vp],
     ),
+    "kb_inner2": (_c_int, [_c_int, _vp, _vp, ctypes.c_longlong, _vp, _vp, _vp]),
 }
 
 
@@ -427,7 +428,8 @@ class DeviceOperator:
             return [float(v) for v in ms]
 
     def last_engines(self) -> list:
-        """Engine names of the four phases of the latest time_passes (kb_last_engines)."""
+        """Engine names of the four phases {split fwd, sum fwd, split adj, sum adj} of the latest
+        sfista_run or time_passes on this operator (kb_last_engines)."""
         out = (ctypes.c_int * 4)()
         _check(load_library().kb_last_engines(self._handle, out), "kb_last_engines")
         return [ENGINES.get(int(v), str(int(v))) for v in out]

@@ -38,6 +38,17 @@ for row in data:
             except ValueError:
                 pass
     stalls.sort(reverse=True)
+    # tensor-pipe evidence (tcgen05 / DMMA / HMMA issue and activity): every pct-of-peak metric
+    # whose name mentions the tensor pipes, so the summary shows tensor utilisation directly
+    tens = []
+    for k, v in d.items():
+        lk = k.lower()
+        if (("pipe_tensor_cycles_active" in lk or "inst_executed_pipe_tc.avg" in lk
+             or "inst_executed_pipe_tmem.avg" in lk or "subpipe_hmma.avg" in lk or "subpipe_dmma.avg" in lk)
+                and "pct" in lk and v not in ("", "n/a")):
+            tens.append(f"{k.replace('TPC.TriageCompute.', '')}={v}")
     print(name)
     print("   ", " ".join(parts))
+    if tens:
+        print("    tensor:", " ".join(sorted(tens)))
     print("    stalls:", ", ".join(f"{n}={v:.2f}" for v, n in stalls[:6]))

@@ -13,7 +13,9 @@ import subprocess
 import sys
 
 rep, dtype = sys.argv[1], sys.argv[2]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+# REPORT may also be the saved `ncu -i REPORT --page raw --csv` text (*.csv)
+raw = open(rep).read() if rep.endswith(".csv") else subprocess.run(
+    ["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
 hdr, units, data = rows[0], rows[1], rows[2:]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
