@@ -39,6 +39,7 @@ extern "C" {
 #define KB_ENGINE_DMMA 2     /* persistent FP64 tensor-core DMMA kernels */
 #define KB_ENGINE_MMA_TF32 3 /* persistent 3xTF32 mma.sync kernels */
 #define KB_ENGINE_TC_TF32 4  /* tcgen05 3xTF32 kernels (tensor-memory accumulators) */
+#define KB_ENGINE_PERSIST_F64 5 /* whole-solve persistent fp64 kernel (small images, one launch) */
 
 #define KB_BC_ZERO 0
 #define KB_BC_REFLECTIVE 1

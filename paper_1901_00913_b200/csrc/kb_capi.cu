@@ -26,6 +26,7 @@
 #include "kb_tc.cuh"
 #include "kb_blur.cuh"
 #include "kb_norms.cuh"
+#include "kb_persist.cuh"
 
 namespace {
 
@@ -1451,6 +1452,78 @@ int kb_sfista_run_lams(const kb_op* op, const void* B, void* X, void* Y, void* w
 }  // extern "C"
 
 namespace {
+// Whole-solve persistent kernel (kb_persist.cuh) for small fp64 single images: one cooperative
+// launch runs every iteration with two grid barriers each. KB_PERSIST=0 disables it, =1 uses it
+// whenever it fits; by default it takes images up to 512^2 (cfg1: launch-bound otherwise).
+struct PsPlan {
+  int RB = 0, nblk = 0;
+  size_t smem = 0;
+};
+PsPlan persist_plan(const kb_op* op) {
+  PsPlan p;
+  static const int mode = [] {
+    const char* v = std::getenv("KB_PERSIST");
+    return v ? std::atoi(v) : -1;
+  }();
+  if (mode == 0 || op->dtype != KB_F64 || op->batch != 1) return p;
+  if (mode < 0 && (long long)op->m * op->n > 512LL * 512) return p;
+  const int sms = sm_count();
+  int RB = (op->m + sms - 1) / sms;
+  const size_t smem = kb::ps_smem_bytes(RB, op->Ha, op->n, op->r, op->Wpa, op->Wpb);
+  if (smem > 200 * 1024) return p;
+  if (allow_smem(kb::kb_solve_persistent, smem) != KB_OK) return p;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kb::kb_solve_persistent, kb::kPsThreads, smem) !=
+          cudaSuccess ||
+      per_sm < 1)
+    return p;
+  p.RB = RB;
+  p.nblk = (op->m + RB - 1) / RB;
+  p.smem = smem;
+  return p;
+}
+
+int launch_persist(const kb_op* op, const PsPlan& pp, const double* B, double* X, double* Y, const Work& w,
+                   const double* beta, int k0, int iters, double L, double lam, int project, int* nonfinite,
+                   cudaStream_t s) {
+  // beta_k go to the (unused on this path) norm-partials region of the workspace
+  const int cap = (int)(4 * (size_t)op->batch * sum_blocks(op));
+  for (int done = 0; done < iters;) {
+    const int cnt = std::min(iters - done, cap);
+    KB_CUDA(cudaMemcpyAsync(w.partials, beta + k0 + done, sizeof(double) * cnt, cudaMemcpyHostToDevice, s));
+    kb::PsArgs a;
+    a.B = B;
+    a.X = X;
+    a.Y = Y;
+    a.R = static_cast<double*>(w.rp);
+    a.ha = static_cast<const double*>(op->ta_conv);
+    a.kbt = static_cast<const double*>(op->tb_conv);
+    a.beta = w.partials;
+    a.nonfinite = nonfinite;
+    a.L = L;
+    a.denom = L + lam * lam;
+    a.m = op->m;
+    a.n = op->n;
+    a.r = op->r;
+    a.Ha = op->Ha;
+    a.Hb = op->Hb;
+    a.Wpa = op->Wpa;
+    a.Wpb = op->Wpb;
+    a.refl_a = op->bc_a == KB_BC_REFLECTIVE;
+    a.refl_b = op->bc_b == KB_BC_REFLECTIVE;
+    a.RB = pp.RB;
+    a.k0 = k0 + done;
+    a.iters = cnt;
+    a.project = project;
+    void* args[] = {&a};
+    KB_CUDA(cudaLaunchCooperativeKernel((const void*)kb::kb_solve_persistent, dim3(pp.nblk), dim3(kb::kPsThreads),
+                                        args, pp.smem, s));
+    done += cnt;
+  }
+  for (int i = 0; i < 4; ++i) w.ctx.phase[i] = KB_ENGINE_PERSIST_F64;
+  return KB_OK;
+}
+
 int sfista_run_impl(const kb_op* op, const void* B, void* X, void* Y, void* work, const double* beta, int k0,
                     int iters, const double* L, const double* lam, int lam_per_image, int project,
                     int* nonfinite, double* norms, int use_graph, void* stream) {
@@ -1480,6 +1553,15 @@ int sfista_run_impl(const kb_op* op, const void* B, void* X, void* Y, void* work
     for (int i = 0; i < 4; ++i)
       if (eng[i] >= 0) op->phase_engine[i] = eng[i];
   };
+  if (!norms) {
+    const PsPlan pp = persist_plan(op);
+    if (pp.nblk > 0) {  // one launch for the whole solve: no graph needed
+      const int rc = launch_persist(op, pp, static_cast<const double*>(B), static_cast<double*>(X),
+                                    static_cast<double*>(Y), w, beta, k0, iters, L[0], lam[0], project, nonfinite, s);
+      if (rc == KB_OK) publish(w.ctx.phase);
+      return rc;
+    }
+  }
   if (!use_graph) {
     const int rc = body(s);
     if (rc == KB_OK) publish(w.ctx.phase);

@@ -22,7 +22,7 @@ from paper_1901_00913_b200 import shard  # noqa: E402
 from oracle import kronblur_port as port  # noqa: E402
 
 
-def emulate_row_blocks(op, B, L, lam, iters, world, dtype="float64"):
+def emulate_row_blocks(op, B, L, lam, iters, world, dtype="float64", split=False):
     m, n = op.shape
     h = shard.halo_rows(op)
     plans = [shard.BlockPlan(m=m, n=n, world=world, rank=r, h=h) for r in range(world)]
@@ -35,6 +35,11 @@ def emulate_row_blocks(op, B, L, lam, iters, world, dtype="float64"):
     flag = torch.full((1,), 2**31 - 1, dtype=torch.int32, device="cuda")
     _, beta = kb.momentum_table(iters)
 
+    def ranges(p):
+        if not split:
+            return [(0, p.rows)]
+        return [(h, p.rows - h), (0, h), (p.rows - h, p.rows)]
+
     def exchange(bufs):
         for r, p in enumerate(plans):
             if p.prev is not None:
@@ -45,10 +50,12 @@ def emulate_row_blocks(op, B, L, lam, iters, world, dtype="float64"):
     for k in range(1, iters + 1):
         exchange(Yh)
         for r in range(world):
-            backs[r].residual(Yh[r], Bl[r], Rh[r])
+            for r0, r1 in ranges(plans[r]):  # split=True: the overlap path's interior + edge strips
+                backs[r].residual(Yh[r], Bl[r], Rh[r], r0, r1)
         exchange(Rh)
         for r in range(world):
-            backs[r].update(Rh[r], X[r], Yh[r], beta[k - 1], k, L, lam, True, flag)
+            for r0, r1 in ranges(plans[r]):
+                backs[r].update(Rh[r], X[r], Yh[r], beta[k - 1], k, L, lam, True, flag, r0, r1)
     torch.cuda.synchronize()
     assert int(flag.item()) > iters
     return torch.cat(X).double().cpu().numpy()
@@ -116,3 +123,74 @@ def test_batch_shard_partition_covers_all_images(rng):
     for i in range(5):
         want, _ = port.sfista(ops[i], Bs[i], 1.2, 0.02, 15, project=True)
         np.testing.assert_allclose(xs[i], want, rtol=0, atol=1e-10 * np.abs(want).max())
+
+
+@pytest.mark.parametrize("bc", ["zero", "reflective"])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_overlap_sub_ranges_match_whole_blocks(bc, dtype, rng):
+    """The overlap schedule computes each block as interior rows [h, rows-h) then the two h-row
+    edge strips; the result must equal the whole-block computation."""
+    psf = random_psf(rng, 11)
+    op = kb.decompose(psf, kb.BoundaryCondition(bc), s=3, shape=(120, 120))
+    B = rng.random((120, 120))
+    whole = emulate_row_blocks(op, B, 1.4, 0.03, 12, 2, dtype)
+    split = emulate_row_blocks(op, B, 1.4, 0.03, 12, 2, dtype, split=True)
+    tol = 1e-12 if dtype == "float64" else 1e-6
+    np.testing.assert_allclose(split, whole, rtol=0, atol=tol * np.abs(whole).max())
+
+
+def test_single_rank_history_and_power_match_unsharded(rng):
+    """world = 1: solve_row_blocks with record_history (device block norms, kb_resid_norms) and
+    the sharded power iteration (kb_apply_block, kb_inner2) reproduce sfista's history and
+    estimate_lipschitz."""
+    from paper_1901_00913_b200.solvers import _start_vector
+
+    psf = random_psf(rng, 9)
+    op = kb.decompose(psf, kb.BoundaryCondition.REFLECTIVE, s=3, shape=(64, 64))
+    B = rng.random((64, 64))
+    plan = shard.BlockPlan(m=64, n=64, world=1, rank=0, h=shard.halo_rows(op))
+    be = shard.DeviceBlockBackend(op, plan, "float64")
+    L = shard.power_iter_row_blocks(be, plan, torch.from_numpy(_start_vector(4, 64, 64, "matrix")).cuda(), 50)
+    assert L == pytest.approx(kb.lipschitz(op, iters=50, seed=4), rel=1e-12)
+    X, hist = shard.solve_row_blocks(be, plan, torch.from_numpy(B).cuda(), L, 0.03, 15, project=True,
+                                     record_history=True)
+    run = kb.sfista(op, B, kb.SolveConfig(lam=0.03, lipschitz=L, max_iter=15, record_history=True),
+                    options=kb.SolveOptions(dtype="float64", project=True))
+    assert len(hist) == len(run.history) == 15
+    for h, r in zip(hist, run.history):
+        assert h["objective"] == pytest.approx(r.objective, rel=1e-11)
+    np.testing.assert_allclose(X.cpu().numpy(), run.x, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_l2_blocked_schedule_is_bit_identical(dtype, monkeypatch, rng):
+    """The opt-in L2-blocked schedule (KB_L2_STRIP rows per strip / KB_L2_GROUP images per group,
+    kb_capi.cu sfista_blocked) runs the same kernels on pieces: results are bit-identical to the
+    whole-plane schedule when strips are multiples of the 64-row chunk."""
+    from paper_1901_00913_b200.device import INT_MAX, DeviceOperator, device_operator
+
+    psf = random_psf(rng, 15)
+    op = kb.decompose(psf, kb.BoundaryCondition.REFLECTIVE, s=4, shape=(1024, 1024))
+    B = torch.from_numpy(rng.random((1024, 1024))).cuda()
+    dev = device_operator(op, dtype)
+    _, beta = kb.momentum_table(6)
+    outs = {}
+    for strip in ("0", "128", "256"):
+        monkeypatch.setenv("KB_L2_STRIP", strip)
+        X, Y = torch.zeros_like(B, dtype=dev.tdtype), torch.zeros_like(B, dtype=dev.tdtype)
+        flag = torch.full((1,), INT_MAX, dtype=torch.int32, device="cuda")
+        dev.sfista_run(B.to(dev.tdtype), X, Y, beta, 0, 6, 1.2, 0.02, True, flag)
+        outs[strip] = X.cpu()
+    assert torch.equal(outs["0"], outs["128"]) and torch.equal(outs["0"], outs["256"])
+    ops = [kb.decompose(random_psf(rng, 7), kb.BoundaryCondition.ZERO, s=2, shape=(128, 128)) for _ in range(7)]
+    devb = DeviceOperator(ops, dtype)
+    Bb = torch.from_numpy(rng.random((7, 128, 128))).cuda().to(devb.tdtype)
+    Ls = np.linspace(1.1, 1.3, 7)
+    res = {}
+    for group in ("0", "3"):
+        monkeypatch.setenv("KB_L2_GROUP", group)
+        X, Y = torch.zeros_like(Bb), torch.zeros_like(Bb)
+        flag = torch.full((1,), INT_MAX, dtype=torch.int32, device="cuda")
+        devb.sfista_run(Bb, X, Y, beta, 0, 6, Ls, 0.02, True, flag)
+        res[group] = X.cpu()
+    assert torch.equal(res["0"], res["3"])

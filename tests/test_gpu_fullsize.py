@@ -149,3 +149,20 @@ def test_full_size_against_live_oracle(name, dtype, iters):
         ref5, _ = port.sfista(op, Bin, L, cfg.lam, 5, project=True)
         got5, _ = solve(op, Bin, L, cfg, dtype, 5)
         assert rel(got5, ref5) <= TOL[dtype]
+
+
+def test_cfg1_against_the_references_own_solution():
+    """cfg1 (256^2 fp64, zero BC, w=31, r=3, lam=0.02, 100 it) with the reference's own factors,
+    data and L (tests/golden/cfg1.npz, written by running kronblur itself): the GPU solve -- the
+    whole-solve persistent kernel at this size -- reproduces the reference's projected solution
+    and, without projection, kronblur.sfista's own x."""
+    g = np.load(os.path.join(GOLDEN, "cfg1.npz"))
+    terms = tuple(kb.KronTerm(sigma=1.0, H=kb.toep(g["H_c"][i], int(g["H_j"])), K=kb.toep(g["K_c"][i], int(g["K_j"])))
+                  for i in range(g["H_c"].shape[0]))
+    op = kb.KronOperator(terms=terms, shape=(256, 256), bc=kb.BoundaryCondition.ZERO, sigma=np.ones(len(terms)),
+                         s=len(terms), rank=len(terms), eps=0.0)
+    cfg = kb.SolveConfig(lam=0.02, lipschitz=float(g["L"]), max_iter=100, record_history=False)
+    for project, want in ((True, g["x_proj"]), (False, g["x_sfista"])):
+        run = kb.sfista(op, g["B"], cfg, options=kb.SolveOptions(dtype="float64", project=project))
+        assert rel(run.x, want) <= 1e-10
+    assert device_operator(op, "float64").last_engines() == ["persist_f64"] * 4
