@@ -35,7 +35,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CFG = "cfg5"
-VARIANTS = (("cfg2", "float64"), ("cfg2", "float32"), ("cfg3", "float32"), ("cfg4", "float32"))
+VARIANTS = (("cfg1", "float64"), ("cfg2", "float64"), ("cfg2", "float32"), ("cfg3", "float32"), ("cfg4", "float32"))
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
@@ -343,6 +343,16 @@ def measure_config(name, dtype, steps, warmup, rank, world, local, clocks=False,
         "nominal_flops_per_px_it": algorithmic(cfg),
         "executed_taps": [wa, wb],
     }
+    if engines_solve and engines_solve[0] == "persist_f64":
+        # one cooperative launch runs the whole solve: its roofline is the solve's own rate
+        per_it_s = ms * 1e-3 / iters
+        ach = sum(flops_phase) / per_it_s / 1e12
+        pk, src = engine_peak("dmma")
+        res["roofline"].update({
+            "kernel": "kb_solve_persistent (whole solve in one cooperative launch, 2 grid barriers per iteration)",
+            "achieved": round(ach, 3), "peak": round(pk, 3), "frac": round(ach / pk, 4),
+            "flops_per_launch": sum(flops_phase) * iters,
+            "peak_source": "measured live by kb_fma_peak in this run: " + src + " (FP64 FMA has the same nominal rate)"})
     res["dev"] = dev
     del Bd, Xd, Yd, flush
     return res

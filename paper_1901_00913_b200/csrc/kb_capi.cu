@@ -1465,7 +1465,7 @@ PsPlan persist_plan(const kb_op* op) {
     const char* v = std::getenv("KB_PERSIST");
     return v ? std::atoi(v) : -1;
   }();
-  if (mode == 0 || op->dtype != KB_F64 || op->batch != 1) return p;
+  if (mode == 0 || op->dtype != KB_F64 || op->batch != 1 || op->n % 2) return p;
   if (mode < 0 && (long long)op->m * op->n > 512LL * 512) return p;
   const int sms = sm_count();
   int RB = (op->m + sms - 1) / sms;
@@ -1553,7 +1553,7 @@ int sfista_run_impl(const kb_op* op, const void* B, void* X, void* Y, void* work
     for (int i = 0; i < 4; ++i)
       if (eng[i] >= 0) op->phase_engine[i] = eng[i];
   };
-  if (!norms) {
+  if (!norms && al16(B) && al16(X) && al16(Y) && al16(w.rp)) {
     const PsPlan pp = persist_plan(op);
     if (pp.nblk > 0) {  // one launch for the whole solve: no graph needed
       const int rc = launch_persist(op, pp, static_cast<const double*>(B), static_cast<double*>(X),

@@ -67,18 +67,27 @@ __global__ void __launch_bounds__(kPsThreads) kb_solve_persistent(PsArgs a) {
   const int r0 = blockIdx.x * a.RB;
   const int r1 = min(m, r0 + a.RB), nr = max(0, r1 - r0);
 
-  // stage rows [r0 - Ha, r1 + Ha) of `src` (out-of-domain rows read as zero; the rules map)
+  // stage rows [r0 - Ha, r1 + Ha) of `src` (out-of-domain rows read as zero; the rules map):
+  // every pair of elements is an independent 16-byte cp.async, so all of a thread's loads are in
+  // flight at once (a load -> store loop serialises ~30 L2 round trips per phase). `.cg` reads
+  // through to L2: the rows were written by other CTAs since this SM last read them, and L1 is
+  // not coherent across SMs (n is even: persist_plan requires it).
   auto stage = [&](const double* src) {
-    for (int t = 0; t < nr + 2 * Ha; ++t) {
+    const int rows = nr + 2 * Ha, half = n >> 1;
+    for (int idx = tid; idx < rows * half; idx += kPsThreads) {
+      const int t = idx / half, c = 2 * (idx - t * half);
       const int g = r0 - Ha + t;
-      double* dst = Ys + (size_t)t * n;
+      double* dst = Ys + (size_t)t * n + c;
       if (g >= 0 && g < m) {
-        const double* s = src + (size_t)g * n;
-        for (int c = tid; c < n; c += kPsThreads) dst[c] = s[c];
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)),
+                     "l"(src + (size_t)g * n + c)
+                     : "memory");
       } else {
-        for (int c = tid; c < n; c += kPsThreads) dst[c] = 0.0;
+        dst[0] = 0.0;
+        dst[1] = 0.0;
       }
     }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
   };
   // axis-0 pass on the staged rows: Z_i[t][c] for the CTA's rows
   auto axis0 = [&](bool adjoint) {

@@ -30,7 +30,10 @@ namespace kb {
 constexpr int kTcTS = 64;        // outputs (S rows) per chunk: 4 N-blocks of 16
 constexpr int kTcRB = 32;        // input rows per ring stage (4 K-steps)
 constexpr int kTcStagesMax = 8;  // tensor-memory A stages (2 K-steps: hi 16 + lo 16 columns each)
-constexpr int kTcRingMax = 8;    // shared-memory tile ring depth (runtime nst <= this)
+#ifndef KB_TC_RING_MAX
+#define KB_TC_RING_MAX 8
+#endif
+constexpr int kTcRingMax = KB_TC_RING_MAX;  // shared-memory tile ring depth (runtime nst <= this)
 constexpr int kTcG = 3;          // terms per group (two accumulator sets of kTcG x 64 columns)
 constexpr int kTcIssuers = 4;    // one MMA-issuing warp per N-block
 constexpr int kTcConv = 1 + kTcIssuers, kTcEpi = kTcConv + 8;  // first converter / epilogue warp

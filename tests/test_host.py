@@ -331,3 +331,28 @@ def test_install_patches_every_by_name_binding(monkeypatch):
     finally:
         undo()
     assert (solvers.sfista, pipeline.sfista, pipeline.estimate_lipschitz, pipeline.kron_apply) == orig
+
+
+def test_product_never_imports_the_oracle_or_the_reference():
+    """The oracle is test infrastructure and the reference is test-only data: nothing in the
+    product package imports oracle/ or kronblur (other than errors.py reusing kronblur's error
+    classes when kronblur is already importable, and dropin.py patching a module it is handed)."""
+    import ast
+    import glob
+
+    pkg = os.path.join(ROOT, "paper_1901_00913_b200")
+    for path in glob.glob(os.path.join(pkg, "*.py")):
+        tree = ast.parse(open(path).read())
+        for node in ast.walk(tree):
+            names = []
+            if isinstance(node, ast.Import):
+                names = [a.name for a in node.names]
+            elif isinstance(node, ast.ImportFrom):
+                names = [node.module or ""]
+            for name in names:
+                assert not name.startswith("oracle"), (path, name)
+                if name.startswith("kronblur"):
+                    assert os.path.basename(path) == "errors.py", (path, name)
+    # and the compute path fails loudly without the native library
+    src = open(os.path.join(pkg, "device.py")).read()
+    assert "no CPU fallback" in src
