@@ -9,9 +9,9 @@ Every array here comes from kronblur (the reference) except where noted: the pro
 the reference's own kron_apply / kron_apply_adjoint / momentum_next inside a restatement of
 solvers._engine with np.maximum(x, 0) after line 171 (the reference has no projection, SURVEY F2);
 without the clamp that restatement reproduces kronblur.sfista bit for bit (checked below).
-Large-config fixtures (cfg2/cfg4) store a fixed random subsample of the solution plus norms,
-computed with the numpy port (oracle/kronblur_port.py), which is itself pinned to the reference by
-the small fixtures (it reproduces kron_apply bit for bit).
+Full-size fixtures of the BASELINE configs (cfg2-cfg5) come from tests/golden/make_fullsize.py
+(the C restatement oracle/kb_oracle.c, itself pinned to these reference fixtures by
+tests/test_oracle_c.py), not from this script.
 """
 
 from __future__ import annotations
