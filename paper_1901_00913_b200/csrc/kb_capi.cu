@@ -1468,8 +1468,27 @@ PsPlan persist_plan(const kb_op* op) {
   if (mode == 0 || op->dtype != KB_F64 || op->batch != 1 || op->n % 2) return p;
   if (mode < 0 && (long long)op->m * op->n > 512LL * 512) return p;
   const int sms = sm_count();
-  int RB = (op->m + sms - 1) / sms;
-  const size_t smem = kb::ps_smem_bytes(RB, op->Ha, op->n, op->r, op->Wpa, op->Wpb);
+  static const int rb_env = [] {
+    const char* v = std::getenv("KB_PERSIST_RB");
+    return v ? std::atoi(v) : 0;
+  }();
+  // one row per CTA when the rows fit co-resident (measured fastest at cfg1: 3.5k vs 3.1k Mpix*it/s
+  // with two rows), else the fewest rows per CTA that do
+  int RB = rb_env > 0 ? rb_env : 1;
+  size_t smem = kb::ps_smem_bytes(RB, op->Ha, op->Hb, op->n, op->r);
+  if (rb_env <= 0) {
+    while (RB < op->m) {
+      int ps = 0;
+      smem = kb::ps_smem_bytes(RB, op->Ha, op->Hb, op->n, op->r);
+      if (smem <= 200 * 1024 && allow_smem(kb::kb_solve_persistent, smem) == KB_OK &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kb::kb_solve_persistent, kb::kPsThreads, smem) ==
+              cudaSuccess &&
+          ps >= 1 && (op->m + RB - 1) / RB <= ps * sms)
+        break;
+      ++RB;
+    }
+    smem = kb::ps_smem_bytes(RB, op->Ha, op->Hb, op->n, op->r);
+  }
   if (smem > 200 * 1024) return p;
   if (allow_smem(kb::kb_solve_persistent, smem) != KB_OK) return p;
   int per_sm = 0;
@@ -1479,6 +1498,7 @@ PsPlan persist_plan(const kb_op* op) {
     return p;
   p.RB = RB;
   p.nblk = (op->m + RB - 1) / RB;
+  if (p.nblk > per_sm * sms) return PsPlan{};  // a cooperative launch must be co-resident
   p.smem = smem;
   return p;
 }
@@ -1487,10 +1507,20 @@ int launch_persist(const kb_op* op, const PsPlan& pp, const double* B, double* X
                    const double* beta, int k0, int iters, double L, double lam, int project, int* nonfinite,
                    cudaStream_t s) {
   // beta_k go to the (unused on this path) norm-partials region of the workspace
-  const int cap = (int)(4 * (size_t)op->batch * sum_blocks(op));
+  // beta (doubles) then the CTAs' phase flags (ints) in the partials region
+  // grid-wide barriers by default: measured faster than the neighbour-flag waits at cfg1
+  // (3.65k vs 2.70k Mpix*it/s, tools/cfg1_ab.sh); KB_PERSIST_SYNC=flags selects the latter
+  static const bool grid_sync = [] {
+    const char* v = std::getenv("KB_PERSIST_SYNC");
+    return !(v && std::string(v) == "flags");
+  }();
+  const int cap = (int)(4 * (size_t)op->batch * sum_blocks(op)) - (pp.nblk + 1) / 2 - 2;
+  if (cap < 1) return fail(KB_ERR_ARGUMENT, "workspace too small for the persistent solve");
+  int* flags = reinterpret_cast<int*>(w.partials + cap + 1);
   for (int done = 0; done < iters;) {
     const int cnt = std::min(iters - done, cap);
     KB_CUDA(cudaMemcpyAsync(w.partials, beta + k0 + done, sizeof(double) * cnt, cudaMemcpyHostToDevice, s));
+    if (!grid_sync) KB_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * pp.nblk, s));
     kb::PsArgs a;
     a.B = B;
     a.X = X;
@@ -1515,6 +1545,7 @@ int launch_persist(const kb_op* op, const PsPlan& pp, const double* B, double* X
     a.k0 = k0 + done;
     a.iters = cnt;
     a.project = project;
+    a.flags = grid_sync ? nullptr : flags;
     void* args[] = {&a};
     KB_CUDA(cudaLaunchCooperativeKernel((const void*)kb::kb_solve_persistent, dim3(pp.nblk), dim3(kb::kPsThreads),
                                         args, pp.smem, s));
