@@ -81,48 +81,63 @@ __global__ void __launch_bounds__(kPsThreads) kb_solve_persistent(PsArgs a) {
   // is not coherent across SMs); out-of-domain rows reflected (refl) or zero
   auto stage = [&](const double* src, int refl) {
     const int rows = nr + 2 * Ha, half = n >> 1;
-    for (int idx = tid; idx < rows * half; idx += kPsThreads) {
-      const int t = idx / half, c = 2 * (idx - t * half);
+    for (int t = 0; t < rows; ++t) {
       const int g = ps_src(r0 - Ha + t, m, refl);
-      double* dst = Ys + (size_t)t * n + c;
-      if (g >= 0) {
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)),
-                     "l"(src + (size_t)g * n + c)
-                     : "memory");
-      } else {
-        dst[0] = 0.0;
-        dst[1] = 0.0;
+      for (int h2 = tid; h2 < half; h2 += kPsThreads) {
+        double* dst = Ys + (size_t)t * n + 2 * h2;
+        if (g >= 0) {
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)),
+                       "l"(src + (size_t)g * n + 2 * h2)
+                       : "memory");
+        } else {
+          dst[0] = 0.0;
+          dst[1] = 0.0;
+        }
       }
     }
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
   };
   // axis 0 (rows): forward Z[t][c] = sum_k th[k] Ys[t + k][c] (x~(s - d), d = Ha - k);
-  // adjoint correlation Z[t][c] = sum_k th[k] Ys[t + 2Ha - k][c] (x(s + d), zero outside)
+  // adjoint correlation Z[t][c] = sum_k th[k] Ys[t + 2Ha - k][c] (x(s + d), zero outside).
+  // Up to kPsR terms share each staged value (one shared load per kPsR FMAs).
+  constexpr int kPsR = 4;
   auto axis0 = [&](bool adjoint) {
     for (int t = 0; t < nr; ++t)
+      for (int c = tid; c < n; c += kPsThreads) {
+        const double* y = Ys + (size_t)t * n + c;
+        for (int i0 = 0; i0 < r; i0 += kPsR) {
+          double acc[kPsR] = {0.0, 0.0, 0.0, 0.0};
+          const int ni = min(kPsR, r - i0);
+#pragma unroll 2
+          for (int k = 0; k < wa; ++k) {
+            const double v = y[(size_t)(adjoint ? 2 * Ha - k : k) * n];
+#pragma unroll
+            for (int q = 0; q < kPsR; ++q)
+              if (q < ni) acc[q] = fma(th[(i0 + q) * wa + k], v, acc[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < kPsR; ++q)
+            if (q < ni) Zs[((size_t)(i0 + q) * RB + t) * np + Hb + c] = acc[q];
+        }
+      }
+    if (!(adjoint && a.refl_a && edge_rows)) return;
+    // + the adjoint's forward-fold terms on the edge rows: sources s - d outside [0, m)
+    for (int t = 0; t < nr; ++t) {
+      const int s = r0 + t;
+      if (s >= Ha && s < m - Ha) continue;
       for (int c = tid; c < n; c += kPsThreads)
         for (int i = 0; i < r; ++i) {
           const double* h = th + i * wa;
-          const double* y = Ys + (size_t)t * n + c;
-          double acc = 0.0;
-          if (!adjoint) {
-#pragma unroll 4
-            for (int k = 0; k < wa; ++k) acc = fma(h[k], y[(size_t)k * n], acc);
-          } else {
-#pragma unroll 4
-            for (int k = 0; k < wa; ++k) acc = fma(h[k], y[(size_t)(2 * Ha - k) * n], acc);
-            if (a.refl_a && edge_rows) {  // + the forward fold: sources s - d outside [0, m)
-              const int s = r0 + t;
-              for (int k = 0; k < wa; ++k) {
-                const int u = s - (Ha - k);
-                if (u >= 0 && u < m) continue;
-                const int f = ps_src(u, m, 1);
-                if (f >= 0) acc = fma(h[k], Ys[(size_t)(f - r0 + Ha) * n + c], acc);
-              }
-            }
+          double acc = Zs[((size_t)i * RB + t) * np + Hb + c];
+          for (int k = 0; k < wa; ++k) {
+            const int u = s - (Ha - k);
+            if (u >= 0 && u < m) continue;
+            const int f = ps_src(u, m, 1);
+            if (f >= 0) acc = fma(h[k], Ys[(size_t)(f - r0 + Ha) * n + c], acc);
           }
           Zs[((size_t)i * RB + t) * np + Hb + c] = acc;
         }
+    }
   };
   // Z halo columns: reflected values (forward reflective) or zeros
   auto zhalo = [&](int refl) {
