@@ -99,27 +99,23 @@ __global__ void __launch_bounds__(kPsThreads) kb_solve_persistent(PsArgs a) {
   };
   // axis 0 (rows): forward Z[t][c] = sum_k th[k] Ys[t + k][c] (x~(s - d), d = Ha - k);
   // adjoint correlation Z[t][c] = sum_k th[k] Ys[t + 2Ha - k][c] (x(s + d), zero outside).
-  // Up to kPsR terms share each staged value (one shared load per kPsR FMAs).
-  constexpr int kPsR = 4;
+  // (Sharing each staged value across the terms measured slower at cfg1: 3.25k vs 3.65k.)
   auto axis0 = [&](bool adjoint) {
     for (int t = 0; t < nr; ++t)
-      for (int c = tid; c < n; c += kPsThreads) {
-        const double* y = Ys + (size_t)t * n + c;
-        for (int i0 = 0; i0 < r; i0 += kPsR) {
-          double acc[kPsR] = {0.0, 0.0, 0.0, 0.0};
-          const int ni = min(kPsR, r - i0);
-#pragma unroll 2
-          for (int k = 0; k < wa; ++k) {
-            const double v = y[(size_t)(adjoint ? 2 * Ha - k : k) * n];
-#pragma unroll
-            for (int q = 0; q < kPsR; ++q)
-              if (q < ni) acc[q] = fma(th[(i0 + q) * wa + k], v, acc[q]);
+      for (int c = tid; c < n; c += kPsThreads)
+        for (int i = 0; i < r; ++i) {
+          const double* h = th + i * wa;
+          const double* y = Ys + (size_t)t * n + c;
+          double acc = 0.0;
+          if (!adjoint) {
+#pragma unroll 4
+            for (int k = 0; k < wa; ++k) acc = fma(h[k], y[(size_t)k * n], acc);
+          } else {
+#pragma unroll 4
+            for (int k = 0; k < wa; ++k) acc = fma(h[k], y[(size_t)(2 * Ha - k) * n], acc);
           }
-#pragma unroll
-          for (int q = 0; q < kPsR; ++q)
-            if (q < ni) Zs[((size_t)(i0 + q) * RB + t) * np + Hb + c] = acc[q];
+          Zs[((size_t)i * RB + t) * np + Hb + c] = acc;
         }
-      }
     if (!(adjoint && a.refl_a && edge_rows)) return;
     // + the adjoint's forward-fold terms on the edge rows: sources s - d outside [0, m)
     for (int t = 0; t < nr; ++t) {

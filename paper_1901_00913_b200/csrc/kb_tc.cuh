@@ -41,7 +41,11 @@ constexpr int kTcThreads = 32 * (kTcEpi + 4);  // TMA warp, issuers, 2 x 4 conve
 constexpr unsigned kTcStageBytes = kTcRB * 128 * 4;  // one [32 rows][128 cols] fp32 tile
 // tensor memory: two accumulator sets of G x 64 columns, then the A stages
 __host__ __device__ __forceinline__ int tc_astages(int G) { return min(kTcStagesMax, (512 - 128 * G) / 32); }
-constexpr unsigned kTcStoreBytes = 4 * 2 * 4096;  // epilogue staging: 4 warps x 2 buffers x [32 L][32 S]
+#ifndef KB_TC_STORE_BUFS
+#define KB_TC_STORE_BUFS 2
+#endif
+constexpr int kTcStoreBufs = KB_TC_STORE_BUFS;  // TMA-store staging buffers per epilogue warp
+constexpr unsigned kTcStoreBytes = 4 * kTcStoreBufs * 4096;  // 4 warps x buffers x [32 L][32 S]
 // dynamic shared memory: [staging][tile ring][bricks] (1 KB alignment slack in front)
 
 __host__ __device__ __forceinline__ int tc_ksteps(int Kw) { return (Kw + 62) / 8 + 1; }
@@ -523,9 +527,9 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
             }
             if (s + 32 <= ch.cnt) {
               // swizzled staging row `lane`: 16-byte chunk c at position c ^ (lane & 7)
-              if (nstore >= 2 && lane == 0) bulk_wait_read<1>();
+              if (nstore >= kTcStoreBufs && lane == 0) bulk_wait_read<kTcStoreBufs - 1>();
               __syncwarp();
-              float* sb = staging + (2 * q + (nstore & 1)) * 1024;
+              float* sb = staging + (kTcStoreBufs * q + (nstore % kTcStoreBufs)) * 1024;
 #pragma unroll
               for (int c = 0; c < 8; ++c)
                 reinterpret_cast<float4*>(sb + lane * 32)[c ^ (lane & 7)] =
