@@ -424,10 +424,7 @@ def run_b200(args):
             "vs_baseline": None,
             "dtype": "f64" if dtype == "float64" else "f32",
             "data": f"synthetic (seeded phantom + PSF + exact-level Gaussian noise, BASELINE {cfg.name})",
-            "config": {"workload": workload_name(cfg, res["batched"]),
-                       "global_batch": cfg.batch if res["batched"] else world,
-                       "parallelism": f"batch-shard{world}" if res["batched"] else f"replicas{world}",
-                       "l2": l2_note(cfg, dtype, len(res["ops"]))},
+            "config": config_dict(cfg, dtype, world),
             "e2e": res["e2e"],
             "roofline": res["roofline"],
             "gpu_launches": res["launches"],
@@ -444,6 +441,15 @@ def run_b200(args):
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def config_dict(cfg, dtype, world):
+    """The `config` object of a line (identical for the b200 and reference arms of a config)."""
+    batched = cfg.batch > 1
+    return {"workload": workload_name(cfg, batched),
+            "global_batch": cfg.batch if batched else world,
+            "parallelism": f"batch-shard{world}" if batched else f"replicas{world}",
+            "l2": l2_note(cfg, dtype, cfg.batch)}
 
 
 def workload_name(cfg, batched):
@@ -665,11 +671,10 @@ def run_reference(args):
         "ms_per_iteration_extrapolated": round(step * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (BASELINE {cfg.name})",
-        "config": {"workload": workload_name(cfg, cfg.batch > 1), "global_batch": 1, "parallelism": "cpu",
-                   "sample": what, "same_config": True},
+        "config": config_dict(cfg, default_dtype(cfg), 1),
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 4), "unit": "Mpixel*iterations/s", "cores": threads,
-                         "kind": "port", "sample": what},
+                         "kind": "port", "sample": what, "same_config": True},
         "e2e": {"value": round(value, 4), "unit": "Mpixel*iterations/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

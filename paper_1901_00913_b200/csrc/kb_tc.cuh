@@ -630,7 +630,14 @@ struct StrideWalk {
 #endif
 constexpr int kTcSumSlots = 4;                       // per-term accumulator slots (64 columns each)
 constexpr int kTcSumEpi = 8;                         // epilogue warps
-constexpr int kTcSumThreads = 32 * (kTcEpi + kTcSumEpi);
+// converter sets of the sum pass (4 warps each, alternate tiles): the sum pass is converter-bound
+// (per-role timeline at cfg5: the issuers wait 39% of the time for A stages)
+#ifndef KB_TC_SUM_SETS
+#define KB_TC_SUM_SETS 2
+#endif
+constexpr int kTcSumSets = KB_TC_SUM_SETS;
+constexpr int kTcSumEpiW = kTcConv + 4 * kTcSumSets;  // first epilogue warp of the sum pass
+constexpr int kTcSumThreads = 32 * (kTcSumEpiW + kTcSumEpi);
 template <int MODE, bool NORMS = true>
 __device__ __forceinline__ void tc_sum_epi8(const float (&v)[8], const Epi<float>& e, long long at, int cnt,
                                             float Lb, float db, float rd, double vs, double (&nrm)[3],
@@ -826,11 +833,11 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
     }
     pa.put(4, 1);
     pb.put(5, 1);
-  } else if (warp < kTcEpi) {
+  } else if (warp < kTcSumEpiW) {
     // ---------------- converters: A stages ----------------
     // set cs owns the tiles with global tile index parity cs and converts both of a tile's A
     // stages (16 rows each: column 32q + lane of each row -> tensor-memory lane, K -> column)
-    const int wt = tid - 32 * kTcConv;  // 0..255
+    const int wt = tid - 32 * kTcConv;  // 0 .. 128 * kTcSumSets - 1
     const int cs = wt >> 7;
     const int q = warp & 3;
     const unsigned lane_base = tmem + ((unsigned)(32 * q) << 16);
@@ -844,7 +851,7 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
       for (int term = 0; term < r; ++term) {
         for (int rb = 0; rb < nrb; ++rb, ++tg, t.advance(nst)) {
           const int nat = min(2, na - 2 * rb);  // A stages of this tile
-          if ((tg & 1) != cs) {
+          if (tg % kTcSumSets != cs) {
             a.advance(nas);
             if (nat == 2) a.advance(nas);
             continue;
@@ -902,7 +909,7 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
     p7.put(7, 1);
   } else {
     // ---------------- epilogue: term slots -> fp32 sums -> fused update of the output rows ----------------
-    const int ew = warp - kTcEpi, q = warp & 3, hh = ew >> 2;  // lane quarter, 32-output half
+    const int ew = warp - kTcSumEpiW, q = warp & 3, hh = ew >> 2;  // lane quarter, 32-output half
     const unsigned lane_base = tmem + ((unsigned)(32 * q) << 16);
     const int nslots = gridDim.x * kTcSumEpi, slot = blockIdx.x * kTcSumEpi + ew;
     const int n = g.len;
