@@ -197,3 +197,35 @@ def test_port_select_lambda_reproduces_reference():
         op = kb.decompose(psf, kb.BoundaryCondition(str(g[f"l{ci}_bc"])), shape=B.shape)
         lam, _ = port.select_lambda(op, B, noise, L)
         assert lam == float(g[f"l{ci}_lam"]), ci
+
+
+# ------------------------------------------------------------------ decompose at BASELINE sizes
+@pytest.mark.parametrize("name,m,index", [("cfg1", 256, 0), ("cfg2", 1024, 0), ("cfg3", 512, 0), ("cfg3", 512, 7),
+                                          ("cfg4", 4096, 0), ("cfg5", 1024, 0)])
+def test_support_block_decompose_matches_reference_at_config_sizes(name, m, index):
+    """The support-block KPA against the reference's own decompose (kron.py:156-208,
+    the full image-size weighted SVD; run from baseline/_ref) on each BASELINE config's PSF at
+    its full image size (cfg5's 16384^2 SVD takes ~15 min, so its PSF is checked at 1024^2):
+    same sigma and rank, same generators after the F11 sign rule, same anchors."""
+    from conftest import reference_module
+    from paper_1901_00913_b200 import workloads as W
+
+    ref = reference_module()
+    if ref is None:
+        pytest.skip("reference not installed in baseline/_ref")
+    cfg = W.CONFIGS[name]
+    psf = W.make_psf(cfg, index=index, seed=0)
+    bc = kb.BoundaryCondition(cfg.bc)
+    ours = kb.decompose(psf, bc, s=cfg.r, shape=(m, m))
+    rpsf = ref.psf.pad_to(ref.psf.Psf(psf.values, psf.center), m, m)
+    theirs = ref.kron.decompose(rpsf, ref.psf.BoundaryCondition(cfg.bc), s=cfg.r)
+    s1 = theirs.sigma[0]
+    np.testing.assert_allclose(ours.sigma[:cfg.r], theirs.sigma[:cfg.r], rtol=0, atol=1e-13 * s1)
+    assert ours.rank == theirs.rank
+    for t, u in zip(ours.terms, theirs.terms):
+        a, b = np.asarray(u.H.c), np.asarray(u.K.c)
+        mag = np.abs(a)
+        sgn = np.sign(a[np.argmax(mag > 1e-3 * mag.max())])  # SURVEY F11 sign rule
+        assert (t.H.j, t.K.j) == (u.H.j, u.K.j)
+        np.testing.assert_allclose(t.H.c, sgn * a, rtol=0, atol=1e-10 * mag.max())
+        np.testing.assert_allclose(t.K.c, sgn * b, rtol=0, atol=1e-10 * np.abs(b).max())
