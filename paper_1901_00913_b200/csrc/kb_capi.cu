@@ -437,7 +437,17 @@ int launch_a(const kb_op* op, Ctx& c, const T* in, T* z, const T* tin, const kb:
       }
       G = 0;
       for (int i = 0; i < tg.n; ++i) G = std::max(G, tg.count[i]);
-      const size_t fixed = (size_t)G * nbr * 1024;
+      // chunk-major order with every term's bricks resident (KB_TC_CHUNK_MAJOR=1, when they fit
+      // beside a >= 6-stage ring): the groups of a chunk re-read its input tiles from L2 instead
+      // of streaming the plane from DRAM once per group. Opt-in: measured no faster at cfg5
+      // (16.8k either way) and slower at cfg3 (41.1k -> 38.4k; profiles/r02_ab_chunk_major.txt).
+      static const int cm_env = [] {
+        const char* v = std::getenv("KB_TC_CHUNK_MAJOR");
+        return v ? std::atoi(v) : 0;
+      }();
+      const int chunk_major = tg.n > 1 && cm_env == 1 &&
+                              (size_t)op->r * nbr * 1024 + 6 * kb::kTcStageBytes <= avail;
+      const size_t fixed = (size_t)(chunk_major ? op->r : G) * nbr * 1024;
       const int nst = std::min<int>(kb::kTcRingMax, (int)((avail - std::min(fixed, avail)) / kb::kTcStageBytes));
       const size_t smem = std::max<size_t>(1024 + kb::kTcStoreBytes + (size_t)nst * kb::kTcStageBytes + fixed,
                                            116 * 1024);  // one CTA per SM
@@ -463,7 +473,7 @@ int launch_a(const kb_op* op, Ctx& c, const T* in, T* z, const T* tin, const kb:
         c.engine = KB_ENGINE_TC_TF32;
         KB_CUDA(cudaLaunchKernelEx(&cfg, kern, mapt, mapz, z, z_ps, z_bs, btab, g, nw2, op->r, op->batch, parts,
                                    tg, G, nst, reinterpret_cast<const float*>(in), in_bs, mirror_h,
-                                   reinterpret_cast<const float*>(msign)));
+                                   reinterpret_cast<const float*>(msign), chunk_major));
         c.mirror = mirror_h > 0;
         return KB_OK;
       }

@@ -261,12 +261,41 @@ __global__ void kb_build_bricks(const float* __restrict__ tin, int Wp, int Kw, i
 // bricks). bricks: [G][nbr][hi 512 B | lo 512 B]. Results leave
 // through a 128-byte-swizzled [32 L][32 S] staging box per worker warp and a TMA store (zmap:
 // Z^T planes b * r + term), so every global write is a full line; ragged chunk ends store directly.
+// (chunk, term group) pairs of the split pass, in one of two orders: group-major (each group
+// streams the whole plane, holding one group's bricks) or chunk-major (all groups of a chunk back
+// to back, every term's bricks resident: the chunk's input tiles are re-read from L2 rather than
+// DRAM -- at cfg5, r = 10 in 4 groups, that is 3 of the 4 reads of X)
+struct PairWalk {
+  ChunkWalk w0, walk;
+  Chunk ch;
+  int gr = 0, ngroups;
+  bool chunk_major, fresh = true;
+  __device__ PairWalk(const ChunkWalk& w, int ng, bool cm) : w0(w), walk(w), ngroups(ng), chunk_major(cm) {}
+  __device__ bool next(Chunk& c, int& g) {
+    if (chunk_major) {
+      if (fresh || ++gr == ngroups) {
+        if (!walk.next(ch, kTcTS)) return false;
+        gr = 0;
+        fresh = false;
+      }
+    } else {
+      while (!walk.next(ch, kTcTS)) {
+        if (++gr >= ngroups) return false;
+        walk = w0;
+      }
+    }
+    c = ch;
+    g = gr;
+    return true;
+  }
+};
+
 __global__ void __launch_bounds__(kTcThreads, 1)
 kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap zmap,
                  float* __restrict__ z, long long z_ps, long long z_bs, const unsigned* __restrict__ btab,
                  AxisGeom g, const double* __restrict__ nw2, int r, int batch, int parts, Groups grp, int G,
                  int nst, const float* __restrict__ in, long long in_bs, int mirror_h,
-                 const float* __restrict__ msign) {
+                 const float* __restrict__ msign, int chunk_major) {
   extern __shared__ __align__(16) unsigned char kb_smem_tc[];
   __shared__ unsigned long long full[kTcRingMax], sfree[kTcRingMax], a_ready[kTcStagesMax],
       a_free[kTcStagesMax], acc_full[2], acc_empty[2], bready;
@@ -315,10 +344,11 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     if (lane == 0) {
       TcProf pw(g, true);
       RingPos t;
-      for (int gr = 0; gr < ngroups; ++gr) {
-        ChunkWalk walk(g.len, LT, parts, batch, 4);
-        Chunk ch;
-        while (walk.next(ch, kTcTS)) {
+      PairWalk pairs(ChunkWalk(g.len, LT, parts, batch, 4), ngroups, chunk_major);
+      Chunk ch;
+      int gr;
+      while (pairs.next(ch, gr)) {
+        {
           for (int rb = 0; rb < nrb; ++rb, t.advance(nst)) {
             pw.start();
 #if KB_TC_SPLIT_PRODUCER_SPIN
@@ -344,12 +374,14 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     // brick descriptors advance by adding (bytes >> 4) to the start-address field
     const unsigned long long b0 = tc_desc(smem_u32(bricks), 128, 256, 0);
     const int qmax = (g.Kw + 14) >> 3;
-    for (int gr = 0; gr < ngroups; ++gr) {
+    const bool live = !(g.dbg & 1);
+    PairWalk pairs(ChunkWalk(g.len, LT, parts, batch, 4), ngroups, chunk_major);
+    Chunk ch;
+    int gr;
+    while (pairs.next(ch, gr)) {
       const int gc = grp.count[gr];
-      const bool live = !(g.dbg & 1);
-      ChunkWalk walk(g.len, LT, parts, batch, 4);
-      Chunk ch;
-      while (walk.next(ch, kTcTS)) {
+      const unsigned boff = chunk_major ? (unsigned)grp.start[gr] * nbr : 0u;  // resident bricks
+      {
         const int ab = chunk & 1;
         pe.start();
         if (chunk >= 2) mbar_wait(&acc_empty[ab], ((chunk >> 1) - 1) & 1);  // epilogue drained this set
@@ -370,14 +402,14 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
             const int k = 2 * ia + h, q = k - 2 * nb;  // brick index o / 8 with o = 8k - 16nb
             if (live && k < nk && q >= 0 && q <= qmax) {
               if (gc == 3) {
-                const unsigned long long bh = b0 + ((unsigned)q * 1024 >> 4);
+                const unsigned long long bh = b0 + ((boff + (unsigned)q) * 1024 >> 4);
                 tc_mma3x3(dcol, ahi + 8 * h, ahi + 16 + 8 * h, bh, (unsigned)nbr * 1024 >> 4, q != 0);
                 continue;
               }
 #pragma unroll
               for (int gi = 0; gi < kTcG; ++gi) {
                 if (gi >= gc) break;
-                const unsigned long long bh = b0 + ((unsigned)(gi * nbr + q) * 1024 >> 4);
+                const unsigned long long bh = b0 + ((boff + (unsigned)(gi * nbr + q)) * 1024 >> 4);
                 tc_mma3(dcol + gi * kTcTS, ahi + 8 * h, ahi + 16 + 8 * h, bh, bh + (512 >> 4), q != 0);
               }
             }
@@ -401,22 +433,24 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     pt.start();
     RingPos a, t;
     int chunk = 0, bricks_key = -1, nbl = 0, tg = 0;
-    for (int gr = 0; gr < ngroups; ++gr) {
+    PairWalk pairs(ChunkWalk(g.len, LT, parts, batch, 4), ngroups, chunk_major);
+    Chunk ch;
+    int gr;
+    while (pairs.next(ch, gr)) {
       const int g0 = grp.start[gr], gc = grp.count[gr];
       const float fsign = grp.sign[gr] < 0 ? -1.f : 1.f;
-      ChunkWalk walk(g.len, LT, parts, batch, 4);
-      Chunk ch;
-      while (walk.next(ch, kTcTS)) {
-        const int key = ch.b * ngroups + gr;
+      {
+        const int key = chunk_major ? ch.b : ch.b * ngroups + gr;
         if (key != bricks_key) {
-          // the group's bricks: one bulk copy from the brick table once the previous chunk's
-          // MMAs (the last readers of the old bricks) completed
+          // the group's bricks (chunk-major: every term's) in one bulk copy from the brick table,
+          // once the previous chunk's MMAs (the last readers of the old bricks) completed
           pb.start();
           if (wt == 0) {
             if (chunk > 0) mbar_wait(&acc_full[(chunk - 1) & 1], ((chunk - 1) >> 1) & 1);
-            const unsigned bytes = (unsigned)(gc * nbr) * 1024;
+            const int t0 = chunk_major ? 0 : g0, tn = chunk_major ? r : gc;
+            const unsigned bytes = (unsigned)(tn * nbr) * 1024;
             mbar_arrive_expect_tx(&bready, bytes);
-            bulk_g2s(bricks, btab + ((long long)ch.b * r + g0) * nbr * 256, bytes, &bready);
+            bulk_g2s(bricks, btab + ((long long)ch.b * r + t0) * nbr * 256, bytes, &bready);
           }
           mbar_wait(&bready, nbl & 1);  // before any A stage of this chunk is announced
           ++nbl;
@@ -491,11 +525,12 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     const unsigned lane_base = tmem + ((unsigned)(32 * q) << 16);
     TcProf p3(g, warp == kTcEpi && lane == 0), p4(g, warp == kTcEpi && lane == 0);
     int chunk = 0, nstore = 0;
-    for (int gr = 0; gr < ngroups; ++gr) {
+    PairWalk pairs(ChunkWalk(g.len, LT, parts, batch, 4), ngroups, chunk_major);
+    Chunk ch;
+    int gr;
+    while (pairs.next(ch, gr)) {
       const int g0 = grp.start[gr], gc = grp.count[gr];
-      ChunkWalk walk(g.len, LT, parts, batch, 4);
-      Chunk ch;
-      while (walk.next(ch, kTcTS)) {
+      {
         const int ab = chunk & 1;
         p3.start();
         mbar_wait(&acc_full[ab], (chunk >> 1) & 1);
