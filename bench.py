@@ -303,7 +303,10 @@ def measure_config(name, dtype, steps, warmup, rank, world, local, clocks=False,
     engines = dev.last_engines()
     wa, wb = dev.bands[1], dev.bands[3]  # executed taps per axis (band after trimming)
     px = m * m * len(ops)
-    flops_phase = [2 * cfg.r * w * px for w in (wa, wb, wa, wb)]  # one axis filter of all r terms
+    # one axis filter of all r terms per phase; with the axis-swapped twin (kb_capi.cu: the wider
+    # band first) pass A filters axis 1 and pass B axis 0
+    swapped = bool(dev.info().get("twin", 0))
+    flops_phase = [2 * cfg.r * w * px for w in ((wb, wa, wb, wa) if swapped else (wa, wb, wa, wb))]
     k_dom = max(range(4), key=lambda i: kern_ms[i])
     achieved_tf = flops_phase[k_dom] / (kern_ms[k_dom] * 1e-3) / 1e12
     peak_dom, peak_src = engine_peak(engines[k_dom])
@@ -317,18 +320,40 @@ def measure_config(name, dtype, steps, warmup, rank, world, local, clocks=False,
     # r Z planes; residual sum reads r Z planes + B, writes R; update sum reads r Z planes + Y +
     # X_prev, writes X and Y
     kern_bytes = esz * px * (1 + cfg.r, cfg.r + 2, 1 + cfg.r, cfg.r + 4)[k_dom]
+    # Which roof binds the dominant kernel: its arithmetic intensity (flops on executed taps over
+    # the DRAM bytes this two-sweep kernel must move, its r Z^T planes included) against the
+    # machine balance (live tensor peak / measured HBM bandwidth). L2-resident configs (cfg1,
+    # cfg2: the whole working set fits the 126 MB L2) are bounded by the tensor roof.
+    ws_mb = len(ops) * (4 + cfg.r) * m * m * esz / 1e6
+    intensity = flops_phase[k_dom] / kern_bytes
+    balance = peak_dom * 1e12 / (hbm_peak * 1e9)
+    hbm_bound = ws_mb > 100 and intensity < balance
+    hbm_ach = kern_bytes / (kern_ms[k_dom] * 1e-3) / 1e9
+    if hbm_bound:
+        head = {"bound": "hbm", "achieved": round(hbm_ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(hbm_ach / hbm_peak, 4),
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                "bytes_per_launch": kern_bytes,
+                "bytes_rule": "DRAM bytes this kernel must move in the two-sweep design: "
+                              + ("X in, r Z^T planes out" if k_dom in (0, 2) else
+                                 "r Z^T planes + B in, R out" if k_dom == 1 else "r Z^T planes + Y + X_prev in, X and Y out"),
+                "tensor": {"achieved": round(achieved_tf, 3), "peak": round(peak_dom, 3), "unit": "TFLOP/s",
+                           "frac": round(achieved_tf / peak_dom, 4), "peak_source": peak_src}}
+    else:
+        head = {"bound": "tensor", "achieved": round(achieved_tf, 3), "peak": round(peak_dom, 3), "unit": "TFLOP/s",
+                "frac": round(achieved_tf / peak_dom, 4),
+                "peak_source": "measured live by kb_fma_peak in this run: " + peak_src}
     res["roofline"] = {
-        "bound": "tensor",
+        **head,
         "kernel": f"{phase[k_dom]} on {engines[k_dom]}: the longest of the iteration's four kernels",
-        "achieved": round(achieved_tf, 3), "peak": round(peak_dom, 3), "unit": "TFLOP/s",
-        "frac": round(achieved_tf / peak_dom, 4),
-        "peak_source": "measured live by kb_fma_peak in this run: " + peak_src,
+        "intensity_flop_per_byte": round(intensity, 2), "machine_balance_flop_per_byte": round(balance, 2),
         "flops_per_launch": flops_phase[k_dom],
-        "flops_rule": f"2 r w_exec flop per pixel: r={cfg.r}, executed taps {wa} (axis 0) / {wb} (axis 1)",
+        "flops_rule": f"2 r w_exec flop per pixel: r={cfg.r}, executed taps {wa} (axis 0) / {wb} (axis 1)"
+                      + ("; axis-swapped twin: pass A = axis 1" if swapped else ""),
         "traffic": traffic[k_dom] if traffic else None,
         "traffic_source": f"profiles/traffic_{cfg.name}.json (ncu --set full, dram read+write of this kernel)",
         "kernel_dram_bytes_compulsory": kern_bytes,
-        "kernel_hbm_frac": round(kern_bytes / (kern_ms[k_dom] * 1e-3) / 1e9 / hbm_peak, 4),
+        "kernel_hbm_frac": round(hbm_ach / hbm_peak, 4),
         "iteration": {
             "per_kernel_ms": [round(x, 5) for x in kern_ms],
             "engines": engines,
@@ -349,6 +374,7 @@ def measure_config(name, dtype, steps, warmup, rank, world, local, clocks=False,
         ach = sum(flops_phase) / per_it_s / 1e12
         pk, src = engine_peak("dmma")
         res["roofline"].update({
+            "bound": "tensor", "unit": "TFLOP/s",
             "kernel": "kb_solve_persistent (whole solve in one cooperative launch, 2 grid barriers per iteration)",
             "achieved": round(ach, 3), "peak": round(pk, 3), "frac": round(ach / pk, 4),
             "flops_per_launch": sum(flops_phase) * iters,

@@ -64,7 +64,8 @@ int kb_op_create(kb_op** out, int dtype, int m, int n, int r, int batch, int bc_
 int kb_op_destroy(kb_op* op);
 /*
  * Layout facts of an operator, info[0..n): {Ha, Wpa, Hb, Wpb, sym_a, sym_b, adjoint pass-A groups,
- * max group}. sym_* = 1 when every generator on that reflective axis is symmetric or
+ * max group, twin}. twin = 1: kb_sfista_run's fast path solves the transposed problem with an
+ * axis-swapped copy of the operator (the wider band in pass A; large fp32 images, KB_AXIS_SWAP). sym_* = 1 when every generator on that reflective axis is symmetric or
  * antisymmetric to 1e-11 relative, so the adjoint folds through sign-reflected tile fills
  * instead of the exact fold kernels (set KB_EXACT_FOLD=1 to force the exact path).
  */

@@ -90,6 +90,10 @@ struct kb_op {
   // selection then counts the chunks of the whole problem, not of one strip
   long long chunk_scale = 1;
   int slots_cap = 0;  // views: norm-partial slots of the parent's workspace (0: sum_blocks(op))
+  // the operator of the transposed image (H and K swapped, m and n swapped) when running the
+  // wider band first is faster (kb_op_create: axis_swap_wanted); the fast sFISTA path then
+  // solves the transposed problem Y^T = sum_i K_i X^T H_i^T in the same workspace
+  kb_op* twin = nullptr;
   // engines of the latest kb_time_passes phases (reporting only; written under g_phase_mu)
   mutable int phase_engine[4] = {0, 0, 0, 0};
 };
@@ -251,6 +255,38 @@ Work layout(const kb_op* op, void* base) {
   off = align_up(off + sizeof(double) * 4 * (size_t)op->batch, 256);
   w.bytes = off;
   return w;
+}
+
+// With an axis-swapped twin the workspace holds the larger of the two layouts, then the
+// transposed B, X and Y planes of the twin's solve.
+size_t twin_planes_offset(const kb_op* op) {
+  return align_up(std::max(layout(op, nullptr).bytes, layout(op->twin, nullptr).bytes), 256);
+}
+void* twin_plane(const kb_op* op, void* base, int i) {
+  return static_cast<unsigned char*>(base) + twin_planes_offset(op) + i * align_up(plane_elems(op) * elem(op), 256);
+}
+
+// out[n][m] = in[m][n] (32 x 32 shared-memory tiles, both sides coalesced)
+template <typename T>
+__global__ void kb_transpose_k(const T* __restrict__ in, T* __restrict__ out, int m, int n) {
+  __shared__ T tile[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int r = r0 + j, c = c0 + threadIdx.x;
+    if (r < m && c < n) tile[j][threadIdx.x] = in[(size_t)r * n + c];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int c = c0 + j, r = r0 + threadIdx.x;
+    if (c < n && r < m) out[(size_t)c * m + r] = tile[threadIdx.x][j];
+  }
+}
+template <typename T>
+int transpose_t(const T* in, T* out, int m, int n, cudaStream_t s) {
+  dim3 grid((n + 31) / 32, (m + 31) / 32);
+  kb_transpose_k<T><<<grid, dim3(32, 8), 0, s>>>(in, out, m, n);
+  KB_CUDA(cudaGetLastError());
+  return KB_OK;
 }
 
 // Split `count` terms starting at `start` into near-equal groups of at most gmax, all with
@@ -1074,6 +1110,7 @@ void classify(const double* taps, int dlo, int w, int& sign, bool& ok) {
 
 void free_op(kb_op* op) {
   if (!op) return;
+  free_op(op->twin);
   cudaFree(op->sign_b);
   cudaFree(op->ta_conv);
   cudaFree(op->ta_corr);
@@ -1275,6 +1312,7 @@ int kb_max_half_width(void) { return kMaxHalf; }
 int kb_op_create(kb_op** out, int dtype, int m, int n, int r, int batch, int bc_a, int bc_b,
                  int a_dlo, int a_w, const double* a_taps, int b_dlo, int b_w,
                  const double* b_taps) {
+  static thread_local bool creating_twin = false;
   if (!out) return fail(KB_ERR_ARGUMENT, "null output handle");
   *out = nullptr;
   if (dtype != KB_F64 && dtype != KB_F32) return fail(KB_ERR_ARGUMENT, "dtype must be KB_F64 or KB_F32");
@@ -1363,6 +1401,26 @@ int kb_op_create(kb_op** out, int dtype, int m, int n, int r, int batch, int bc_
     free_op(op);
     return rc;
   }
+  // Axis swap (measured at cfg5, tools/swap_exp.py: 15.2-15.5 -> 14.7 ms per iteration): the
+  // two-sweep passes re-read and re-convert (TS + 2H)/TS input rows per output in pass B, so the
+  // wider band belongs in pass A. For large fp32 single images with a markedly wider axis-1 band
+  // the fast sFISTA path solves the transposed problem with this twin. KB_AXIS_SWAP=0/1 overrides.
+  static const int swap_env = [] {
+    const char* v = std::getenv("KB_AXIS_SWAP");
+    return v ? std::atoi(v) : -1;
+  }();
+  const bool want = swap_env == 1 || (swap_env < 0 && dtype == KB_F32 && (long long)m * n >= 4096LL * 4096);
+  if (!creating_twin && batch == 1 && Hb >= Ha + 8 && want) {
+    creating_twin = true;
+    kb_op* tw = nullptr;
+    rc = kb_op_create(&tw, dtype, n, m, r, batch, bc_b, bc_a, b_dlo, b_w, b_taps, a_dlo, a_w, a_taps);
+    creating_twin = false;
+    if (rc != KB_OK) {
+      free_op(op);
+      return rc;
+    }
+    op->twin = tw;
+  }
   *out = op;
   return KB_OK;
 }
@@ -1372,12 +1430,18 @@ int kb_op_destroy(kb_op* op) {
   return KB_OK;
 }
 
-size_t kb_workspace_bytes(const kb_op* op) { return op ? layout(op, nullptr).bytes : 0; }
+size_t kb_workspace_bytes(const kb_op* op) {
+  if (!op) return 0;
+  size_t b = layout(op, nullptr).bytes;
+  if (op->twin) b = twin_planes_offset(op) + 3 * align_up(plane_elems(op) * elem(op), 256);
+  return b;
+}
 
 int kb_op_info(const kb_op* op, int* info, int n) {
   KB_TRY(check_op(op));
-  const int v[8] = {op->Ha, op->Wpa, op->Hb, op->Wpb, op->sym_a, op->sym_b, op->grp_adj.n, op->gmax};
-  for (int i = 0; i < n && i < 8; ++i) info[i] = v[i];
+  const int v[9] = {op->Ha, op->Wpa, op->Hb, op->Wpb, op->sym_a, op->sym_b, op->grp_adj.n, op->gmax,
+                    op->twin != nullptr};
+  for (int i = 0; i < n && i < 9; ++i) info[i] = v[i];
   return KB_OK;
 }
 
@@ -1572,7 +1636,9 @@ int sfista_run_impl(const kb_op* op, const void* B, void* X, void* Y, void* work
   if (!B || !X || !Y || !work || !beta || !L || !nonfinite) return fail(KB_ERR_ARGUMENT, "null argument");
   if (iters < 0 || k0 < 0) return fail(KB_ERR_ARGUMENT, "iters and k0 must be >= 0");
   if (iters == 0) return KB_OK;
-  Work w = layout(op, work);
+  // fast path with an axis-swapped twin: the launches run the twin on transposed planes
+  const kb_op* run = (op->twin && !norms && op->batch == 1) ? op->twin : op;
+  Work w = layout(run, work);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   std::vector<double> host(2 * (size_t)op->batch);
   for (int b = 0; b < op->batch; ++b) {
@@ -1586,6 +1652,17 @@ int sfista_run_impl(const kb_op* op, const void* B, void* X, void* Y, void* work
     if (op->dtype == KB_F64)
       return sfista_launches<double>(op, static_cast<const double*>(B), static_cast<double*>(X),
                                      static_cast<double*>(Y), w, beta, k0, iters, project, nonfinite, norms, cs);
+    if (run != op) {  // solve the transposed problem: B^T, X^T, Y^T in, X, Y back
+      float* Bt = static_cast<float*>(twin_plane(op, work, 0));
+      float* Xt = static_cast<float*>(twin_plane(op, work, 1));
+      float* Yt = static_cast<float*>(twin_plane(op, work, 2));
+      KB_TRY(transpose_t<float>(static_cast<const float*>(B), Bt, op->m, op->n, cs));
+      KB_TRY(transpose_t<float>(static_cast<const float*>(X), Xt, op->m, op->n, cs));
+      KB_TRY(transpose_t<float>(static_cast<const float*>(Y), Yt, op->m, op->n, cs));
+      KB_TRY(sfista_launches<float>(run, Bt, Xt, Yt, w, beta, k0, iters, project, nonfinite, nullptr, cs));
+      KB_TRY(transpose_t<float>(Xt, static_cast<float*>(X), op->n, op->m, cs));
+      return transpose_t<float>(Yt, static_cast<float*>(Y), op->n, op->m, cs);
+    }
     return sfista_launches<float>(op, static_cast<const float*>(B), static_cast<float*>(X),
                                   static_cast<float*>(Y), w, beta, k0, iters, project, nonfinite, norms, cs);
   };
@@ -1761,7 +1838,10 @@ int kb_time_passes(const kb_op* op, const void* Y, const void* B, void* R, void*
   KB_TRY(check_op(op));
   if (!Y || !B || !R || !X || !Yio || !work || !L || !nonfinite || !ms4 || reps < 1)
     return fail(KB_ERR_ARGUMENT, "bad kb_time_passes arguments");
-  Work w = layout(op, work);
+  // with an axis-swapped twin the fast path runs the twin's kernels: time those (the planes are
+  // only buffers here, of the same element count)
+  const kb_op* top = op->twin ? op->twin : op;
+  Work w = layout(top, work);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   std::vector<double> host(2 * (size_t)op->batch);
   for (int b = 0; b < op->batch; ++b) {
@@ -1769,6 +1849,14 @@ int kb_time_passes(const kb_op* op, const void* Y, const void* B, void* R, void*
     host[op->batch + b] = L[b] + lam * lam;
   }
   KB_CUDA(cudaMemcpyAsync(w.scal, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (op->twin) {
+    const int rc = time_passes_t<float>(top, static_cast<const float*>(Y), static_cast<const float*>(B),
+                                        static_cast<float*>(R), static_cast<float*>(X), static_cast<float*>(Yio), w,
+                                        reps, ms4, nonfinite, s);
+    std::lock_guard<std::mutex> lock(g_phase_mu);
+    for (int i = 0; i < 4; ++i) op->phase_engine[i] = top->phase_engine[i];
+    return rc;
+  }
   if (op->dtype == KB_F64)
     return time_passes_t<double>(op, static_cast<const double*>(Y), static_cast<const double*>(B), static_cast<double*>(R), static_cast<double*>(X), static_cast<double*>(Yio), w, reps, ms4, nonfinite, s);
   return time_passes_t<float>(op, static_cast<const float*>(Y), static_cast<const float*>(B), static_cast<float*>(R), static_cast<float*>(X), static_cast<float*>(Yio), w, reps, ms4, nonfinite, s);

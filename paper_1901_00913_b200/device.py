@@ -308,9 +308,9 @@ class DeviceOperator:
 
     def info(self) -> dict:
         """Device layout facts (kb_op_info)."""
-        vals = (_c_int * 8)()
-        _check(load_library().kb_op_info(self._handle, vals, 8), "kb_op_info")
-        keys = ("Ha", "Wpa", "Hb", "Wpb", "sym_a", "sym_b", "adj_groups", "gmax")
+        vals = (_c_int * 9)()
+        _check(load_library().kb_op_info(self._handle, vals, 9), "kb_op_info")
+        keys = ("Ha", "Wpa", "Hb", "Wpb", "sym_a", "sym_b", "adj_groups", "gmax", "twin")
         return dict(zip(keys, (int(v) for v in vals)))
 
     # -- buffers ---------------------------------------------------------------------------
