@@ -454,14 +454,15 @@ int launch_a(const kb_op* op, Ctx& c, const T* in, T* z, const T* tin, const kb:
     if (btab && use_tc_split(op, g) && z_bs == (long long)op->r * z_ps) {
       const int nbr = kb::tc_bricks(g.Kw);
       // bricks of up to kTcG terms first, then as deep a tile ring as the rest of shared memory
-      // holds (at least 3 stages)
-      const size_t avail = 226 * 1024 - 1024 - kb::kTcStoreBytes;
+      // holds (at least 4 stages: with 3 the pipeline hangs or faults -- found with
+      // -DKB_TC_RING_MAX=3 at cfg4/cfg5 -- so narrower rings fall back to the mma.sync passes)
+      const size_t avail = 226 * 1024 - 1024 - kb::tc_store_bytes(4);
       static const int gmax = [] {
         const char* v = std::getenv("KB_TC_G");
         return v ? std::max(1, std::min(kb::kTcG, std::atoi(v))) : kb::kTcG;
       }();
       int G = std::min(op->r, gmax);
-      while (G > 1 && (size_t)G * nbr * 1024 + 3 * kb::kTcStageBytes > avail) --G;
+      while (G > 1 && (size_t)G * nbr * 1024 + 4 * kb::kTcStageBytes > avail) --G;
       // sign-uniform term groups of <= G terms: the runs of equal fill sign of the pass' groups,
       // each cut into near-equal pieces
       kb::Groups tg{};
@@ -484,21 +485,32 @@ int launch_a(const kb_op* op, Ctx& c, const T* in, T* z, const T* tin, const kb:
       const int chunk_major = tg.n > 1 && cm_env == 1 &&
                               (size_t)op->r * nbr * 1024 + 6 * kb::kTcStageBytes <= avail;
       const size_t fixed = (size_t)(chunk_major ? op->r : G) * nbr * 1024;
-      const int nst = std::min<int>(kb::kTcRingMax, (int)((avail - std::min(fixed, avail)) / kb::kTcStageBytes));
-      const size_t smem = std::max<size_t>(1024 + kb::kTcStoreBytes + (size_t)nst * kb::kTcStageBytes + fixed,
+      // 8 epilogue warps when a >= 4-stage ring still fits beside their staging (cfg5: the split
+      // is bound by its Z^T stores, 3.3 -> 3.1 ms); KB_TC_SPLIT_EPI=4/8 overrides
+      static const int epi_env = [] {
+        const char* v = std::getenv("KB_TC_SPLIT_EPI");
+        return v ? std::atoi(v) : 0;
+      }();
+      auto ring = [&](int epi) {
+        const size_t av = 226 * 1024 - 1024 - kb::tc_store_bytes(epi);
+        return std::min<int>(kb::kTcRingMax, (int)((av - std::min(fixed, av)) / kb::kTcStageBytes));
+      };
+      const int epi = epi_env == 4 ? 4 : (epi_env == 8 || ring(8) >= 4) ? 8 : 4;
+      const int nst = ring(epi);
+      const size_t smem = std::max<size_t>(1024 + kb::tc_store_bytes(epi) + (size_t)nst * kb::kTcStageBytes + fixed,
                                            116 * 1024);  // one CTA per SM
       CUtensorMap mapt, mapz;
-      if (nst >= 3 && tg.n <= kb::kMaxGroups &&
+      if (nst >= 4 && tg.n <= kb::kMaxGroups &&
           make_tmap(&mapt, in_map, g.other, in_rows, op->batch, g.other, in_bs, kb::kTcRB, 4, 128) &&
           make_tmap(&mapz, z, g.len, g.other, (long long)op->batch * op->r, g.len, z_ps, 32, 4, 32,
                     CU_TENSOR_MAP_SWIZZLE_128B)) {
-        auto kern = kb::kb_pass_split_tc;
+        auto kern = epi == 8 ? kb::kb_pass_split_tc<8> : kb::kb_pass_split_tc<4>;
         KB_TRY(allow_smem(kern, smem));
         int parts, nb;
         kb::plan_items(g.len, (g.other + 127) / 128, op->batch, sm_count(), parts, nb);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(nb);
-        cfg.blockDim = dim3(kb::kTcThreads);
+        cfg.blockDim = dim3(kb::tc_split_threads(epi));
         cfg.dynamicSmemBytes = smem;
         cfg.stream = s;
         cudaLaunchAttribute at[1];
@@ -605,7 +617,7 @@ int launch_b(const kb_op* op, Ctx& c, const T* z, const T* tin, const kb::AxisGe
       const long long nch = (long long)((g.len + kb::kTcTS - 1) / kb::kTcTS) * ((g.other + 127) / 128) * op->batch;
       const int nb = (int)std::min<long long>(sm_count(), nch);
       CUtensorMap mapt;
-      if (nst >= 3 && nb * kb::kTcSumEpi <= (op->slots_cap ? op->slots_cap : sum_blocks(op)) &&
+      if (nst >= 4 && nb * kb::kTcSumEpi <= (op->slots_cap ? op->slots_cap : sum_blocks(op)) &&
           make_tmap(&mapt, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, kb::kTcRB, 4, 128)) {
         auto kern = MODE == kb::EPI_UPDATE && !e.want_norms ? kb::kb_pass_sum_tc<MODE, false> : kb::kb_pass_sum_tc<MODE>;
         KB_TRY(allow_smem(kern, smem));

@@ -37,7 +37,11 @@ constexpr int kTcRingMax = KB_TC_RING_MAX;  // shared-memory tile ring depth (ru
 constexpr int kTcG = 3;          // terms per group (two accumulator sets of kTcG x 64 columns)
 constexpr int kTcIssuers = 4;    // one MMA-issuing warp per N-block
 constexpr int kTcConv = 1 + kTcIssuers, kTcEpi = kTcConv + 8;  // first converter / epilogue warp
-constexpr int kTcThreads = 32 * (kTcEpi + 4);  // TMA warp, issuers, 2 x 4 converters, 4 epilogue warps
+// The split pass is instantiated with 4 epilogue warps (one per tensor-memory lane quarter) or 8
+// (two per quarter, each storing one 32-output half of a chunk: at cfg5 the split is bound by its
+// Z^T stores, 3.3 -> 3.1 ms). 8 needs 32 KB more staging, so the host picks it only when a
+// >= 4-stage tile ring still fits beside the bricks.
+__host__ __device__ constexpr int tc_split_threads(int epi) { return 32 * (kTcEpi + epi); }
 constexpr unsigned kTcStageBytes = kTcRB * 128 * 4;  // one [32 rows][128 cols] fp32 tile
 // tensor memory: two accumulator sets of G x 64 columns, then the A stages
 __host__ __device__ __forceinline__ int tc_astages(int G) { return min(kTcStagesMax, (512 - 128 * G) / 32); }
@@ -45,7 +49,8 @@ __host__ __device__ __forceinline__ int tc_astages(int G) { return min(kTcStages
 #define KB_TC_STORE_BUFS 2
 #endif
 constexpr int kTcStoreBufs = KB_TC_STORE_BUFS;  // TMA-store staging buffers per epilogue warp
-constexpr unsigned kTcStoreBytes = 4 * kTcStoreBufs * 4096;  // 4 warps x buffers x [32 L][32 S]
+// epilogue staging: warps x buffers x [32 L][32 S]
+__host__ __device__ constexpr unsigned tc_store_bytes(int epi) { return epi * kTcStoreBufs * 4096; }
 // dynamic shared memory: [staging][tile ring][bricks] (1 KB alignment slack in front)
 
 __host__ __device__ __forceinline__ int tc_ksteps(int Kw) { return (Kw + 62) / 8 + 1; }
@@ -290,7 +295,8 @@ struct PairWalk {
   }
 };
 
-__global__ void __launch_bounds__(kTcThreads, 1)
+template <int EPI>
+__global__ void __launch_bounds__(tc_split_threads(EPI), 1)
 kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap zmap,
                  float* __restrict__ z, long long z_ps, long long z_bs, const unsigned* __restrict__ btab,
                  AxisGeom g, const double* __restrict__ nw2, int r, int batch, int parts, Groups grp, int G,
@@ -302,8 +308,9 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
   __shared__ unsigned tmem_base;
   unsigned char* base = kb_smem_tc + ((1024 - (smem_u32(kb_smem_tc) & 1023)) & 1023);
   float* staging = reinterpret_cast<float*>(base);  // [4 warps][2][32][32], 128-byte swizzled rows
-  float* stages = reinterpret_cast<float*>(base + kTcStoreBytes);  // [nst][32][128]
-  unsigned* bricks = reinterpret_cast<unsigned*>(base + kTcStoreBytes + nst * kTcStageBytes);
+  constexpr unsigned kStore = tc_store_bytes(EPI);
+  float* stages = reinterpret_cast<float*>(base + kStore);  // [nst][32][128]
+  unsigned* bricks = reinterpret_cast<unsigned*>(base + kStore + nst * kTcStageBytes);
   // warp index and tensor-memory base through a lane-0 shuffle: provably warp-uniform, so the MMA
   // operands are computed in uniform registers (no per-MMA register-to-uniform moves)
   const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
@@ -323,7 +330,7 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], kTcIssuers);
-      mbar_init(&acc_empty[b], 4);
+      mbar_init(&acc_empty[b], EPI);
     }
     mbar_init(&bready, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -521,7 +528,7 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     pt.put(7);
   } else {
     // ---------------- epilogue: accumulators -> Z^T rows ----------------
-    const int q = warp & 3;
+    const int q = warp & 3, ew = warp - kTcEpi, hsel = ew >> 2;  // lane quarter, output half (8 warps)
     const unsigned lane_base = tmem + ((unsigned)(32 * q) << 16);
     TcProf p3(g, warp == kTcEpi && lane == 0), p4(g, warp == kTcEpi && lane == 0);
     int chunk = 0, nstore = 0;
@@ -541,7 +548,7 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
         const float oscale = nw2 ? (float)(1.0 / sqrt(nw2[ch.b])) : 1.f;
         for (int gg = 0; gg < gc; ++gg) {
           float* zp = z + ch.b * z_bs + (long long)(g0 + gg) * z_ps + (long long)l * g.len + ch.s0;
-          for (int h = 0; h < kTcTS / 32; ++h) {
+          for (int h = EPI == 8 ? hsel : 0; h < kTcTS / 32; h += EPI / 4) {
             const int s = 32 * h;
             if (s >= ch.cnt) break;
             float va[16], vb[16];
@@ -564,7 +571,7 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
               // swizzled staging row `lane`: 16-byte chunk c at position c ^ (lane & 7)
               if (nstore >= kTcStoreBufs && lane == 0) bulk_wait_read<kTcStoreBufs - 1>();
               __syncwarp();
-              float* sb = staging + (kTcStoreBufs * q + (nstore % kTcStoreBufs)) * 1024;
+              float* sb = staging + (kTcStoreBufs * ew + (nstore % kTcStoreBufs)) * 1024;
 #pragma unroll
               for (int c = 0; c < 8; ++c)
                 reinterpret_cast<float4*>(sb + lane * 32)[c ^ (lane & 7)] =
