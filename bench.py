@@ -496,7 +496,7 @@ def run_row_blocks(args):
     from paper_1901_00913_b200 import workloads as W
     from paper_1901_00913_b200.device import fma_peak
     from paper_1901_00913_b200.shard import (BlockPlan, DeviceBlockBackend, halo_rows, power_iter_row_blocks,
-                                             solve_row_blocks)
+                                             prefer_swap, solve_row_blocks, swapped)
     from paper_1901_00913_b200.solvers import _start_vector
 
     rank, world, local = dist_env()
@@ -509,10 +509,16 @@ def run_row_blocks(args):
     args.dtype = args.dtype or default_dtype(cfg)
     m, iters = cfg.m, cfg.iters
     B, op, _ = build_problem(cfg, args.dtype, seed=0, lipschitz=False)
+    # the single-GPU fast path's axis swap (wider band in pass A): shard the transposed image
+    swap = prefer_swap(op, args.dtype)
+    if swap:
+        op, B = swapped(op), np.ascontiguousarray(B.T)
     plan = BlockPlan(m, m, world, rank, halo_rows(op))
-    # L: matrix-form power iteration (50 steps, fp64, seed 0) sharded like the solve
+    # L: matrix-form power iteration (50 steps, fp64, seed 0) sharded like the solve (transposed
+    # start vector in the swapped frame: the same sequence)
     back64 = DeviceBlockBackend(op, plan, "float64")
-    v0 = _start_vector(0, m, m, "matrix")[plan.g0:plan.g0 + plan.rows]
+    v0 = _start_vector(0, m, m, "matrix")
+    v0 = (v0.T if swap else v0)[plan.g0:plan.g0 + plan.rows]
     L = power_iter_row_blocks(back64, plan, torch.from_numpy(np.ascontiguousarray(v0)).cuda(), 50)
     del back64
     torch.cuda.empty_cache()
@@ -589,7 +595,8 @@ def run_row_blocks(args):
             "data": f"synthetic (seeded phantom + PSF + exact-level Gaussian noise, BASELINE {cfg.name})",
             "config": {"workload": f"{args.config}: {m}x{m} {cfg.bc} BC, w={cfg.w}, r={cfg.r}, lam={cfg.lam}, "
                                    f"x>=0, {iters} iterations per step, row blocks of {plan.rows} rows, "
-                                   f"halo {plan.h}" + (", interior/halo overlap" if overlap else ""),
+                                   f"halo {plan.h}" + (", interior/halo overlap" if overlap else "")
+                                   + (", transposed image (axis swap)" if swap else ""),
                        "global_batch": 1, "parallelism": f"row-blocks{world}",
                        "l2": "flushed between steps (256 MiB write); HBM-backed working set"},
             "e2e": {"value": m * m * iters / 1e6 / e2e_s, "unit": "Mpixel*iterations/s",

@@ -61,6 +61,29 @@ def halo_rows(op, rel_tol: float | None = None) -> int:
     return h
 
 
+def swapped(op):
+    """The operator of the transposed image, Y^T = sum_i K_i X^T H_i^T (H and K swapped)."""
+    from .kron import KronOperator, KronTerm
+
+    return KronOperator(terms=tuple(KronTerm(sigma=t.sigma, H=t.K, K=t.H) for t in op.terms),
+                        shape=(op.shape[1], op.shape[0]), bc=op.bc, sigma=op.sigma, s=op.s, rank=op.rank,
+                        eps=op.eps)
+
+
+def prefer_swap(op, dtype: str) -> bool:
+    """kb_op_create's axis-swap rule (large fp32 images whose axis-1 band is >= 8 wider than the
+    axis-0 band run the wider band in pass A): the sharded solve then splits the TRANSPOSED image
+    into row blocks, so N > 1 runs the same kernels as the single-GPU fast path."""
+    import os
+
+    env = os.environ.get("KB_AXIS_SWAP")
+    if env is not None:
+        return env == "1"
+    if dtype != "float32" or op.shape[0] * op.shape[1] < 4096 * 4096:
+        return False
+    return halo_rows(swapped(op)) >= halo_rows(op) + 8
+
+
 def batch_partition(batch: int, world: int) -> list[tuple[int, int]]:
     """Contiguous balanced image ranges: [(start, count)] per rank (counts may be 0)."""
     base, extra = divmod(batch, world)

@@ -203,3 +203,14 @@ def test_l2_blocked_schedule_is_bit_identical(dtype, monkeypatch, rng):
         assert torch.equal(res["0"], res["3"])
     else:
         assert float((res["3"] - res["0"]).norm() / res["0"].norm()) <= 1e-6
+
+
+def test_row_blocks_of_the_transposed_image_match(rng):
+    """The sharded solve in the axis-swapped frame (bench.py run_row_blocks with prefer_swap):
+    row blocks of B^T with H and K swapped give x^T of the ordinary solve."""
+    psf = random_psf(rng, 11)
+    op = kb.decompose(psf, kb.BoundaryCondition.REFLECTIVE, s=3, shape=(96, 96))
+    B = rng.random((96, 96))
+    got = emulate_row_blocks(shard.swapped(op), np.ascontiguousarray(B.T), 1.3, 0.02, 15, 2)
+    want, _ = port.sfista(op, B, 1.3, 0.02, 15, project=True)
+    np.testing.assert_allclose(got.T, want, rtol=0, atol=1e-10 * np.abs(want).max())

@@ -288,3 +288,16 @@ def test_batch_shard_world2_partitions_without_communication():
     for i in range(5):
         want, _ = port.sfista(ops[i], Bs[i], Ls[i], 0.02, 15, project=True)
         np.testing.assert_allclose(x[i], want, rtol=0, atol=1e-13)
+
+
+def test_prefer_swap_rule():
+    """The bench's sharded axis swap follows kb_op_create's twin rule: large fp32 images whose
+    axis-1 band is >= 8 wider than the axis-0 band."""
+    from paper_1901_00913_b200 import workloads as W
+
+    cfg5 = W.CONFIGS["cfg5"]
+    op = kb.decompose(W.make_psf(cfg5), kb.BoundaryCondition("reflective"), s=10, shape=(16384, 16384))
+    assert shard.prefer_swap(op, "float32") and not shard.prefer_swap(op, "float64")
+    sw = shard.swapped(op)
+    assert shard.halo_rows(sw) >= shard.halo_rows(op) + 8 and not shard.prefer_swap(sw, "float32")
+    assert sw.terms[0].H is op.terms[0].K and sw.shape == (16384, 16384)
