@@ -40,6 +40,7 @@ extern "C" {
 #define KB_ENGINE_MMA_TF32 3 /* persistent 3xTF32 mma.sync kernels */
 #define KB_ENGINE_TC_TF32 4  /* tcgen05 3xTF32 kernels (tensor-memory accumulators) */
 #define KB_ENGINE_PERSIST_F64 5 /* whole-solve persistent fp64 kernel (small images, one launch) */
+#define KB_ENGINE_TC_FUSED 6 /* one-sweep tcgen05 3xTF32 kernel: both passes of an application in one launch */
 
 #define KB_BC_ZERO 0
 #define KB_BC_REFLECTIVE 1

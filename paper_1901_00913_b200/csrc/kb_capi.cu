@@ -24,6 +24,7 @@
 #include "kb_ffma.cuh"
 #include "kb_tf32.cuh"
 #include "kb_tc.cuh"
+#include "kb_fused.cuh"
 #include "kb_blur.cuh"
 #include "kb_norms.cuh"
 #include "kb_persist.cuh"
@@ -85,6 +86,11 @@ struct kb_op {
   unsigned* br_a_corr = nullptr;
   unsigned* br_b_conv = nullptr;
   unsigned* br_b_corr = nullptr;
+  // pass-B bricks of the fused kernel (kb_fused.cuh): half width Hbf = Hb rounded up to a
+  // multiple of 4, so its X tiles start on a 16-byte column (TMA); alias br_b_* when Hb % 4 == 0
+  int Hbf = 0;
+  unsigned* br_bf_conv = nullptr;
+  unsigned* br_bf_corr = nullptr;
   GraphCache* graph = nullptr;
   // > 1 for the strip / image-group views of an L2-blocked solve (sfista_blocked): engine
   // selection then counts the chunks of the whole problem, not of one strip
@@ -781,25 +787,151 @@ int stage_b(const kb_op* op, int adjoint, kb::Epi<T> e, const Work& w, cudaStrea
   return rc;
 }
 
+// ---- one-sweep tcgen05 application (kb_fused.cuh) ------------------------------------------
+// Both passes of one application in one kernel, the Z_i tiles handed over on chip. Applies to
+// fp32 operators whose pass-A band fits a resident 6-stage X tile (Ha <= 31) and whose pass-B
+// band leaves >= 2 N-blocks per 128-column Z tile (Hb <= 27), without exact adjoint folds.
+// KB_FUSED=0 / 1 turns it off / on wherever it applies; by default it takes operators with
+// >= 4 tiles per SM (cfg3's batch, cfg5), where the two-sweep passes are bound by the Z^T
+// round trip through HBM.
+int fused_policy() {
+  static const int p = [] {
+    const char* v = std::getenv("KB_FUSED");
+    return v ? std::atoi(v) : -1;
+  }();
+  return p;
+}
+
+size_t fused_smem(const kb::FuGeom& f) {
+  return 1024 + (size_t)f.nxs * kb::kTcStageBytes + kb::kFuZsBytes + 2 * (size_t)(f.nbr_a + f.nbr_b) * 1024;
+}
+
+long long fused_tiles(const kb_op* op, const kb::FuGeom& f) { return (long long)f.LT * f.nchunks * op->batch; }
+
+bool fused_plan(const kb_op* op, int adjoint, const RowBlock& rb, kb::FuGeom& f) {
+  const int pol = fused_policy();
+  if (pol == 0 || tc_policy(3) == 0 || op->dtype != KB_F32 || !use_tma_f32(op) || op->r > 32) return false;
+  if (!(adjoint ? op->br_a_corr : op->br_a_conv) || !(adjoint ? op->br_bf_corr : op->br_bf_conv)) return false;
+  const bool refl_a = op->bc_a == KB_BC_REFLECTIVE, refl_b = op->bc_b == KB_BC_REFLECTIVE;
+  if (adjoint && ((refl_a && !op->sym_a) || (refl_b && !op->sym_b))) return false;  // exact folds
+  std::memset(&f, 0, sizeof(f));
+  // pass B's window is Hbf = Hb rounded up to 4: the X tile then starts at column c0 - Hbf, a
+  // 16-byte boundary, as TMA requires of a box's innermost coordinate
+  const int Kwa = (2 * op->Ha + 1 + 3) / 4 * 4, Kwb = (2 * op->Hbf + 1 + 3) / 4 * 4;
+  f.qmax_a = (Kwa + 14) >> 3;
+  f.qmax_b = (Kwb + 14) >> 3;
+  const int nk_a = (15 + f.qmax_a + 1) & ~1;  // 8 N-blocks of 16 rows: K-steps 0 .. 14 + qmax_a
+  f.na_a = nk_a / 2;
+  f.nxs = (f.na_a + 1) / 2;
+  if (f.nxs > kb::kFuXStMax) return false;
+  // pass-B N-blocks whose K range (K-steps 0 .. 2(nblk-1) + qmax_b) stays inside the 128-row Z tile
+  f.nblk = std::min(kb::kFuNbMax, (15 - f.qmax_b) / 2 + 1);
+  if (f.qmax_b > 13 || f.nblk < 2) return false;
+  f.nbr_a = kb::tc_bricks(Kwa);
+  f.nbr_b = kb::tc_bricks(Kwb);
+  f.len = op->m;
+  f.n = op->n;
+  f.Ha = op->Ha;
+  f.Hb = op->Hbf;
+  f.nchunks = ((op->n + 15) / 16 + f.nblk - 1) / f.nblk;
+  f.LT = (op->m + kb::kFuL - 1) / kb::kFuL;
+  f.fill_a = refl_a;
+  f.fill_b = refl_b;
+  f.g0 = rb.g0;
+  f.Mg = rb.mg;
+  f.halo_lo = rb.hlo;
+  f.halo_hi = rb.hhi;
+  f.sa_neg = 0;
+  if (adjoint && refl_a)
+    for (int i = 0; i < op->grp_adj.n; ++i)
+      if (op->grp_adj.sign[i] < 0)
+        for (int k = 0; k < op->grp_adj.count[i]; ++k) f.sa_neg |= 1u << (op->grp_adj.start[i] + k);
+  f.dbg = debug_mode();
+  if (fused_smem(f) > 226 * 1024) return false;
+  const long long tiles = fused_tiles(op, f);
+  const int nb = (int)std::min<long long>(sm_count(), tiles);
+  if (nb * kb::kFuEpi > (op->slots_cap ? op->slots_cap : sum_blocks(op))) return false;
+  return pol == 1 || tiles * op->chunk_scale >= 4LL * sm_count();
+}
+
+template <int MODE>
+int launch_fused(const kb_op* op, Ctx& c, int adjoint, const float* in, const kb::FuGeom& f,
+                 const kb::Epi<float>& e, const double* nw2, cudaStream_t s) {
+  const unsigned* ba = adjoint ? op->br_a_corr : op->br_a_conv;
+  const unsigned* bb = adjoint ? op->br_bf_corr : op->br_bf_conv;
+  const float* sb = (adjoint && op->sym_b && op->bc_b == KB_BC_REFLECTIVE) ? static_cast<const float*>(op->sign_b)
+                                                                          : nullptr;
+  const size_t smem = fused_smem(f);
+  static const int grid_cap = [] {  // debugging: fewer CTAs (KB_FUSED_GRID)
+    const char* v = std::getenv("KB_FUSED_GRID");
+    return v ? std::max(1, std::atoi(v)) : 1 << 30;
+  }();
+  const int nb = (int)std::min<long long>(std::min(sm_count(), grid_cap), fused_tiles(op, f));
+  const long long in_bs = (long long)plane_elems(op);
+  CUtensorMap map;
+  if (!make_tmap(&map, in - (long long)f.halo_lo * op->n, op->n, (long long)op->m + f.halo_lo + f.halo_hi,
+                 op->batch, op->n, in_bs, kb::kTcRB, 4, 128))
+    return fail(KB_ERR_ARGUMENT, "input not aligned for the fused tcgen05 kernel");
+  auto kern = MODE == kb::EPI_UPDATE && !e.want_norms ? kb::kb_fused_tc<MODE, false> : kb::kb_fused_tc<MODE>;
+  KB_TRY(allow_smem(kern, smem));
+  if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // warps skip untouched images
+    KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kFuEpi, s));
+  c.slots = nb * kb::kFuEpi;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nb);
+  cfg.blockDim = dim3(kb::kFuThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = use_pdl() ? 1 : 0;
+  c.engine = KB_ENGINE_TC_FUSED;
+  static const bool trace = std::getenv("KB_FUSED_TRACE") != nullptr;
+  if (trace)
+    std::fprintf(stderr,
+                 "[fused] mode %d adj %d m %d n %d batch %d r %d Ha %d Hb %d qa %d qb %d na_a %d nxs %d nblk %d "
+                 "nchunks %d LT %d fill %d/%d sa_neg %x grid %d smem %zu\n",
+                 MODE, adjoint, op->m, op->n, op->batch, op->r, f.Ha, f.Hb, f.qmax_a, f.qmax_b, f.na_a, f.nxs, f.nblk,
+                 f.nchunks, f.LT, f.fill_a, f.fill_b, f.sa_neg, nb, smem);
+  KB_CUDA(cudaLaunchKernelEx(&cfg, kern, map, in, in_bs, ba, bb, f, sb, nw2, e, op->r, op->batch));
+  return KB_OK;
+}
+
+// One application with epilogue MODE: the fused kernel where it applies, else pass A + pass B.
+template <typename T, int MODE>
+int apply_stage(const kb_op* op, int adjoint, const T* in, kb::Epi<T> e, const Work& w, const RowBlock& rb,
+                const double* nw2, cudaStream_t s) {
+  if constexpr (sizeof(T) == 4) {
+    kb::FuGeom f;
+    if (!(debug_mode() & 1024) && epi_aligned(e) && al16(in) && fused_plan(op, adjoint, rb, f)) {
+      KB_TRY(launch_fused<MODE>(op, w.ctx, adjoint, in, f, e, nw2, s));
+      w.ctx.phase[adjoint ? 2 : 0] = w.ctx.phase[adjoint ? 3 : 1] = KB_ENGINE_TC_FUSED;
+      return KB_OK;
+    }
+  }
+  KB_TRY(stage_a<T>(op, adjoint, in, w, rb, nw2, s));
+  if (debug_mode() & 1024) return KB_OK;  // profiling / debugging: pass A only (Z^T left in the workspace)
+  return stage_b<T, MODE>(op, adjoint, e, w, s);
+}
+
 // ---- operator application (one direction) ------------------------------------------------
 template <typename T>
 int apply_t(const kb_op* op, int adjoint, const T* X, T* Y, const Work& w, const RowBlock& rb,
             cudaStream_t s) {
-  KB_TRY(stage_a<T>(op, adjoint, X, w, rb, nullptr, s));
-  if (debug_mode() & 1024) return KB_OK;  // profiling / debugging: pass A only (Z^T left in the workspace)
   kb::Epi<T> e = epi_base<T>(op, kb::EPI_PLAIN);
   e.out = Y;
-  return stage_b<T, kb::EPI_PLAIN>(op, adjoint, e, w, s);
+  return apply_stage<T, kb::EPI_PLAIN>(op, adjoint, X, e, w, rb, nullptr, s);
 }
 
 template <typename T>
 int residual_t(const kb_op* op, const T* Y, const T* B, T* R, const Work& w, const RowBlock& rb,
                cudaStream_t s) {
-  KB_TRY(stage_a<T>(op, 0, Y, w, rb, nullptr, s));
   kb::Epi<T> e = epi_base<T>(op, kb::EPI_RESID);
   e.out = R;
   e.bsub = B;
-  return stage_b<T, kb::EPI_RESID>(op, 0, e, w, s);
+  return apply_stage<T, kb::EPI_RESID>(op, 0, Y, e, w, rb, nullptr, s);
 }
 
 template <typename T>
@@ -824,9 +956,8 @@ template <typename T>
 int update_t(const kb_op* op, const T* R, T* X, T* Y, const Work& w, const RowBlock& rb,
              double beta, int k, const double* Ldev, const double* ddev, int project,
              int* nonfinite, double* norms_out, cudaStream_t s) {
-  KB_TRY(stage_a<T>(op, 1, R, w, rb, nullptr, s));
-  KB_TRY((stage_b<T, kb::EPI_UPDATE>(op, 1, update_epi<T>(op, X, Y, w, beta, k, Ldev, ddev, project,
-                                                          nonfinite, norms_out != nullptr), w, s)));
+  KB_TRY((apply_stage<T, kb::EPI_UPDATE>(op, 1, R, update_epi<T>(op, X, Y, w, beta, k, Ldev, ddev, project,
+                                                                 nonfinite, norms_out != nullptr), w, rb, nullptr, s)));
   if (norms_out) {
     kb::kb_reduce_partials<<<op->batch, 256, 0, s>>>(w.partials, w.ctx.slots, 3, norms_out,
                                                       op->batch, 1);
@@ -915,6 +1046,9 @@ kb_op group_view(const kb_op* op, int b0, int gb, long long scale) {
   v.br_a_corr = static_cast<unsigned*>(off(op->br_a_corr, bra, sizeof(unsigned)));
   v.br_b_conv = static_cast<unsigned*>(off(op->br_b_conv, brb, sizeof(unsigned)));
   v.br_b_corr = static_cast<unsigned*>(off(op->br_b_corr, brb, sizeof(unsigned)));
+  const long long brbf = (long long)op->r * kb::tc_bricks((2 * op->Hbf + 1 + 3) / 4 * 4) * 256;
+  v.br_bf_conv = static_cast<unsigned*>(off(op->br_bf_conv, brbf, sizeof(unsigned)));
+  v.br_bf_corr = static_cast<unsigned*>(off(op->br_bf_corr, brbf, sizeof(unsigned)));
   return v;
 }
 
@@ -1021,17 +1155,15 @@ int power_t(const kb_op* op, T* v, T* wbuf, const Work& w, int iters, double* hi
     T* cur = (k & 1) ? wbuf : v;   // holds w_{k-1} (unnormalised) or v_0
     T* nxt = (k & 1) ? v : wbuf;
     const double* nw2 = k == 0 ? nullptr : hist + (size_t)(k - 1) * 2 * op->batch + op->batch;
-    KB_TRY(stage_a<T>(op, 0, cur, w, rb, nw2, s));
     kb::Epi<T> e1 = epi_base<T>(op, kb::EPI_PLAIN);
     e1.out = u;
-    KB_TRY((stage_b<T, kb::EPI_PLAIN>(op, 0, e1, w, s)));
-    KB_TRY(stage_a<T>(op, 1, u, w, rb, nullptr, s));
+    KB_TRY((apply_stage<T, kb::EPI_PLAIN>(op, 0, cur, e1, w, rb, nw2, s)));
     kb::Epi<T> e2 = epi_base<T>(op, kb::EPI_POWER);
     e2.out = nxt;
     e2.vin = cur;
     e2.vnw2 = nw2;
     e2.partials = w.partials;
-    KB_TRY((stage_b<T, kb::EPI_POWER>(op, 1, e2, w, s)));
+    KB_TRY((apply_stage<T, kb::EPI_POWER>(op, 1, u, e2, w, rb, nullptr, s)));
     kb::kb_reduce_partials<<<op->batch, 256, 0, s>>>(w.partials, w.ctx.slots, 2,
                                                       hist + (size_t)k * 2 * op->batch,
                                                       op->batch, 1);
@@ -1080,17 +1212,16 @@ int upload_tables(kb_op* op, int dlo, int w, const double* taps, const std::vect
 
 // brick tables of an axis' two fp32 tap tables, when its band can take the tcgen05 passes
 int build_brick_tables(kb_op* op, int H, int Wp, const void* conv, const void* corr, unsigned** bconv,
-                       unsigned** bcorr) {
-  const int Kw = (2 * H + 1 + 3) / 4 * 4;
-  if (Kw < 32 && tc_policy(3) != 1) return KB_OK;
-  const int nbr = kb::tc_bricks(Kw);
+                       unsigned** bcorr, int shift = 0) {
+  const int Kw = (2 * H + 1 + 3) / 4 * 4;  // every fp32 band: the fused kernel takes narrow ones too
+  const int nbr = kb::tc_bricks((2 * (H + shift) + 1 + 3) / 4 * 4);
   const long long bt = (long long)op->batch * op->r;
   const size_t bytes = (size_t)bt * nbr * 1024;
   KB_CUDA(cudaMalloc(bconv, bytes));
   KB_CUDA(cudaMalloc(bcorr, bytes));
   const int blocks = (int)std::min<long long>((bt * nbr * 128 + 255) / 256, 4096);
-  kb::kb_build_bricks<<<blocks, 256>>>(static_cast<const float*>(conv), Wp, Kw, nbr, bt, *bconv);
-  kb::kb_build_bricks<<<blocks, 256>>>(static_cast<const float*>(corr), Wp, Kw, nbr, bt, *bcorr);
+  kb::kb_build_bricks<<<blocks, 256>>>(static_cast<const float*>(conv), Wp, Kw, nbr, bt, *bconv, shift);
+  kb::kb_build_bricks<<<blocks, 256>>>(static_cast<const float*>(corr), Wp, Kw, nbr, bt, *bcorr, shift);
   KB_CUDA(cudaGetLastError());
   KB_CUDA(cudaDeviceSynchronize());
   return KB_OK;
@@ -1132,6 +1263,8 @@ void free_op(kb_op* op) {
   cudaFree(op->br_a_corr);
   cudaFree(op->br_b_conv);
   cudaFree(op->br_b_corr);
+  if (op->br_bf_conv != op->br_b_conv) cudaFree(op->br_bf_conv);
+  if (op->br_bf_corr != op->br_b_corr) cudaFree(op->br_bf_corr);
   if (op->graph) {
     if (op->graph->exec) cudaGraphExecDestroy(op->graph->exec);
     delete op->graph;
@@ -1269,7 +1402,20 @@ int time_passes_t(const kb_op* op, const T* Y, const T* B, T* R, T* X, T* Yio, c
   const kb::Epi<T> eu = update_epi<T>(op, X, Yio, w, 0.0, 1, w.scal, w.scal + op->batch, 1,
                                       nonfinite, false);
   int rc = KB_OK;
+  // fused directions (kb_fused.cuh): phase 0 / 2 time the one-sweep kernel, phase 1 / 3 are empty
+  bool fused[2] = {false, false};
+  if constexpr (sizeof(T) == 4) {
+    kb::FuGeom f;
+    fused[0] = !(debug_mode() & 1024) && epi_aligned(er) && al16(Y) && fused_plan(op, 0, rb, f);
+    fused[1] = !(debug_mode() & 1024) && epi_aligned(eu) && al16(R) && fused_plan(op, 1, rb, f);
+  }
   for (int phase = 0; phase < 4 && rc == KB_OK; ++phase) {
+    if (fused[phase >> 1] && (phase & 1)) {
+      ms4[phase] = 0.f;
+      std::lock_guard<std::mutex> lock(g_phase_mu);
+      op->phase_engine[phase] = KB_ENGINE_TC_FUSED;
+      continue;
+    }
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
@@ -1278,9 +1424,15 @@ int time_passes_t(const kb_op* op, const T* Y, const T* B, T* R, T* X, T* Yio, c
     }
     for (int rep = 0; rep < reps && rc == KB_OK; ++rep) {
       switch (phase) {
-        case 0: rc = stage_a<T>(op, 0, Y, w, rb, nullptr, s); break;
+        case 0:
+          rc = fused[0] ? apply_stage<T, kb::EPI_RESID>(op, 0, Y, er, w, rb, nullptr, s)
+                        : stage_a<T>(op, 0, Y, w, rb, nullptr, s);
+          break;
         case 1: rc = stage_b<T, kb::EPI_RESID>(op, 0, er, w, s); break;
-        case 2: rc = stage_a<T>(op, 1, R, w, rb, nullptr, s); break;
+        case 2:
+          rc = fused[1] ? apply_stage<T, kb::EPI_UPDATE>(op, 1, R, eu, w, rb, nullptr, s)
+                        : stage_a<T>(op, 1, R, w, rb, nullptr, s);
+          break;
         default: rc = stage_b<T, kb::EPI_UPDATE>(op, 1, eu, w, s); break;
       }
     }
@@ -1408,6 +1560,14 @@ int kb_op_create(kb_op** out, int dtype, int m, int n, int r, int batch, int bc_
       rc = build_brick_tables(op, Ha, op->Wpa, op->ta_conv, op->ta_corr, &op->br_a_conv, &op->br_a_corr);
     if (rc == KB_OK)
       rc = build_brick_tables(op, Hb, op->Wpb, op->tb_conv, op->tb_corr, &op->br_b_conv, &op->br_b_corr);
+    op->Hbf = (Hb + 3) / 4 * 4;
+    if (rc == KB_OK && op->Hbf != Hb)
+      rc = build_brick_tables(op, Hb, op->Wpb, op->tb_conv, op->tb_corr, &op->br_bf_conv, &op->br_bf_corr,
+                              op->Hbf - Hb);
+    if (op->Hbf == Hb) {
+      op->br_bf_conv = op->br_b_conv;
+      op->br_bf_corr = op->br_b_corr;
+    }
   }
   if (rc != KB_OK) {
     free_op(op);

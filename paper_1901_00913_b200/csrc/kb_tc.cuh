@@ -240,14 +240,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // (image, term) the nbr bricks of kb_pass_split_tc / kb_pass_sum_tc in their shared-memory
 // layout, [batch][r][nbr][hi 128 | lo 128 words], so a pass loads a term's bricks with one bulk
 // copy instead of rebuilding them on its threads.
+// `shift` > 0 builds the bricks of the same taps for a window widened by `shift` on each side
+// (half width H + shift; the fused kernel's TMA-aligned tile origin, kb_fused.cuh)
 __global__ void kb_build_bricks(const float* __restrict__ tin, int Wp, int Kw, int nbr, long long bt_total,
-                                unsigned* __restrict__ out) {
+                                unsigned* __restrict__ out, int shift = 0) {
   const long long total = bt_total * nbr * 128;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     const long long bt = idx / (nbr * 128);
     const int rem = (int)(idx - bt * nbr * 128), qb = rem >> 7, e = rem & 127, nn = e >> 3, kk = e & 7;
-    const int ti = 8 * qb + kk - nn;
+    const int ti = 8 * qb + kk - nn - shift;
     const float c = (ti >= 0 && ti < Kw) ? tin[bt * Wp + ti] : 0.f;
     unsigned h, l;
     tf32_split_rn(c, h, l);

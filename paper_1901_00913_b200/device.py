@@ -28,7 +28,7 @@ KB_OK, KB_ERR_ARGUMENT, KB_ERR_CUDA, KB_ERR_NUMERIC = 0, 2, 3, 4
 KB_F64, KB_F32 = 0, 1
 KB_PEAK_TC_TF32 = 2
 # pass engines (kb_last_engines)
-ENGINES = {0: "generic", 1: "ffma", 2: "dmma", 3: "mma_tf32", 4: "tcgen05_tf32", 5: "persist_f64"}
+ENGINES = {0: "generic", 1: "ffma", 2: "dmma", 3: "mma_tf32", 4: "tcgen05_tf32", 5: "persist_f64", 6: "tcgen05_fused"}
 KB_BC_ZERO, KB_BC_REFLECTIVE = 0, 1
 KB_RESID_NORMS_WORK = 2 * 8 * 296  # include/kronblur_b200.h
 INT_MAX = 2**31 - 1
