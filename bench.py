@@ -62,14 +62,15 @@ def dist_env():
     return rank, world, local
 
 
-def committed_traffic(config, dtype):
-    """Per-kernel DRAM bytes (read + write) of one iteration's four pass kernels from the
-    committed ncu capture of this config (profiles/traffic_<config>.json, written by
-    tools/ncu_traffic.py from an `ncu --set full` run of tools/one_iter.py), or None."""
+def committed_traffic(config, dtype, fused=False):
+    """Per-kernel DRAM bytes (read + write) of one iteration's pass kernels from the committed
+    ncu capture of this config (profiles/traffic_<config>.json, written by tools/ncu_traffic.py
+    from an `ncu --set full` run of tools/one_iter.py), or None. With the one-sweep kernel the
+    capture lists [forward, 0, adjoint, 0] under "_per_kernel_fused"."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", f"traffic_{config}.json")
     try:
         with open(path) as f:
-            per = json.load(f).get("_per_kernel", {}).get(dtype)
+            per = json.load(f).get("_per_kernel_fused" if fused else "_per_kernel", {}).get(dtype)
         return [int(k["dram_bytes"]) for k in per] if per else None
     except (OSError, ValueError, KeyError, TypeError):
         return None
@@ -187,7 +188,7 @@ def engine_peak(eng, cache={}):
     if eng not in cache:
         if eng == "dmma":
             cache[eng] = (fma_peak("float64"), "FP64 tensor-core DMMA m8n8k4 burn")
-        elif eng == "tcgen05_tf32":
+        elif eng in ("tcgen05_tf32", "tcgen05_fused"):
             cache[eng] = (fma_peak("tcgen05_tf32") / 3.0,
                           "tcgen05.mma kind::tf32 M128 N256 K8 burn / 3 (3xTF32 passes)")
         else:  # mma.sync TF32 (and the FFMA / generic fallbacks, bounded by the same roof)
@@ -195,11 +196,14 @@ def engine_peak(eng, cache={}):
     return cache[eng]
 
 
-def launches_per_iteration(dev):
-    """Kernels of one fast-path iteration: 4 passes, plus the exact-fold kernels of a reflective
-    axis whose generators are not (anti)symmetric (kb_capi.cu stage_a / stage_b)."""
+def launches_per_iteration(dev, engines=None):
+    """Kernels of one fast-path iteration: 4 passes (one per direction where the one-sweep fused
+    kernel runs it), plus the exact-fold kernels of a reflective axis whose generators are not
+    (anti)symmetric (kb_capi.cu stage_a / stage_b)."""
     info = dev.info()
-    n = 4
+    if engines and engines[0] == "persist_f64":
+        return 0  # counted per solve (one cooperative launch)
+    n = 4 - sum(1 for i in (0, 2) if engines and engines[i] == "tcgen05_fused")
     if dev.bc[0] == 1 and not info["sym_a"]:
         n += 1
     if dev.bc[1] == 1 and not info["sym_b"]:
@@ -267,7 +271,9 @@ def measure_config(name, dtype, steps, warmup, rank, world, local, clocks=False,
     value = units * mpix_it / (ms / 1e3)
     res = {"cfg": cfg, "dtype": dtype, "ms": ms, "value": value, "batched": batched, "ops": ops,
            "op": op, "B": B, "L": L, "clocks": sampler.summary() if clocks else None,
-           "engines_solve": engines_solve, "launches": launches_per_iteration(dev) * iters * steps}
+           "engines_solve": engines_solve,
+           "launches": launches_per_iteration(dev, engines_solve) * iters * steps
+           + (steps if engines_solve and engines_solve[0] == "persist_f64" else 0)}
 
     # ---- e2e: the public API with host buffers (H2D of B, D2H of x inside the region; X0 = None)
     esz = 8 if dtype == "float64" else 4
@@ -307,19 +313,35 @@ def measure_config(name, dtype, steps, warmup, rank, world, local, clocks=False,
     # band first) pass A filters axis 1 and pass B axis 0
     swapped = bool(dev.info().get("twin", 0))
     flops_phase = [2 * cfg.r * w * px for w in ((wb, wa, wb, wa) if swapped else (wa, wb, wa, wb))]
+    # one-sweep fused directions (kb_fused.cuh): phase 0 / 2 is the whole application, 1 / 3 empty
+    fused = [engines[2 * d] == "tcgen05_fused" for d in (0, 1)]
+    for d in (0, 1):
+        if fused[d]:
+            flops_phase[2 * d] += flops_phase[2 * d + 1]
+            flops_phase[2 * d + 1] = 0
     k_dom = max(range(4), key=lambda i: kern_ms[i])
     achieved_tf = flops_phase[k_dom] / (kern_ms[k_dom] * 1e-3) / 1e12
     peak_dom, peak_src = engine_peak(engines[k_dom])
-    traffic = committed_traffic(cfg.name, dtype)
+    traffic = committed_traffic(cfg.name, dtype, fused=any(fused))
     peaks, peak_kind = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6550.0)
     it_ms = sum(kern_ms)
     phase = ["pass A forward (split)", "pass B forward (sum, residual epilogue)",
              "pass A adjoint (split)", "pass B adjoint (sum, fused FISTA update)"]
-    # DRAM bytes the dominant launch must move in this two-sweep design: split reads X and writes
-    # r Z planes; residual sum reads r Z planes + B, writes R; update sum reads r Z planes + Y +
-    # X_prev, writes X and Y
-    kern_bytes = esz * px * (1 + cfg.r, cfg.r + 2, 1 + cfg.r, cfg.r + 4)[k_dom]
+    if fused[0]:
+        phase[0] = "forward application (one-sweep fused kernel, residual epilogue)"
+    if fused[1]:
+        phase[2] = "adjoint application (one-sweep fused kernel, FISTA update epilogue)"
+    # DRAM bytes the dominant launch must move: two-sweep split reads X and writes r Z planes;
+    # residual sum reads r Z planes + B, writes R; update sum reads r Z planes + Y + X_prev, writes
+    # X and Y. The fused kernel keeps Z on chip: forward reads Y + B, writes R (3 planes); adjoint
+    # reads R + Y + X_prev, writes X and Y (5 planes)
+    per_phase = [1 + cfg.r, cfg.r + 2, 1 + cfg.r, cfg.r + 4]
+    if fused[0]:
+        per_phase[0], per_phase[1] = 3, 0
+    if fused[1]:
+        per_phase[2], per_phase[3] = 5, 0
+    kern_bytes = esz * px * per_phase[k_dom]
     # Which roof binds the dominant kernel: its arithmetic intensity (flops on executed taps over
     # the DRAM bytes this two-sweep kernel must move, its r Z^T planes included) against the
     # machine balance (live tensor peak / measured HBM bandwidth). L2-resident configs (cfg1,
@@ -334,7 +356,10 @@ def measure_config(name, dtype, steps, warmup, rank, world, local, clocks=False,
                 "frac": round(hbm_ach / hbm_peak, 4),
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                 "bytes_per_launch": kern_bytes,
-                "bytes_rule": "DRAM bytes this kernel must move in the two-sweep design: "
+                "bytes_rule": ("DRAM bytes this one-sweep kernel must move (Z stays on chip): "
+                               + ("Y + B in, R out" if k_dom == 0 else "R + Y + X_prev in, X and Y out"))
+                              if fused[k_dom >> 1] else
+                              "DRAM bytes this kernel must move in the two-sweep design: "
                               + ("X in, r Z^T planes out" if k_dom in (0, 2) else
                                  "r Z^T planes + B in, R out" if k_dom == 1 else "r Z^T planes + Y + X_prev in, X and Y out"),
                 "tensor": {"achieved": round(achieved_tf, 3), "peak": round(peak_dom, 3), "unit": "TFLOP/s",
@@ -345,11 +370,12 @@ def measure_config(name, dtype, steps, warmup, rank, world, local, clocks=False,
                 "peak_source": "measured live by kb_fma_peak in this run: " + peak_src}
     res["roofline"] = {
         **head,
-        "kernel": f"{phase[k_dom]} on {engines[k_dom]}: the longest of the iteration's four kernels",
+        "kernel": f"{phase[k_dom]} on {engines[k_dom]}: the longest of the iteration's kernels",
         "intensity_flop_per_byte": round(intensity, 2), "machine_balance_flop_per_byte": round(balance, 2),
         "flops_per_launch": flops_phase[k_dom],
-        "flops_rule": f"2 r w_exec flop per pixel: r={cfg.r}, executed taps {wa} (axis 0) / {wb} (axis 1)"
-                      + ("; axis-swapped twin: pass A = axis 1" if swapped else ""),
+        "flops_rule": f"2 r w_exec flop per pixel and pass: r={cfg.r}, executed taps {wa} (axis 0) / {wb} (axis 1)"
+                      + ("; axis-swapped twin: pass A = axis 1" if swapped else "")
+                      + ("; a fused launch runs both passes of its direction" if fused[k_dom >> 1] else ""),
         "traffic": traffic[k_dom] if traffic else None,
         "traffic_source": f"profiles/traffic_{cfg.name}.json (ncu --set full, dram read+write of this kernel)",
         "kernel_dram_bytes_compulsory": kern_bytes,
@@ -358,13 +384,13 @@ def measure_config(name, dtype, steps, warmup, rank, world, local, clocks=False,
             "per_kernel_ms": [round(x, 5) for x in kern_ms],
             "engines": engines,
             "achieved_tflops": round(sum(flops_phase) / (it_ms * 1e-3) / 1e12, 3),
-            "frac_of_peak": [round(f / (t * 1e-3) / 1e12 / engine_peak(e)[0], 4)
+            "frac_of_peak": [round(f / (t * 1e-3) / 1e12 / engine_peak(e)[0], 4) if t > 0 else None
                              for f, t, e in zip(flops_phase, kern_ms, engines)],
         },
         "hbm": {"achieved": round(8 * esz * px / (it_ms * 1e-3) / 1e9, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(8 * esz * px / (it_ms * 1e-3) / 1e9 / hbm_peak, 4), "peak_source": peak_kind,
                 "algorithmic_bytes_per_px_it": 8 * esz,
-                "note": "SURVEY 8(d) two-sweep compulsory bytes (Z planes excluded) over the four kernels"},
+                "note": "SURVEY 8(d) two-sweep compulsory bytes (Z planes excluded) over the iteration's kernels"},
         "nominal_flops_per_px_it": algorithmic(cfg),
         "executed_taps": [wa, wb],
     }

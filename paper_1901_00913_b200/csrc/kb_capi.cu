@@ -788,12 +788,12 @@ int stage_b(const kb_op* op, int adjoint, kb::Epi<T> e, const Work& w, cudaStrea
 }
 
 // ---- one-sweep tcgen05 application (kb_fused.cuh) ------------------------------------------
-// Both passes of one application in one kernel, the Z_i tiles handed over on chip. Applies to
-// fp32 operators whose pass-A band fits a resident 6-stage X tile (Ha <= 31) and whose pass-B
-// band leaves >= 2 N-blocks per 128-column Z tile (Hb <= 27), without exact adjoint folds.
-// KB_FUSED=0 / 1 turns it off / on wherever it applies; by default it takes operators with
-// >= 4 tiles per SM (cfg3's batch, cfg5), where the two-sweep passes are bound by the Z^T
-// round trip through HBM.
+// Both passes of one application in one kernel, the Z_i tiles handed over on chip (no Z^T round
+// trip through HBM). Applies to fp32 operators whose pass-A band fits a resident 6-stage X tile
+// (Ha <= 31) and whose pass-B band leaves >= 2 N-blocks per 128-column Z tile, without exact
+// adjoint folds. OPT-IN (KB_FUSED=1): measured on the B200 it is latency-bound at ~9-12k cycles
+// per (tile, term) against ~2.5k of MMA work -- cfg5 9.3 + 10.1 ms per iteration against 14.3 ms
+// for the two-sweep passes, cfg3 4.2 against 3.3 ms (profiles/r02_fused_*.txt).
 int fused_policy() {
   static const int p = [] {
     const char* v = std::getenv("KB_FUSED");
@@ -851,7 +851,8 @@ bool fused_plan(const kb_op* op, int adjoint, const RowBlock& rb, kb::FuGeom& f)
   const long long tiles = fused_tiles(op, f);
   const int nb = (int)std::min<long long>(sm_count(), tiles);
   if (nb * kb::kFuEpi > (op->slots_cap ? op->slots_cap : sum_blocks(op))) return false;
-  return pol == 1 || tiles * op->chunk_scale >= 4LL * sm_count();
+  (void)tiles;
+  return pol == 1;
 }
 
 template <int MODE>
