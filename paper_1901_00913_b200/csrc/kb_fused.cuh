@@ -118,59 +118,6 @@ __device__ __forceinline__ int fu_nab(const FuGeom& f, int nblk) {  // pass-B A 
   return (2 * (nblk - 1) + f.qmax_b + 2) >> 1;
 }
 
-// out-of-domain entry of the X tile on a reflective axis: the folded source times the fill
-// signs (zero where the fold leaves the domain or the axis has zero boundary conditions)
-__device__ __forceinline__ float fu_edge(const float* __restrict__ in, long long img, int lr, int col,
-                                         const FuGeom& f, float sa, float sb, float tile_v) {
-  const int gr = f.g0 + lr;
-  const bool rin = gr >= 0 && gr < f.Mg, cin = col >= 0 && col < f.n;
-  if (rin && cin) return tile_v;
-  float s = 1.f;
-  int rr = gr, cc = col;
-  if (!rin) {
-    if (!f.fill_a) return 0.f;
-    rr = kb_fold(gr, f.Mg);
-    s = sa;
-  }
-  if (!cin) {
-    if (!f.fill_b) return 0.f;
-    cc = kb_fold(col, f.n);
-    s *= sb;
-  }
-  const int lrr = rr - f.g0;
-  if (rr < 0 || cc < 0 || lrr < -f.halo_lo || lrr >= f.len + f.halo_hi) return 0.f;
-  return s * in[img + (long long)lrr * f.n + cc];
-}
-
-// The same entry taken from the resident X tile: the fold source of every row / column the tile's
-// outputs need lies inside the tile (rows [l0 - Ha, l0 + 128 + Ha), columns [c0 - Hb, c0 - Hb
-// + 128)); global memory only for sources outside it (images smaller than the tile's margins)
-__device__ __forceinline__ float fu_edge_tile(const float* xs, const float* __restrict__ in, long long img, int lr,
-                                              int col, const FuGeom& f, int l0, int c0, float sa, float sb,
-                                              float tile_v) {
-  const int gr = f.g0 + lr;
-  const bool rin = gr >= 0 && gr < f.Mg, cin = col >= 0 && col < f.n;
-  if (rin && cin) return tile_v;
-  float s = 1.f;
-  int rr = gr, cc = col;
-  if (!rin) {
-    if (!f.fill_a) return 0.f;
-    rr = kb_fold(gr, f.Mg);
-    s = sa;
-  }
-  if (!cin) {
-    if (!f.fill_b) return 0.f;
-    cc = kb_fold(col, f.n);
-    s *= sb;
-  }
-  if (rr < 0 || cc < 0) return 0.f;
-  const int ti = rr - f.g0 - (l0 - f.Ha), tc = cc - (c0 - f.Hb);
-  if (ti >= 0 && ti < 32 * f.nxs && tc >= 0 && tc < 128) return s * xs[ti * 128 + tc];
-  const int lrr = rr - f.g0;
-  if (lrr < -f.halo_lo || lrr >= f.len + f.halo_hi) return 0.f;
-  return s * in[img + (long long)lrr * f.n + cc];
-}
-
 __device__ __forceinline__ void tc_ld32(unsigned addr, float (&v)[32]) {
   unsigned u[32];
   asm volatile(
@@ -493,9 +440,19 @@ kb_fused_tc(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ 
     while (walk.next(t, f)) {
       const int col = t.c0 - f.Hb + tcol;
       const bool cedge = f.fill_b && (t.c0 - f.Hb < 0 || t.c0 - f.Hb + 128 > f.n);
+      // edge tiles: this lane's column source in the resident tile (identity inside the domain,
+      // the fold source outside it; -1: zero -- the fold leaves the domain or the source lies
+      // outside the tile, which only columns no output of the tile reads can hit)
+      int csrc = tcol;
+      bool cflip = false;
+      if (col < 0 || col >= f.n) {
+        const int cc = f.fill_b ? kb_fold(col, f.n) : -1;
+        csrc = cc < 0 ? -1 : cc - (t.c0 - f.Hb);
+        if (csrc >= 128) csrc = -1;
+        cflip = true;
+      }
       // a tile with reflected rows or columns reads fold sources from any of its X stages
       const bool edge_tile = cedge || (f.fill_a && (f.g0 + t.l0 - f.Ha < 0 || f.g0 + t.l0 + kFuL + f.Ha > f.Mg));
-      const long long img = (long long)t.b * in_bs;
       for (int term = 0; term < r; ++term) {
         const int uu = T * r + term;
         const float sa = (f.sa_neg >> term) & 1 ? -1.f : 1.f;
@@ -528,7 +485,20 @@ kb_fused_tc(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ 
               for (int i = 0; i < 16; ++i) xv[i] = tile[i * 128];
               if (redge || cedge) {
 #pragma unroll
-                for (int i = 0; i < 16; ++i) xv[i] = fu_edge_tile(xs, in, img, lr0 + i, col, f, t.l0, t.c0, sa, sb, xv[i]);
+                for (int i = 0; i < 16; ++i) {
+                  // row source (warp-uniform): the row itself, its fold source, or none
+                  const int gr = f.g0 + lr0 + i;
+                  int ti = 32 * j + 16 * h + i;
+                  bool ok = csrc >= 0;
+                  float sg = cflip ? sb : 1.f;
+                  if (gr < 0 || gr >= f.Mg) {
+                    const int rr = f.fill_a ? kb_fold(gr, f.Mg) : -1;
+                    ok = ok && rr >= 0;
+                    ti = rr - f.g0 - (t.l0 - f.Ha);
+                    sg *= sa;
+                  }
+                  xv[i] = (ok && ti >= 0 && ti < 32 * f.nxs) ? sg * xs[ti * 128 + csrc] : 0.f;
+                }
               }
               unsigned hi[16], lo[16];
 #pragma unroll
