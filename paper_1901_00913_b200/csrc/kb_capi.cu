@@ -25,6 +25,7 @@
 #include "kb_tf32.cuh"
 #include "kb_tc.cuh"
 #include "kb_fused.cuh"
+#include "kb_tc1.cuh"
 #include "kb_blur.cuh"
 #include "kb_norms.cuh"
 #include "kb_persist.cuh"
@@ -612,6 +613,43 @@ int launch_b(const kb_op* op, Ctx& c, const T* z, const T* tin, const kb::AxisGe
     }
   } else {
     const unsigned* btab = brick_table(op, tin);
+    // 128-output chunks with one accumulator across the r terms (kb_tc1.cuh) for bands up to
+    // Kw = 64 (KB_TC_SUM1=0 / 1: off / on wherever the tcgen05 sum pass runs)
+    static const int sum1_env = [] {
+      const char* v = std::getenv("KB_TC_SUM1");
+      return v ? std::atoi(v) : -1;
+    }();
+    if (btab && use_tc(op, g, 128) && persistent_ok && sum1_env != 0 && (sum1_env == 1 || g.Kw <= 64)) {
+      const int nbr = kb::tc_bricks(g.Kw);
+      const size_t fixed = 2 * (size_t)nbr * 1024;
+      const size_t avail = 226 * 1024 - 1024;
+      const int nst = fixed < avail ? std::min<int>(kb::kTcRingMax, (int)((avail - fixed) / kb::kTcStageBytes)) : 0;
+      const size_t smem = std::max<size_t>(1024 + (size_t)nst * kb::kTcStageBytes + fixed, 116 * 1024);
+      const long long nch = (long long)((g.len + kb::kT1TS - 1) / kb::kT1TS) * ((g.other + 127) / 128) * op->batch;
+      const int nb = (int)std::min<long long>(sm_count(), nch);
+      CUtensorMap mapt;
+      if (nst >= 4 && nb * kb::kT1Epi <= (op->slots_cap ? op->slots_cap : sum_blocks(op)) &&
+          make_tmap(&mapt, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, kb::kTcRB, 4, 128)) {
+        auto kern = MODE == kb::EPI_UPDATE && !e.want_norms ? kb::kb_pass_sum_tc1<MODE, false> : kb::kb_pass_sum_tc1<MODE>;
+        KB_TRY(allow_smem(kern, smem));
+        if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // warps skip untouched images
+          KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kT1Epi, s));
+        c.slots = nb * kb::kT1Epi;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(nb);
+        cfg.blockDim = dim3(kb::kT1Threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = use_pdl() ? 1 : 0;
+        c.engine = KB_ENGINE_TC_TF32;
+        KB_CUDA(cudaLaunchKernelEx(&cfg, kern, mapt, op->r, btab, g, e, op->batch, nst));
+        return KB_OK;
+      }
+    }
     if (btab && use_tc(op, g, 128) && persistent_ok) {
       // tcgen05 sum pass (kb_tc.cuh): double-buffered bricks from the brick table, tile ring
       const int nbr = kb::tc_bricks(g.Kw);

@@ -144,6 +144,9 @@ __device__ __forceinline__ void tc_ld32(unsigned addr, float (&v)[32]) {
 #ifndef KB_FU_PROF
 #define KB_FU_PROF 0
 #endif
+#ifndef KB_FU_NOLDS
+#define KB_FU_NOLDS 0  // profiling: X converters skip their shared-memory loads
+#endif
 struct FuProf {
   unsigned long long acc = 0, t0 = 0;
   bool on;
@@ -482,7 +485,7 @@ kb_fused_tc(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ 
               const bool redge = f.fill_a && (f.g0 + lr0 < 0 || f.g0 + lr0 + 16 > f.Mg);
               float xv[16];
 #pragma unroll
-              for (int i = 0; i < 16; ++i) xv[i] = tile[i * 128];
+              for (int i = 0; i < 16; ++i) xv[i] = KB_FU_NOLDS ? __int_as_float(0x3f800000 + i + tcol) : tile[i * 128];
               if (redge || cedge) {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
