@@ -394,6 +394,12 @@ def measure_config(name, dtype, steps, warmup, rank, world, local, clocks=False,
         "nominal_flops_per_px_it": algorithmic(cfg),
         "executed_taps": [wa, wb],
     }
+    if traffic and len(traffic) == 4 and all(t >= 0 for t in traffic):
+        # the whole iteration's DRAM bytes as ncu measured them (committed capture of the same
+        # kernels) over this run's iteration time: how close the iteration runs to the HBM roof
+        tb = float(sum(traffic))
+        res["roofline"]["iteration"]["dram_bytes_ncu"] = int(tb)
+        res["roofline"]["iteration"]["dram_frac"] = round(tb / (it_ms * 1e-3) / 1e9 / hbm_peak, 4)
     if engines_solve and engines_solve[0] == "persist_f64":
         # one cooperative launch runs the whole solve: its roofline is the solve's own rate
         per_it_s = ms * 1e-3 / iters
