@@ -13,7 +13,7 @@
 //       transposed in tensor memory by the converter warps, B = Toeplitz bricks), accumulated in
 //       a double-buffered 128 x 128 tensor-memory accumulator;
 //   hand-off: four drain warps move the accumulator (lane = column t) into a [t][l] shared tile
-//       (16-byte chunks XOR-swizzled by t & 7, conflict-free both ways), then read it back with
+//       (rows padded to 132 floats, conflict-free both ways), then read it back with
 //       lane = row l, split into tf32 hi + lo and store pass B's A stages to tensor memory -- into
 //       a 4-slot ring inside the accumulator buffer they just drained, so pass A's next-but-one
 //       term reuses the buffer once pass B has consumed those stages;
@@ -71,7 +71,11 @@ constexpr int kFuWIssA = 1, kFuWIssB = kFuWIssA + kFuIssA, kFuWConvX = kFuWIssB 
               kFuWDrain = kFuWConvX + 4 * kFuXSets, kFuWEpi = kFuWDrain + 4 * kFuDSets;
 constexpr int kFuEpi = 4;        // epilogue warps (one per lane quarter, 32 columns per round)
 constexpr int kFuThreads = 32 * (kFuWEpi + kFuEpi);
-constexpr unsigned kFuZsBytes = 128u * 128u * 4u;  // the [t][l] hand-off tile
+// the [t][l] hand-off tile: rows padded to 132 floats (528 B = 33 x 16 B), so the drain's float4
+// stores (lane = row t: 8 lanes per phase land on 8 distinct 16-byte bank groups) and the Z
+// converters' loads (lane = column l, consecutive words) are both conflict-free without index math
+constexpr int kFuZsStride = 132;
+constexpr unsigned kFuZsBytes = 128u * kFuZsStride * 4u;
 
 struct FuGeom {
   int len;          // local rows of the block (axis 0)
@@ -561,7 +565,7 @@ kb_fused_tc(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ 
     FuTile t;
     RingPos sb0, sb1;  // per-buffer ring positions (scalars: a runtime-indexed array would live in local memory)
     int u = 0;
-    float4* zrow = reinterpret_cast<float4*>(zs + tt * 128);
+    float4* zrow = reinterpret_cast<float4*>(zs + tt * kFuZsStride);
     const bool me = tid == 32 * kFuWDrain;
     FuProf p6(me), p7(me), p8(me), p9(me), p13(me);
     while (walk.next(t, f)) {
@@ -593,7 +597,7 @@ kb_fused_tc(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ 
           }
 #pragma unroll
           for (int c = 0; c < 8; ++c)
-            zrow[(8 * jj + c) ^ (tt & 7)] =
+            zrow[8 * jj + c] =
                 make_float4(v[4 * c] * oscale, v[4 * c + 1] * oscale, v[4 * c + 2] * oscale, v[4 * c + 3] * oscale);
         }
         p8.stop();
@@ -616,7 +620,7 @@ kb_fused_tc(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ 
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int tr = 16 * ib + i;
-            const float z = zs[tr * 128 + (((l >> 2) ^ (tr & 7)) << 2) + (l & 3)];
+            const float z = zs[tr * kFuZsStride + l];
             hi[i] = __float_as_uint(z) & 0xffffe000u;
             lo[i] = __float_as_uint(z - __uint_as_float(hi[i]));
           }
