@@ -202,7 +202,10 @@ bool use_tc(const kb_op* op, const kb::AxisGeom& g, int min_kw) {
   const long long chunks =
       (long long)((g.len + kb::kTcTS - 1) / kb::kTcTS) * ((g.other + 127) / 128) * op->batch * op->chunk_scale;
   // wide bands with enough chunks to occupy the SMs, or any band from 32 taps once there are
-  // >= 8 chunks per SM (cfg3's 512-image batch, cfg5's 16384^2: 2x the mma.sync passes there)
+  // >= 8 chunks per SM (cfg3's 512-image batch, cfg5's 16384^2: 2x the mma.sync passes there);
+  // the sum pass from 32 taps with >= 128 chunks (cfg2 fp32: 12.8 / 17.4 us against 19.5 / 24.6
+  // on mma.sync, while its split stays faster on mma.sync)
+  if (min_kw == 128 && g.Kw >= 32 && chunks >= 128) return true;
   return (g.Kw >= min_kw && chunks >= 128) || (g.Kw >= 32 && chunks >= 8LL * sm_count());
 }
 // the brick table built from tap table `tin`, or null
@@ -619,14 +622,15 @@ int launch_b(const kb_op* op, Ctx& c, const T* z, const T* tin, const kb::AxisGe
       const char* v = std::getenv("KB_TC_SUM1");
       return v ? std::atoi(v) : -1;
     }();
-    if (btab && use_tc(op, g, 128) && persistent_ok && sum1_env != 0 && (sum1_env == 1 || g.Kw <= 64)) {
+    const long long nch1 = (long long)((g.len + kb::kT1TS - 1) / kb::kT1TS) * ((g.other + 127) / 128) * op->batch;
+    if (btab && use_tc(op, g, 128) && persistent_ok && sum1_env != 0 &&
+        (sum1_env == 1 || (g.Kw <= 64 && nch1 * op->chunk_scale >= 2LL * sm_count()))) {
       const int nbr = kb::tc_bricks(g.Kw);
       const size_t fixed = 2 * (size_t)nbr * 1024;
       const size_t avail = 226 * 1024 - 1024;
       const int nst = fixed < avail ? std::min<int>(kb::kTcRingMax, (int)((avail - fixed) / kb::kTcStageBytes)) : 0;
       const size_t smem = std::max<size_t>(1024 + (size_t)nst * kb::kTcStageBytes + fixed, 116 * 1024);
-      const long long nch = (long long)((g.len + kb::kT1TS - 1) / kb::kT1TS) * ((g.other + 127) / 128) * op->batch;
-      const int nb = (int)std::min<long long>(sm_count(), nch);
+      const int nb = (int)std::min<long long>(sm_count(), nch1);
       CUtensorMap mapt;
       if (nst >= 4 && nb * kb::kT1Epi <= (op->slots_cap ? op->slots_cap : sum_blocks(op)) &&
           make_tmap(&mapt, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, kb::kTcRB, 4, 128)) {
