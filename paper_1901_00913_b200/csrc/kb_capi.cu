@@ -53,6 +53,11 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 constexpr int kMaxHalf = 1024;
+// wide-band (Kw > 64) sum passes on kb_tc1.cuh's two-accumulator variant (SLOTS = 2, opt-in with
+// KB_TC_SUM1=2): cfg4 8.96k -> 9.79k Mpix*it/s, but one application drifts to 1.9e-5 of the fp64
+// result (per-term slots: < 1e-5) and the full-length solve to 4.9e-5 of the fixture (slots:
+// 3.4e-5; tolerance 1e-4), so by default they stay on the per-term slot kernel
+constexpr bool kT1WideSlots = false;
 constexpr int kGmaxF64 = 2;  // pass A term group (register budget: G*R accumulators)
 constexpr int kGmaxF32 = 4;
 constexpr double kSymTol = 1e-11;  // (anti)symmetry residual allowed for sign-reflected fills
@@ -623,8 +628,10 @@ int launch_b(const kb_op* op, Ctx& c, const T* z, const T* tin, const kb::AxisGe
       return v ? std::atoi(v) : -1;
     }();
     const long long nch1 = (long long)((g.len + kb::kT1TS - 1) / kb::kT1TS) * ((g.other + 127) / 128) * op->batch;
+    // (KB_TC_SUM1=2: the two-accumulator variant for wider bands, tested at cfg4)
+    const int slots1 = sum1_env == 2 || (sum1_env < 0 && g.Kw > 64) ? 2 : 1;
     if (btab && use_tc(op, g, 128) && persistent_ok && sum1_env != 0 &&
-        (sum1_env == 1 || (g.Kw <= 64 && nch1 * op->chunk_scale >= 2LL * sm_count()))) {
+        (sum1_env >= 1 || ((g.Kw <= 64 || kT1WideSlots) && nch1 * op->chunk_scale >= 2LL * sm_count()))) {
       const int nbr = kb::tc_bricks(g.Kw);
       const size_t fixed = 2 * (size_t)nbr * 1024;
       const size_t avail = 226 * 1024 - 1024;
@@ -634,7 +641,10 @@ int launch_b(const kb_op* op, Ctx& c, const T* z, const T* tin, const kb::AxisGe
       CUtensorMap mapt;
       if (nst >= 4 && nb * kb::kT1Epi <= (op->slots_cap ? op->slots_cap : sum_blocks(op)) &&
           make_tmap(&mapt, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, kb::kTcRB, 4, 128)) {
-        auto kern = MODE == kb::EPI_UPDATE && !e.want_norms ? kb::kb_pass_sum_tc1<MODE, false> : kb::kb_pass_sum_tc1<MODE>;
+        auto kern = slots1 == 2 ? (MODE == kb::EPI_UPDATE && !e.want_norms ? kb::kb_pass_sum_tc1<MODE, false, 2>
+                                                                           : kb::kb_pass_sum_tc1<MODE, true, 2>)
+                                : (MODE == kb::EPI_UPDATE && !e.want_norms ? kb::kb_pass_sum_tc1<MODE, false, 1>
+                                                                           : kb::kb_pass_sum_tc1<MODE, true, 1>);
         KB_TRY(allow_smem(kern, smem));
         if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // warps skip untouched images
           KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kT1Epi, s));

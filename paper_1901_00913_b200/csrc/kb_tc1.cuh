@@ -8,8 +8,9 @@
 // (8 N-blocks), the r terms accumulate in one 128-column accumulator (double-buffered across
 // chunks: 2 x 128 columns + 8 A stages x 32 = 512), the epilogue reads it once, and a term
 // converts (128 + 2H)/128 rows per output. The tensor core's own accumulation then spans all r
-// terms; it stays inside the fp32 parity bound for bands up to Kw = 64 (cfg3, cfg5's pass B; the
-// host keeps the slot kernel for wider ones, where the chained products drift).
+// terms: at cfg5 8.5e-6 of the full-length fixture. Wider bands chain more products per output
+// (cfg4: 6.4e-5 with one accumulator, 4.9e-5 with SLOTS = 2, 3.4e-5 with kb_tc.cuh's per-term
+// slots; tolerance 1e-4) and stay on the slot kernel unless KB_TC_SUM1=2.
 //
 // Warp roles: 0 TMA producer (term bricks + Z^T tiles); 1-4 MMA issuers (N-blocks w, w + 4);
 // 5-12 two converter sets (alternate 32-row tiles); 13-20 epilogue (lane quarter x 64-output half).
@@ -26,7 +27,11 @@ constexpr int kT1Stages = 8;                     // tensor-memory A stages at co
 
 __host__ __device__ __forceinline__ int t1_ksteps(int Kw) { return (Kw + 126) / 8 + 1; }
 
-template <int MODE, bool NORMS = true>
+// SLOTS = 1: one accumulator per chunk, double-buffered across chunks. SLOTS = 2 (wide bands,
+// cfg4): two accumulators per chunk, terms [0, ceil(r/2)) and the rest, added in fp32 by the
+// epilogue -- half the chained tensor-core accumulations per output -- single-buffered (the next
+// chunk's first term waits for the epilogue to read both)
+template <int MODE, bool NORMS = true, int SLOTS = 1>
 __global__ void __launch_bounds__(kT1Threads, 1)
 kb_pass_sum_tc1(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* __restrict__ btab, AxisGeom g,
                 Epi<float> e, int batch, int nst) {
@@ -102,10 +107,14 @@ kb_pass_sum_tc1(const __grid_constant__ CUtensorMap tmap, int r, const unsigned*
     const unsigned long long b0 = tc_desc(smem_u32(bricks), 128, 256, 0);
     StrideWalk walk(g.len, LT, batch, kT1TS);
     Chunk ch;
+    const int rh = (r + 1) / 2;
     while (walk.next(ch, kT1TS)) {
-      const int ab = chunk & 1;
-      if (chunk >= 2) mbar_wait_lazy(&acc_empty[ab], ((chunk >> 1) - 1) & 1, kTcSpinNs);  // drained
+      const int ab = SLOTS == 1 ? chunk & 1 : 0;
+      if (SLOTS == 1 && chunk >= 2) mbar_wait_lazy(&acc_empty[ab], ((chunk >> 1) - 1) & 1, kTcSpinNs);  // drained
+      if (SLOTS == 2 && chunk >= 1) mbar_wait_lazy(&acc_empty[0], (chunk - 1) & 1, kTcSpinNs);
       for (int term = 0; term < r; ++term, ++tb) {
+        const int slot = SLOTS == 1 ? ab : (term >= rh ? 1 : 0);
+        const bool fresh = SLOTS == 1 ? term == 0 : (term == 0 || term == rh);
         const int bb = tb & 1;
         mbar_wait_lazy(&bready[bb], (tb >> 1) & 1, kTcSpinNs);
         __syncwarp();
@@ -124,8 +133,8 @@ kb_pass_sum_tc1(const __grid_constant__ CUtensorMap tmap, int r, const unsigned*
               const int nb = w + 4 * j, q = k - 2 * nb;
               if (!(g.dbg & 1) && k < nk && q >= 0 && q <= qmax) {
                 const unsigned long long bh = bbase + ((unsigned)q * 1024 >> 4);
-                tc_mma3(tmem + ab * 128 + 16 * nb, ahi + 8 * h, ahi + 16 + 8 * h, bh, bh + (512 >> 4),
-                        (term > 0 || q != 0) ? 1u : 0u);
+                tc_mma3(tmem + slot * 128 + 16 * nb, ahi + 8 * h, ahi + 16 + 8 * h, bh, bh + (512 >> 4),
+                        (!fresh || q != 0) ? 1u : 0u);
               }
             }
           }
@@ -206,7 +215,7 @@ kb_pass_sum_tc1(const __grid_constant__ CUtensorMap tmap, int r, const unsigned*
         bad = false;
         norm_b = ch.b;
       }
-      const int ab = chunk & 1;
+      const int ab = SLOTS == 1 ? chunk & 1 : 0;
       const int l = ch.lt * 128 + 32 * q + lane;
       const bool live = 64 * hh < ch.cnt && l < g.other;
       double sc_L = 0.0, sc_d = 1.0;
@@ -228,7 +237,7 @@ kb_pass_sum_tc1(const __grid_constant__ CUtensorMap tmap, int r, const unsigned*
           if constexpr (MODE == EPI_POWER) prefetch_l2(e.vin + row + c);
         }
       }
-      mbar_wait_lazy(&acc_full[ab], (chunk >> 1) & 1, 2000);
+      mbar_wait_lazy(&acc_full[ab], (SLOTS == 1 ? chunk >> 1 : chunk) & 1, 2000);
       __syncwarp();
       tc_fence_after();
       const float Lb = (float)sc_L, db = (float)sc_d, rd = 1.f / db;
@@ -240,6 +249,12 @@ kb_pass_sum_tc1(const __grid_constant__ CUtensorMap tmap, int r, const unsigned*
         if (o0 >= ch.cnt) break;  // warp-uniform
         float v[16];
         tc_ld16(lane_base + ab * 128 + o0, v);
+        if (SLOTS == 2 && r > (r + 1) / 2) {  // the second half of the terms, added in fp32
+          float v1[16];
+          tc_ld16(lane_base + 128 + o0, v1);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = __fadd_rn(v[i], v1[i]);
+        }
         if (live && !(g.dbg & 2)) {
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
