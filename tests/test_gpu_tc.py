@@ -75,3 +75,28 @@ def test_default_policy_takes_tcgen05_for_wide_bands():
         a = d32.apply(X.float(), adjoint=adjoint).double()
         b = d64.apply(X, adjoint=adjoint)
         assert float(torch.linalg.norm(a - b) / torch.linalg.norm(b)) <= 1e-5
+
+
+@pytest.fixture(scope="module", params=["1", "2"])
+def forced_sum1(request):
+    # the 128-output sum pass (kb_tc1.cuh) on every tcgen05 sum of tc_cases.py: one accumulator
+    # per chunk (KB_TC_SUM1=1) or two (=2) -- small images, wide bands, both BCs, and the exact
+    # adjoint fold corrections of non-symmetric reflective generators, none of which the default
+    # policy routes through it
+    env = dict(os.environ, KB_FP32_TC="1", KB_TC_SUM1=request.param)
+    out = subprocess.run([sys.executable, os.path.join(HERE, "tc_cases.py")], env=env, capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    return [json.loads(line) for line in out.stdout.splitlines() if line.startswith("{")]
+
+
+def test_single_accumulator_sum_pass_parity(forced_sum1):
+    cases = [c for c in forced_sum1 if "case" in c]
+    assert len(cases) == 9
+    for c in cases:
+        assert c["engines"] == ["tcgen05_tf32"] * 4, c
+        assert c["fwd"] <= 1e-5, c
+        assert c["adj"] <= 1e-5, c
+    for c in (c for c in forced_sum1 if "solve" in c):
+        assert c["rel"] <= 1e-4, c
+        assert c["dpsnr"] <= 0.01, c
