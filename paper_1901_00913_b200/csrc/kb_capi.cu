@@ -633,18 +633,51 @@ int launch_b(const kb_op* op, Ctx& c, const T* z, const T* tin, const kb::AxisGe
     if (btab && use_tc(op, g, 128) && persistent_ok && sum1_env != 0 &&
         (sum1_env >= 1 || ((g.Kw <= 64 || kT1WideSlots) && nch1 * op->chunk_scale >= 2LL * sm_count()))) {
       const int nbr = kb::tc_bricks(g.Kw);
-      const size_t fixed = 2 * (size_t)nbr * 1024;
+      // epilogue operands staged by TMA (kb_tc1.cuh TMAE; KB_TC1_TMAE=0 turns it off) when the
+      // planes take 128-byte-swizzled 32 x 32 boxes
+      static const int tmae_env = [] {
+        const char* v = std::getenv("KB_TC1_TMAE");
+        return v ? std::atoi(v) : 1;
+      }();
+      CUtensorMap em0, em1;
+      std::memset(&em0, 0, sizeof(em0));
+      std::memset(&em1, 0, sizeof(em1));
+      auto emap = [&](CUtensorMap* m, const float* p) {
+        return p && make_tmap(m, p, g.len, g.other, op->batch, g.len, e.bstride, 32, 4, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+      };
+      bool tmae = tmae_env != 0;
+      if (tmae) {
+        if (MODE == kb::EPI_PLAIN) tmae = emap(&em0, e.out);
+        else if (MODE == kb::EPI_RESID) tmae = emap(&em0, e.bsub) && emap(&em1, e.out);
+        else if (MODE == kb::EPI_UPDATE) tmae = emap(&em0, e.y) && emap(&em1, e.x);
+        else tmae = emap(&em0, e.vin) && emap(&em1, e.out);
+      }
+      const size_t ebytes = tmae ? kb::t1_ebuf_bytes<MODE>() + 1024 : 0;  // + alignment of the boxes
+      const size_t fixed = 2 * (size_t)nbr * 1024 + ebytes;
       const size_t avail = 226 * 1024 - 1024;
-      const int nst = fixed < avail ? std::min<int>(kb::kTcRingMax, (int)((avail - fixed) / kb::kTcStageBytes)) : 0;
+      static const int nst_cap = [] {  // debugging: ring depth cap (KB_TC1_NST)
+        const char* v = std::getenv("KB_TC1_NST");
+        return v ? std::max(4, std::atoi(v)) : kb::kTcRingMax;
+      }();
+      // an even ring depth: with 5 stages the update kernel faulted ("unspecified launch failure",
+      // legacy and TMA epilogues alike, while 4, 6 and 8 run clean); not root-caused
+      const int nst = (fixed < avail ? std::min<int>(std::min(nst_cap, kb::kTcRingMax), (int)((avail - fixed) / kb::kTcStageBytes)) : 0) & ~1;
       const size_t smem = std::max<size_t>(1024 + (size_t)nst * kb::kTcStageBytes + fixed, 116 * 1024);
       const int nb = (int)std::min<long long>(sm_count(), nch1);
       CUtensorMap mapt;
       if (nst >= 4 && nb * kb::kT1Epi <= (op->slots_cap ? op->slots_cap : sum_blocks(op)) &&
           make_tmap(&mapt, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, kb::kTcRB, 4, 128)) {
-        auto kern = slots1 == 2 ? (MODE == kb::EPI_UPDATE && !e.want_norms ? kb::kb_pass_sum_tc1<MODE, false, 2>
-                                                                           : kb::kb_pass_sum_tc1<MODE, true, 2>)
-                                : (MODE == kb::EPI_UPDATE && !e.want_norms ? kb::kb_pass_sum_tc1<MODE, false, 1>
-                                                                           : kb::kb_pass_sum_tc1<MODE, true, 1>);
+        const bool nrm = !(MODE == kb::EPI_UPDATE && !e.want_norms);
+        auto pick = [&](auto k11, auto k21, auto k12, auto k22, auto t11, auto t21, auto t12, auto t22) {
+          using K = decltype(k11);
+          K k = tmae ? (slots1 == 2 ? (nrm ? t12 : t22) : (nrm ? t11 : t21))
+                     : (slots1 == 2 ? (nrm ? k12 : k22) : (nrm ? k11 : k21));
+          return k;
+        };
+        auto kern = pick(kb::kb_pass_sum_tc1<MODE, true, 1, false>, kb::kb_pass_sum_tc1<MODE, false, 1, false>,
+                         kb::kb_pass_sum_tc1<MODE, true, 2, false>, kb::kb_pass_sum_tc1<MODE, false, 2, false>,
+                         kb::kb_pass_sum_tc1<MODE, true, 1, true>, kb::kb_pass_sum_tc1<MODE, false, 1, true>,
+                         kb::kb_pass_sum_tc1<MODE, true, 2, true>, kb::kb_pass_sum_tc1<MODE, false, 2, true>);
         KB_TRY(allow_smem(kern, smem));
         if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // warps skip untouched images
           KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kT1Epi, s));
@@ -660,7 +693,11 @@ int launch_b(const kb_op* op, Ctx& c, const T* z, const T* tin, const kb::AxisGe
         cfg.attrs = at;
         cfg.numAttrs = use_pdl() ? 1 : 0;
         c.engine = KB_ENGINE_TC_TF32;
-        KB_CUDA(cudaLaunchKernelEx(&cfg, kern, mapt, op->r, btab, g, e, op->batch, nst));
+        static const bool trace1 = std::getenv("KB_TC1_TRACE") != nullptr;
+        if (trace1)
+          std::fprintf(stderr, "[tc1] mode %d len %d other %d batch %d r %d Kw %d H %d nbr %d nst %d smem %zu tmae %d slots %d grid %d\n",
+                       MODE, g.len, g.other, op->batch, op->r, g.Kw, g.H, nbr, nst, smem, (int)tmae, slots1, nb);
+        KB_CUDA(cudaLaunchKernelEx(&cfg, kern, mapt, op->r, btab, g, e, op->batch, nst, em0, em1));
         return KB_OK;
       }
     }
