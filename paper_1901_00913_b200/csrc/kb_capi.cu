@@ -704,9 +704,27 @@ int launch_b(const kb_op* op, Ctx& c, const T* z, const T* tin, const kb::AxisGe
     if (btab && use_tc(op, g, 128) && persistent_ok) {
       // tcgen05 sum pass (kb_tc.cuh): double-buffered bricks from the brick table, tile ring
       const int nbr = kb::tc_bricks(g.Kw);
-      const size_t fixed = 2 * (size_t)nbr * 1024;
+      // epilogue operands staged by TMA (KB_TC1_TMAE=0 turns it off here too)
+      static const int tmae_env = [] {
+        const char* v = std::getenv("KB_TC1_TMAE");
+        return v ? std::atoi(v) : 1;
+      }();
+      CUtensorMap em0, em1;
+      std::memset(&em0, 0, sizeof(em0));
+      std::memset(&em1, 0, sizeof(em1));
+      auto emap = [&](CUtensorMap* m, const float* p) {
+        return p && make_tmap(m, p, g.len, g.other, op->batch, g.len, e.bstride, 32, 4, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+      };
+      bool tmae = tmae_env != 0;
+      if (tmae) {
+        if (MODE == kb::EPI_PLAIN) tmae = emap(&em0, e.out);
+        else if (MODE == kb::EPI_RESID) tmae = emap(&em0, e.bsub) && emap(&em1, e.out);
+        else if (MODE == kb::EPI_UPDATE) tmae = emap(&em0, e.y) && emap(&em1, e.x);
+        else tmae = emap(&em0, e.vin) && emap(&em1, e.out);
+      }
+      const size_t fixed = 2 * (size_t)nbr * 1024 + (tmae ? kb::tc_ebuf_bytes<MODE>() + 1024 : 0);
       const size_t avail = 226 * 1024 - 1024;
-      const int nst = fixed < avail ? std::min<int>(kb::kTcRingMax, (int)((avail - fixed) / kb::kTcStageBytes)) : 0;
+      const int nst = (fixed < avail ? std::min<int>(kb::kTcRingMax, (int)((avail - fixed) / kb::kTcStageBytes)) : 0) & ~1;
       const size_t smem = std::max<size_t>(1024 + (size_t)nst * kb::kTcStageBytes + fixed, 116 * 1024);
       // chunks are dealt round-robin over one block per SM (kb::StrideWalk)
       const long long nch = (long long)((g.len + kb::kTcTS - 1) / kb::kTcTS) * ((g.other + 127) / 128) * op->batch;
@@ -714,7 +732,9 @@ int launch_b(const kb_op* op, Ctx& c, const T* z, const T* tin, const kb::AxisGe
       CUtensorMap mapt;
       if (nst >= 4 && nb * kb::kTcSumEpi <= (op->slots_cap ? op->slots_cap : sum_blocks(op)) &&
           make_tmap(&mapt, zmap, g.other, zrows, (long long)op->batch * op->r, g.other, z_ps, kb::kTcRB, 4, 128)) {
-        auto kern = MODE == kb::EPI_UPDATE && !e.want_norms ? kb::kb_pass_sum_tc<MODE, false> : kb::kb_pass_sum_tc<MODE>;
+        const bool nrm = !(MODE == kb::EPI_UPDATE && !e.want_norms);
+        auto kern = tmae ? (nrm ? kb::kb_pass_sum_tc<MODE, true, true> : kb::kb_pass_sum_tc<MODE, false, true>)
+                         : (nrm ? kb::kb_pass_sum_tc<MODE, true, false> : kb::kb_pass_sum_tc<MODE, false, false>);
         KB_TRY(allow_smem(kern, smem));
         if (op->batch > 1 && (MODE == kb::EPI_POWER || e.want_norms))  // warps skip untouched images
           KB_CUDA(cudaMemsetAsync(e.partials, 0, sizeof(double) * 4 * (size_t)op->batch * nb * kb::kTcSumEpi, s));
@@ -730,7 +750,7 @@ int launch_b(const kb_op* op, Ctx& c, const T* z, const T* tin, const kb::AxisGe
         cfg.attrs = at;
         cfg.numAttrs = use_pdl() ? 1 : 0;
         c.engine = KB_ENGINE_TC_TF32;
-        KB_CUDA(cudaLaunchKernelEx(&cfg, kern, mapt, op->r, btab, g, e, op->batch, nst));
+        KB_CUDA(cudaLaunchKernelEx(&cfg, kern, mapt, op->r, btab, g, e, op->batch, nst, em0, em1));
         return KB_OK;
       }
     }

@@ -762,13 +762,18 @@ __device__ __forceinline__ void tc_sum_epi8(const float (&v)[8], const Epi<float
   }
 }
 
-template <int MODE, bool NORMS = true>  // NORMS = false: update without the history norms
+// TMAE: the epilogue operands staged by TMA (one 32 x 32 128-byte-swizzled box per epilogue warp
+// and operand plane, loaded during the chunk's terms, results stored by TMA; see kb_tc1.cuh)
+template <int MODE>
+__host__ __device__ constexpr unsigned tc_ebuf_bytes() { return kTcSumEpi * (MODE == EPI_UPDATE ? 2 : 1) * 4096u; }
+template <int MODE, bool NORMS = true, bool TMAE = false>  // NORMS = false: update without the history norms
 __global__ void __launch_bounds__(kTcSumThreads, 1)
 kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* __restrict__ btab, AxisGeom g,
-               Epi<float> e, int batch, int nst) {
+               Epi<float> e, int batch, int nst, const __grid_constant__ CUtensorMap emap0,
+               const __grid_constant__ CUtensorMap emap1) {
   extern __shared__ __align__(16) unsigned char kb_smem_tc[];
   __shared__ unsigned long long full[kTcRingMax], sfree[kTcRingMax], a_ready[kTcStagesMax],
-      a_free[kTcStagesMax], slot_full[kTcSumSlots], slot_empty[kTcSumSlots], bready[2], bfree[2];
+      a_free[kTcStagesMax], slot_full[kTcSumSlots], slot_empty[kTcSumSlots], bready[2], bfree[2], eful[kTcSumEpi];
   __shared__ unsigned tmem_base;
   unsigned char* base = kb_smem_tc + ((1024 - (smem_u32(kb_smem_tc) & 1023)) & 1023);
   const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
@@ -777,6 +782,7 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
   const int nas = kTcStagesMax, acol = 64 * kTcSumSlots;  // term slots at 64 j, A stages above
   float* stages = reinterpret_cast<float*>(base);  // [nst][32][128]
   unsigned* bricks = reinterpret_cast<unsigned*>(base + nst * kTcStageBytes);  // [2][nbr][256]
+  unsigned char* ebuf = base + (((size_t)nst * kTcStageBytes + 2 * (size_t)nbr * 1024 + 1023) & ~(size_t)1023);
 
   if (tid == 0) {
     for (int st = 0; st < nst; ++st) {
@@ -795,6 +801,7 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
       mbar_init(&bready[b], 1);
       mbar_init(&bfree[b], kTcIssuers);
     }
+    for (int w = 0; w < kTcSumEpi; ++w) mbar_init(&eful[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -951,7 +958,7 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
     p3.put(3, 1);
     p6.put(6, 1);
     p7.put(7, 1);
-  } else {
+  } else if (!TMAE) {
     // ---------------- epilogue: term slots -> fp32 sums -> fused update of the output rows ----------------
     const int ew = warp - kTcSumEpiW, q = warp & 3, hh = ew >> 2;  // lane quarter, 32-output half
     const unsigned lane_base = tmem + ((unsigned)(32 * q) << 16);
@@ -1038,6 +1045,162 @@ kb_pass_sum_tc(const __grid_constant__ CUtensorMap tmap, int r, const unsigned* 
         }
       }
     }
+    if (norm_b >= 0) kb_warp_finish_f<MODE>(e, nrm, bad, norm_b, nslots, slot, lane);
+  } else {
+    // ---------------- epilogue with TMA-staged operands: term slots -> fp32 sums -> boxes ----------------
+    constexpr int NPL = MODE == EPI_UPDATE ? 2 : 1;
+    const int ew = warp - kTcSumEpiW, q = warp & 3, hh = ew >> 2;  // lane quarter, 32-output half
+    const unsigned lane_base = tmem + ((unsigned)(32 * q) << 16);
+    const int nslots = gridDim.x * kTcSumEpi, slot = blockIdx.x * kTcSumEpi + ew;
+    const int n = g.len;
+    unsigned char* mybox = ebuf + (size_t)ew * NPL * 4096;
+    const CUtensorMap* pm0 = &emap0;  // parameter-space addresses (see kb_tc1.cuh)
+    const CUtensorMap* pm1 = &emap1;
+    double nrm[3] = {0.0, 0.0, 0.0};
+    bool bad = false;
+    int norm_b = -1, chunk = 0;
+    RingPos sl;
+    StrideWalk walk(g.len, LT, batch, kTcTS);
+    auto load_boxes = [&](const Chunk& c2) {
+      if (MODE == EPI_PLAIN) return;
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&eful[ew], NPL * 4096);
+        const int c0 = c2.s0 + 32 * hh, r0 = c2.lt * 128 + 32 * q;
+        tma_load_3d(mybox, pm0, c0, r0, c2.b, &eful[ew]);
+        if (NPL == 2) tma_load_3d(mybox + 4096, pm1, c0, r0, c2.b, &eful[ew]);
+      }
+    };
+    {
+      StrideWalk peek = walk;
+      Chunk c2;
+      if (peek.next(c2, kTcTS)) load_boxes(c2);
+    }
+    Chunk ch;
+    while (walk.next(ch, kTcTS)) {
+      if (ch.b != norm_b) {
+        if (norm_b >= 0) kb_warp_finish_f<MODE>(e, nrm, bad, norm_b, nslots, slot, lane);
+        nrm[0] = nrm[1] = nrm[2] = 0.0;
+        bad = false;
+        norm_b = ch.b;
+      }
+      const bool live = 32 * hh < ch.cnt;
+      double sc_L = 0.0, sc_d = 1.0;
+      if constexpr (MODE == EPI_UPDATE) {
+        sc_L = e.L[ch.b];
+        sc_d = e.denom[ch.b];
+      }
+      if constexpr (MODE == EPI_POWER) sc_L = e.vnw2 ? e.vnw2[ch.b] : 1.0;
+      float sum[32];
+      for (int term = 0; term < r; ++term, sl.advance(kTcSumSlots)) {
+        mbar_wait_idle(&slot_full[sl.i], sl.phase, 2000);
+        __syncwarp();
+        tc_fence_after();
+        if (live) {
+          const unsigned col = lane_base + sl.i * 64 + 32 * hh;
+          float v[16];
+#pragma unroll
+          for (int p2 = 0; p2 < 2; ++p2) {
+            tc_ld16(col + 16 * p2, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) sum[16 * p2 + i] = term ? __fadd_rn(sum[16 * p2 + i], v[i]) : v[i];
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&slot_empty[sl.i]);
+      }
+      const int l = ch.lt * 128 + 32 * q + lane;
+      const bool row_ok = l < g.other;
+      if (MODE != EPI_PLAIN) mbar_wait_lazy(&eful[ew], chunk & 1, 2000);
+      if (live && !(g.dbg & 2)) {
+        const float Lb = (float)sc_L, db = (float)sc_d, rd = 1.f / db;
+        const double vs = MODE == EPI_POWER && e.vnw2 ? sqrt(sc_L) : 1.0;
+        const float beta = (float)e.beta;
+        const bool fold_edge = e.foldH > 0 && (ch.s0 < e.foldH || ch.s0 + kTcTS > n - e.foldH);
+        if (fold_edge && row_ok) {  // exact adjoint fold corrections of the reflective axis (edge chunks)
+          const int FH = e.foldH;
+          const float* fz = e.fold + ((long long)ch.b * g.other + l) * (2 * FH);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int qi = ch.s0 + 32 * hh + i;
+            if (qi < FH) sum[i] += fz[qi];
+            else if (qi >= n - FH && qi < n) sum[i] += fz[qi - (n - 2 * FH)];
+          }
+        }
+#pragma unroll
+        for (int c16 = 0; c16 < 8; ++c16) {
+          const unsigned off = (unsigned)lane * 128 + (unsigned)((c16 ^ (lane & 7)) * 16);
+          float4* p0 = reinterpret_cast<float4*>(mybox + off);
+          const float* vv = sum + 4 * c16;
+          const int col0 = 32 * hh + 4 * c16;
+          float4 a0 = *p0;
+          float* u = reinterpret_cast<float*>(&a0);
+          if constexpr (MODE == EPI_PLAIN) {
+            *p0 = make_float4(vv[0], vv[1], vv[2], vv[3]);
+          } else if constexpr (MODE == EPI_RESID) {
+            *p0 = make_float4(__fsub_rn(vv[0], u[0]), __fsub_rn(vv[1], u[1]), __fsub_rn(vv[2], u[2]),
+                              __fsub_rn(vv[3], u[3]));
+          } else if constexpr (MODE == EPI_UPDATE) {
+            float4* p1 = reinterpret_cast<float4*>(mybox + 4096 + off);
+            float4 a1 = *p1;
+            float* w = reinterpret_cast<float*>(&a1);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float a = __fsub_rn(__fmul_rn(Lb, u[i]), vv[i]);
+              const float q0 = __fmul_rn(a, rd);
+              float x = fmaf(fmaf(-db, q0, a), rd, q0);
+              if (e.project) x = (x > 0.f || x != x) ? x : 0.f;
+              const float d = __fsub_rn(x, w[i]);
+              if (row_ok && col0 + i < ch.cnt) {
+                bad |= !isfinite(x);
+                if (NORMS && e.want_norms) {
+                  nrm[0] += (double)d * d;
+                  nrm[1] += (double)w[i] * w[i];
+                  nrm[2] += (double)x * x;
+                }
+              }
+              u[i] = __fadd_rn(x, __fmul_rn(beta, d));
+              w[i] = x;
+            }
+            *p0 = a0;
+            *p1 = a1;
+          } else {  // EPI_POWER
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              if (row_ok && col0 + i < ch.cnt) {
+                const double vvv = e.vnw2 ? (double)u[i] / vs : (double)u[i];
+                nrm[0] += vvv * vv[i];
+                nrm[1] += (double)vv[i] * vv[i];
+              }
+            }
+            *p0 = make_float4(vv[0], vv[1], vv[2], vv[3]);
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0 && live && !(g.dbg & 2)) {
+        const int c0 = ch.s0 + 32 * hh, r0 = ch.lt * 128 + 32 * q;
+        if constexpr (MODE == EPI_UPDATE) {
+          tma_store_3d(pm0, mybox, c0, r0, ch.b);
+          tma_store_3d(pm1, mybox + 4096, c0, r0, ch.b);
+        } else if constexpr (MODE == EPI_PLAIN) {
+          tma_store_3d(pm0, mybox, c0, r0, ch.b);
+        } else {
+          tma_store_3d(pm1, mybox, c0, r0, ch.b);
+        }
+        bulk_commit();
+      }
+      if (lane == 0) bulk_wait_read<0>();  // the box may be refilled
+      __syncwarp();
+      {
+        StrideWalk peek = walk;
+        Chunk c2;
+        if (peek.next(c2, kTcTS)) load_boxes(c2);
+      }
+      ++chunk;
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
     if (norm_b >= 0) kb_warp_finish_f<MODE>(e, nrm, bad, norm_b, nslots, slot, lane);
   }
   tc_fence_before();
