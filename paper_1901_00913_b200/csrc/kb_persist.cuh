@@ -81,18 +81,19 @@ __global__ void __launch_bounds__(kPsThreads) kb_solve_persistent(PsArgs a) {
   // is not coherent across SMs); out-of-domain rows reflected (refl) or zero
   auto stage = [&](const double* src, int refl) {
     const int rows = nr + 2 * Ha, half = n >> 1;
-    for (int t = 0; t < rows; ++t) {
+    // one flat loop over (row, column pair): every thread busy (a row-by-row loop left half the
+    // threads idle at n = 256 and doubled the staging iterations: 3.65k -> 3.05k Mpix*it/s)
+    for (int idx = tid; idx < rows * half; idx += kPsThreads) {
+      const int t = idx / half, c = 2 * (idx - t * half);
       const int g = ps_src(r0 - Ha + t, m, refl);
-      for (int h2 = tid; h2 < half; h2 += kPsThreads) {
-        double* dst = Ys + (size_t)t * n + 2 * h2;
-        if (g >= 0) {
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)),
-                       "l"(src + (size_t)g * n + 2 * h2)
-                       : "memory");
-        } else {
-          dst[0] = 0.0;
-          dst[1] = 0.0;
-        }
+      double* dst = Ys + (size_t)t * n + c;
+      if (g >= 0) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)),
+                     "l"(src + (size_t)g * n + c)
+                     : "memory");
+      } else {
+        dst[0] = 0.0;
+        dst[1] = 0.0;
       }
     }
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
