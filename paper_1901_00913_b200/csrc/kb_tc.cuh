@@ -297,6 +297,14 @@ struct PairWalk {
   }
 };
 
+// the split pass' barrier waits: plain polling, or (KB_TC_SPLIT_LAZY=1 at build time) try_wait
+// with a suspend-time hint so waiting warps leave their issue slots (and power) to the others
+// (A/B at cfg5: 21.13k either way, the clock stays at the 1.5 GHz power cap)
+#ifndef KB_TC_SPLIT_LAZY
+#define KB_TC_SPLIT_LAZY 0
+#endif
+#define KB_TCS_WAIT(bar, par) \
+  (KB_TC_SPLIT_LAZY ? mbar_wait_lazy((bar), (par), kTcSpinNs) : mbar_wait((bar), (par)))
 template <int EPI>
 __global__ void __launch_bounds__(tc_split_threads(EPI), 1)
 kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap zmap,
@@ -393,7 +401,7 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
       {
         const int ab = chunk & 1;
         pe.start();
-        if (chunk >= 2) mbar_wait(&acc_empty[ab], ((chunk >> 1) - 1) & 1);  // epilogue drained this set
+        if (chunk >= 2) KB_TCS_WAIT(&acc_empty[ab], ((chunk >> 1) - 1) & 1);  // epilogue drained this set
         __syncwarp();
         pe.stop();
         tc_fence_after();
@@ -401,7 +409,7 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
         for (int ia = 0; ia < na; ++ia, a.advance(nas)) {
           const int st = a.i;
           pa.start();
-          mbar_wait(&a_ready[st], a.phase);  // A stage (and, at a group change, bricks) ready
+          KB_TCS_WAIT(&a_ready[st], a.phase);  // A stage (and, at a group change, bricks) ready
           __syncwarp();  // reconverge: elect.sync below must see the whole warp
           pa.stop();
           if (!(g.dbg & 8)) tc_fence_after();
@@ -455,13 +463,13 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
           // once the previous chunk's MMAs (the last readers of the old bricks) completed
           pb.start();
           if (wt == 0) {
-            if (chunk > 0) mbar_wait(&acc_full[(chunk - 1) & 1], ((chunk - 1) >> 1) & 1);
+            if (chunk > 0) KB_TCS_WAIT(&acc_full[(chunk - 1) & 1], ((chunk - 1) >> 1) & 1);
             const int t0 = chunk_major ? 0 : g0, tn = chunk_major ? r : gc;
             const unsigned bytes = (unsigned)(tn * nbr) * 1024;
             mbar_arrive_expect_tx(&bready, bytes);
             bulk_g2s(bricks, btab + ((long long)ch.b * r + t0) * nbr * 256, bytes, &bready);
           }
-          mbar_wait(&bready, nbl & 1);  // before any A stage of this chunk is announced
+          KB_TCS_WAIT(&bready, nbl & 1);  // before any A stage of this chunk is announced
           ++nbl;
           bricks_key = key;
           pb.stop();
@@ -474,7 +482,7 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
             continue;
           }
           p2.start();
-          mbar_wait(&full[t.i], t.phase);
+          KB_TCS_WAIT(&full[t.i], t.phase);
           p2.stop();
           tc_fence_after();
           const float* tile = stages + t.i * (kTcStageBytes / 4) + 32 * q + lane;
@@ -486,7 +494,7 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
             if (h == nat) break;
             if (h == 1) st1 = a.i;
             p1.start();
-            mbar_wait(&a_free[a.i], a.phase ^ 1);
+            KB_TCS_WAIT(&a_free[a.i], a.phase ^ 1);
             p1.stop();
             pc.start();
             if (!(g.dbg & 4)) {
@@ -542,7 +550,7 @@ kb_pass_split_tc(const __grid_constant__ CUtensorMap tmap, const __grid_constant
       {
         const int ab = chunk & 1;
         p3.start();
-        mbar_wait(&acc_full[ab], (chunk >> 1) & 1);
+        KB_TCS_WAIT(&acc_full[ab], (chunk >> 1) & 1);
         p3.stop();
         p4.start();
         tc_fence_after();
