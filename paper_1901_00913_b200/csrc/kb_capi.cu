@@ -29,6 +29,7 @@
 #include "kb_blur.cuh"
 #include "kb_norms.cuh"
 #include "kb_persist.cuh"
+#include "kb_persist2.cuh"
 
 namespace {
 
@@ -106,6 +107,9 @@ struct kb_op {
   // wider band first is faster (kb_op_create: axis_swap_wanted); the fast sFISTA path then
   // solves the transposed problem Y^T = sum_i K_i X^T H_i^T in the same workspace
   kb_op* twin = nullptr;
+  // fp64: host copies of the four tap tables ([batch][r][Wp], axis a then b) for the launch
+  // parameters of the zero-BC whole-solve kernel (kb_persist2.cuh)
+  std::vector<double> h_conv[2], h_corr[2];
   // engines of the latest kb_time_passes phases (reporting only; written under g_phase_mu)
   mutable int phase_engine[4] = {0, 0, 0, 0};
 };
@@ -1309,9 +1313,14 @@ void build_tables(int dlo, int w, const double* taps, int batch, int r, const st
 
 template <typename T>
 int upload_tables(kb_op* op, int dlo, int w, const double* taps, const std::vector<int>& perm, int H,
-                  int Wp, void** conv_d, void** corr_d) {
+                  int Wp, void** conv_d, void** corr_d, std::vector<double>* keep_conv = nullptr,
+                  std::vector<double>* keep_corr = nullptr) {
   std::vector<T> conv, corr;
   build_tables<T>(dlo, w, taps, op->batch, op->r, perm, H, Wp, conv, corr);
+  if constexpr (sizeof(T) == 8) {
+    if (keep_conv) *keep_conv = conv;
+    if (keep_corr) *keep_corr = corr;
+  }
   const size_t bytes = conv.size() * sizeof(T);
   KB_CUDA(cudaMalloc(conv_d, bytes));
   KB_CUDA(cudaMalloc(corr_d, bytes));
@@ -1659,8 +1668,11 @@ int kb_op_create(kb_op** out, int dtype, int m, int n, int r, int batch, int bc_
 
   int rc;
   if (dtype == KB_F64) {
-    rc = upload_tables<double>(op, a_dlo, a_w, a_taps, perm, Ha, op->Wpa, &op->ta_conv, &op->ta_corr);
-    if (rc == KB_OK) rc = upload_tables<double>(op, b_dlo, b_w, b_taps, perm, Hb, op->Wpb, &op->tb_conv, &op->tb_corr);
+    rc = upload_tables<double>(op, a_dlo, a_w, a_taps, perm, Ha, op->Wpa, &op->ta_conv, &op->ta_corr,
+                               &op->h_conv[0], &op->h_corr[0]);
+    if (rc == KB_OK)
+      rc = upload_tables<double>(op, b_dlo, b_w, b_taps, perm, Hb, op->Wpb, &op->tb_conv, &op->tb_corr,
+                                 &op->h_conv[1], &op->h_corr[1]);
     if (rc == KB_OK && ok_b) rc = upload_signs<double>(op, sign_b);
   } else {
     rc = upload_tables<float>(op, a_dlo, a_w, a_taps, perm, Ha, op->Wpa, &op->ta_conv, &op->ta_corr);
@@ -1814,7 +1826,52 @@ namespace {
 struct PsPlan {
   int RB = 0, nblk = 0;
   size_t smem = 0;
+  int v2 = 0;  // kb_solve_persistent2 (zero BC, narrow bands) instead of kb_solve_persistent
 };
+
+using Ps2Kernel = void (*)(kb::P2Args);
+template <int R>
+Ps2Kernel ps2_kernel_r(int RB) {
+  return RB == 1 ? kb::kb_solve_persistent2<R, 1> : kb::kb_solve_persistent2<R, 2>;
+}
+Ps2Kernel ps2_kernel(int r, int RB) {
+  switch (r) {
+    case 1: return ps2_kernel_r<1>(RB);
+    case 2: return ps2_kernel_r<2>(RB);
+    case 3: return ps2_kernel_r<3>(RB);
+    default: return ps2_kernel_r<4>(RB);
+  }
+}
+// The second whole-solve form (kb_persist2.cuh): zero BC on both axes, half widths <= 15,
+// r <= 4, n a multiple of 64 up to 512. KB_PERSIST2=0 keeps the first form; KB_PERSIST_RB picks
+// the rows per CTA (1 or 2).
+PsPlan persist2_plan(const kb_op* op) {
+  PsPlan p;
+  const char* v = std::getenv("KB_PERSIST2");
+  if (v && v[0] == '0') return p;
+  if (op->bc_a != KB_BC_ZERO || op->bc_b != KB_BC_ZERO || op->Ha > kb::kP2H || op->Hb > kb::kP2H ||
+      op->r > kb::kP2MaxR || op->n % 64 || op->n > 512 || op->h_conv[0].empty() || op->h_conv[1].empty())
+    return p;
+  const char* rbv = std::getenv("KB_PERSIST_RB");
+  const int want = rbv ? std::atoi(rbv) : 0;
+  const int sms = sm_count();
+  for (int RB = want == 1 || want == 2 ? want : 2; RB >= 1; --RB) {
+    const Ps2Kernel k = ps2_kernel(op->r, RB);
+    const size_t smem = kb::p2_smem_bytes(RB, op->n, op->r);
+    int per_sm = 0;
+    if (smem <= 200 * 1024 && allow_smem(k, smem) == KB_OK &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kb::kP2Threads, smem) == cudaSuccess &&
+        per_sm >= 1 && (op->m + RB - 1) / RB <= per_sm * sms) {
+      p.RB = RB;
+      p.nblk = (op->m + RB - 1) / RB;
+      p.smem = smem;
+      p.v2 = 1;
+      return p;
+    }
+    if (want == 1 || want == 2) break;
+  }
+  return p;
+}
 PsPlan persist_plan(const kb_op* op) {
   PsPlan p;
   static const int mode = [] {
@@ -1823,6 +1880,10 @@ PsPlan persist_plan(const kb_op* op) {
   }();
   if (mode == 0 || op->dtype != KB_F64 || op->batch != 1 || op->n % 2) return p;
   if (mode < 0 && (long long)op->m * op->n > 512LL * 512) return p;
+  {
+    const PsPlan p2 = persist2_plan(op);
+    if (p2.v2) return p2;
+  }
   const int sms = sm_count();
   static const int rb_env = [] {
     const char* v = std::getenv("KB_PERSIST_RB");
@@ -1873,6 +1934,44 @@ int launch_persist(const kb_op* op, const PsPlan& pp, const double* B, double* X
   const int cap = (int)(4 * (size_t)op->batch * sum_blocks(op)) - (pp.nblk + 1) / 2 - 2;
   if (cap < 1) return fail(KB_ERR_ARGUMENT, "workspace too small for the persistent solve");
   int* flags = reinterpret_cast<int*>(w.partials + cap + 1);
+  if (pp.v2) {
+    kb::P2Args a{};
+    a.B = B;
+    a.X = X;
+    a.Y = Y;
+    a.R = static_cast<double*>(w.rp);
+    a.beta = w.partials;
+    a.nonfinite = nonfinite;
+    a.L = L;
+    a.denom = L + lam * lam;
+    a.m = op->m;
+    a.n = op->n;
+    a.project = project;
+    // centred 31-tap windows: window tap k' <-> table tap k' - 15 + H
+    auto centre = [&](const std::vector<double>& tab, int H, int Wp, double (*dst)[kb::kP2W]) {
+      for (int i = 0; i < op->r; ++i)
+        for (int k = 0; k < kb::kP2W; ++k) {
+          const int t = k - kb::kP2H + H;
+          dst[i][k] = (t >= 0 && t <= 2 * H) ? tab[(size_t)i * Wp + t] : 0.0;
+        }
+    };
+    centre(op->h_conv[0], op->Ha, op->Wpa, a.fa);
+    centre(op->h_corr[0], op->Ha, op->Wpa, a.aa);
+    centre(op->h_conv[1], op->Hb, op->Wpb, a.fb);
+    centre(op->h_corr[1], op->Hb, op->Wpb, a.ab);
+    const Ps2Kernel kern = ps2_kernel(op->r, pp.RB);
+    for (int done = 0; done < iters;) {
+      const int cnt = std::min(iters - done, cap);
+      KB_CUDA(cudaMemcpyAsync(w.partials, beta + k0 + done, sizeof(double) * cnt, cudaMemcpyHostToDevice, s));
+      a.k0 = k0 + done;
+      a.iters = cnt;
+      void* args[] = {&a};
+      KB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(pp.nblk), dim3(kb::kP2Threads), args, pp.smem, s));
+      done += cnt;
+    }
+    for (int i = 0; i < 4; ++i) w.ctx.phase[i] = KB_ENGINE_PERSIST_F64;
+    return KB_OK;
+  }
   for (int done = 0; done < iters;) {
     const int cnt = std::min(iters - done, cap);
     KB_CUDA(cudaMemcpyAsync(w.partials, beta + k0 + done, sizeof(double) * cnt, cudaMemcpyHostToDevice, s));
