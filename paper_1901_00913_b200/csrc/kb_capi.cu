@@ -256,6 +256,11 @@ int generic_slots(const kb_op* op) {
   return ((op->n + TS - 1) / TS) * ((op->m + 31) / 32);
 }
 int sum_blocks(const kb_op* op) { return std::max(persistent_slots(op), generic_slots(op)); }
+// doubles in the partials region: the norm slots, and at least room for a whole-solve launch's
+// beta table plus one 128-byte phase flag per CTA (kb_persist2.cuh)
+size_t partials_doubles(const kb_op* op) {
+  return std::max<size_t>(4 * (size_t)op->batch * sum_blocks(op), 16384);
+}
 
 Work layout(const kb_op* op, void* base) {
   Work w;
@@ -269,7 +274,7 @@ Work layout(const kb_op* op, void* base) {
   w.fold = b ? b + off : nullptr;
   off = align_up(off + elem(op) * (size_t)op->batch * op->m * 2 * std::max(op->Hb, 1), 256);
   w.partials = b ? reinterpret_cast<double*>(b + off) : nullptr;
-  off = align_up(off + sizeof(double) * 4 * (size_t)op->batch * sum_blocks(op), 256);
+  off = align_up(off + sizeof(double) * partials_doubles(op), 256);
   w.scal = b ? reinterpret_cast<double*>(b + off) : nullptr;
   off = align_up(off + sizeof(double) * 4 * (size_t)op->batch, 256);
   w.bytes = off;
@@ -1931,7 +1936,7 @@ int launch_persist(const kb_op* op, const PsPlan& pp, const double* B, double* X
     const char* v = std::getenv("KB_PERSIST_SYNC");
     return !(v && std::string(v) == "flags");
   }();
-  const int cap = (int)(4 * (size_t)op->batch * sum_blocks(op)) - (pp.nblk + 1) / 2 - 2;
+  const int cap = (int)partials_doubles(op) - (pp.nblk + 1) / 2 - 2;
   if (cap < 1) return fail(KB_ERR_ARGUMENT, "workspace too small for the persistent solve");
   int* flags = reinterpret_cast<int*>(w.partials + cap + 1);
   if (pp.v2) {
@@ -1947,6 +1952,18 @@ int launch_persist(const kb_op* op, const PsPlan& pp, const double* B, double* X
     a.m = op->m;
     a.n = op->n;
     a.project = project;
+    // neighbour phase epochs instead of grid-wide barriers (KB_PERSIST2_SYNC=grid|flags): the
+    // flags, one 128-byte line per CTA, sit behind the beta table in the partials region
+    static const bool p2_flags = [] {
+      const char* v = std::getenv("KB_PERSIST2_SYNC");
+      return v ? std::string(v) == "flags" : false;
+    }();
+    const int fdoubles = (pp.nblk * kb::kP2FlagStride + 1) / 2 + 16;
+    const int cap2 = (int)partials_doubles(op) - fdoubles - 2;
+    const bool use_flags = p2_flags && cap2 >= 1;
+    const int capv = use_flags ? cap2 : cap;
+    if (use_flags)  // 128-byte aligned
+      a.flags = reinterpret_cast<int*>((reinterpret_cast<uintptr_t>(w.partials + capv + 1) + 127) & ~(uintptr_t)127);
     // centred 31-tap windows: window tap k' <-> table tap k' - 15 + H
     auto centre = [&](const std::vector<double>& tab, int H, int Wp, double (*dst)[kb::kP2W]) {
       for (int i = 0; i < op->r; ++i)
@@ -1960,15 +1977,35 @@ int launch_persist(const kb_op* op, const PsPlan& pp, const double* B, double* X
     centre(op->h_conv[1], op->Hb, op->Wpb, a.fb);
     centre(op->h_corr[1], op->Hb, op->Wpb, a.ab);
     const Ps2Kernel kern = ps2_kernel(op->r, pp.RB);
+#ifdef KB_P2_TRACE
+    static long long* trace_d = nullptr;
+    if (!trace_d) cudaMalloc(&trace_d, 64 * sizeof(long long));
+    cudaMemsetAsync(trace_d, 0, 64 * sizeof(long long), s);
+    a.trace = trace_d;
+#endif
     for (int done = 0; done < iters;) {
-      const int cnt = std::min(iters - done, cap);
+      const int cnt = std::min(iters - done, capv);
       KB_CUDA(cudaMemcpyAsync(w.partials, beta + k0 + done, sizeof(double) * cnt, cudaMemcpyHostToDevice, s));
+      if (a.flags) KB_CUDA(cudaMemsetAsync(a.flags, 0, sizeof(int) * pp.nblk * kb::kP2FlagStride, s));
       a.k0 = k0 + done;
       a.iters = cnt;
       void* args[] = {&a};
       KB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(pp.nblk), dim3(kb::kP2Threads), args, pp.smem, s));
       done += cnt;
     }
+#ifdef KB_P2_TRACE
+    if (std::getenv("KB_P2_TRACE")) {
+      long long h[64];
+      cudaStreamSynchronize(s);
+      cudaMemcpy(h, trace_d, sizeof(h), cudaMemcpyDeviceToHost);
+      static const char* names[] = {"p1 start", "p1 waited", "p1 staged(issued)", "p1 axis0", "p1 sync", "p1 axis1+store",
+                                    "p1 phase_end", "p2 waited", "p2 staged(issued)", "p2 axis0", "p2 sync",
+                                    "p2 axis1+update", "p2 phase_end"};
+      std::fprintf(stderr, "[p2 trace]");
+      for (int i = 1; i < 13; ++i) std::fprintf(stderr, " %s +%lld;", names[i], h[i] - h[i - 1]);
+      std::fprintf(stderr, " total %lld\n", h[12] - h[0]);
+    }
+#endif
     for (int i = 0; i < 4; ++i) w.ctx.phase[i] = KB_ENGINE_PERSIST_F64;
     return KB_OK;
   }

@@ -44,6 +44,8 @@ struct P2Args {
   double* R;
   const double* beta;  // [iters] momentum coefficients beta_{k0+1 ..}
   int* nonfinite;
+  long long* trace;  // KB_P2_TRACE builds: clock64 stamps of the middle CTA's middle iteration
+  int* flags;  // [gridDim.x] phase epochs, zeroed before the launch; nullptr = grid-wide barriers
   double L, denom;
   int m, n, k0, iters, project;
   // centred taps: forward axis 0 Z[s] = sum_k fa[i][k] Y[s - 15 + k]; aa = the adjoint's
@@ -69,6 +71,19 @@ __host__ __device__ inline size_t p2_smem_bytes(int RB, int n, int r) {
 #define KB_P2_PIECE 8
 #endif
 constexpr int kP2Piece = KB_P2_PIECE;  // staged rows per bulk copy / mbarrier (axis 0 starts on the first)
+#ifndef KB_P2_FSTRIDE
+#define KB_P2_FSTRIDE 32
+#endif
+#ifndef KB_P2_POLL_NS
+#define KB_P2_POLL_NS 0
+#endif
+constexpr int kP2FlagStride = KB_P2_FSTRIDE;  // ints between two CTAs' phase flags (32: a 128-byte line each)
+#ifndef KB_P2_DIRECT
+#define KB_P2_DIRECT 0  // 1: axis 0 reads its source rows from L2 straight into registers (measured slower)
+#endif
+#ifndef KB_P2_CHAINS
+#define KB_P2_CHAINS 2
+#endif
 
 __device__ __forceinline__ void p2_dmma(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -112,7 +127,7 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
   // contiguous) and one mbarrier each, so axis 0 starts on the first rows while the rest arrive;
   // pieces wholly outside the image only arrive
   auto stage = [&](const double* src) {
-    if (tid == 0) {
+    if (!KB_P2_DIRECT && tid == 0) {
       // rows written by other CTAs before the grid barrier (generic proxy) -> bulk copy (async)
       asm volatile("fence.proxy.async.global;" ::: "memory");
 #pragma unroll
@@ -135,17 +150,31 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
   };
   // axis 0 on the staged rows: Z_i[t][c] = sum_k taps[i][k] Ys[t + k][c]; every staged value
   // feeds the R x RB accumulators of its column (taps: compile-time parameter offsets)
-  auto axis0 = [&](const double (&tp)[kP2MaxR][kP2W]) {
+  auto axis0 = [&](const double (&tp)[kP2MaxR][kP2W], const double* __restrict__ src) {
     for (int c = tid; c < n; c += kP2Threads) {
       double acc[R][RB];
 #pragma unroll
       for (int i = 0; i < R; ++i)
 #pragma unroll
         for (int t = 0; t < RB; ++t) acc[i][t] = 0.0;
+#if KB_P2_DIRECT
+      // the column's RB + 30 source values straight from L2 into registers (ld.global.cg: other
+      // SMs wrote them; a warp reads 256 contiguous bytes per row), all in flight at once
+      double yv[RB + 2 * kP2H];
 #pragma unroll
       for (int k2 = 0; k2 < RB + 2 * kP2H; ++k2) {
+        const int gr = r0 - kP2H + k2;
+        yv[k2] = (gr >= 0 && gr < m) ? __ldcg(src + (size_t)gr * n + c) : 0.0;
+      }
+#endif
+#pragma unroll
+      for (int k2 = 0; k2 < RB + 2 * kP2H; ++k2) {
+#if KB_P2_DIRECT
+        const double y = yv[k2];
+#else
         if (k2 % kP2Piece == 0) mbar_wait(&bar[k2 / kP2Piece], parity);
         const double y = Ys[(size_t)k2 * n + c];
+#endif
 #pragma unroll
         for (int t = 0; t < RB; ++t) {
           const int k = k2 - t;
@@ -165,19 +194,72 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
   // warp w takes blocks w, w + 8 (<= RB per warp at n <= 512)
   const int nmb = n >> 6, nblk = nr * nmb;
   // lane's outputs in its block: column 64 mbc + 8 (lane >> 2) + 2 (lane & 3) + {0, 1}
+  // KB_P2_CHAINS independent accumulator chains per term (K-steps dealt round robin), the terms
+  // interleaved: a warp has one or two blocks per phase, so one chain of 10 r dependent DMMAs
+  // would run at the instruction's latency
   auto axis1 = [&](int mb, int adj, double (&d)[2]) {
     const int t = mb / nmb, mbc = mb - t * nmb;
+    const int j0 = 64 * mbc + 8 * (lane >> 2) + (lane & 3);
+    double acc[R][KB_P2_CHAINS][2];
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int h = 0; h < KB_P2_CHAINS; ++h) acc[i][h][0] = acc[i][h][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < kP2KS; ++s)
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+        p2_dmma(acc[i][s % KB_P2_CHAINS], Zs[((size_t)i * RB + t) * NZ + p2_zidx(j0 + 4 * s)],
+                Bf[((size_t)(adj * R + i) * kP2KS + s) * 32 + lane]);
     d[0] = d[1] = 0.0;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-      const double* zr = Zs + ((size_t)i * RB + t) * NZ;
-      const int j0 = 64 * mbc + 8 * (lane >> 2) + (lane & 3);
-      const double* bf = Bf + ((size_t)(adj * R + i) * kP2KS) * 32 + lane;
+      double t0 = acc[i][0][0], t1 = acc[i][0][1];
 #pragma unroll
-      for (int s = 0; s < kP2KS; ++s) p2_dmma(d, zr[p2_zidx(j0 + 4 * s)], bf[32 * s]);
+      for (int h = 1; h < KB_P2_CHAINS; ++h) {
+        t0 = __dadd_rn(t0, acc[i][h][0]);
+        t1 = __dadd_rn(t1, acc[i][h][1]);
+      }
+      d[0] = __dadd_rn(d[0], t0);
+      d[1] = __dadd_rn(d[1], t1);
     }
   };
   auto out_col = [&](int mb) { return 64 * (mb % nmb) + 8 * (lane >> 2) + 2 * (lane & 3); };
+
+  // Between phases a CTA needs only the rows of the CTAs within 15 rows of its own (the halo of
+  // its next axis-0 pass), so with a.flags it waits for those CTAs' phase epochs -- warp 0, one
+  // lane per neighbour, acquire loads -- instead of a grid-wide barrier; lane 0 then issues the
+  // bulk copies. The same epochs order the writes: before writing R (resp. Y) a CTA has seen its
+  // neighbours finish the phase that read the previous R (resp. Y).
+  const int b_lo = max(0, (r0 - kP2H) / RB), b_hi = min((int)gridDim.x - 1, (r0 + RB - 1 + kP2H) / RB);
+  auto wait_neighbours = [&](int epoch) {  // b_hi - b_lo < 32: one lane of warp 0 per neighbour
+    if (epoch > 0) {
+      if (warp == 0) {
+        if (b_lo + lane <= b_hi) {
+          int v;
+          do {
+            asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];"
+                         : "=r"(v)
+                         : "l"(a.flags + (size_t)(b_lo + lane) * kP2FlagStride)
+                         : "memory");
+            if (KB_P2_POLL_NS > 0 && v < epoch) __nanosleep(KB_P2_POLL_NS);
+          } while (v < epoch);
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
+        __syncwarp();
+      }
+      if (KB_P2_DIRECT) __syncthreads();  // every thread loads the neighbours' rows
+    }
+  };
+  auto phase_end = [&](int epoch) {
+    if (a.flags) {
+      __syncthreads();  // the CTA's stores happen before thread 0's release (cumulative)
+      if (tid == 0)
+        asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.flags + (size_t)blockIdx.x * kP2FlagStride), "r"(epoch) : "memory");
+    } else {
+      grid.sync();
+    }
+  };
 
   // register-resident state of the lane's outputs
   double xs[RB][2], ys[RB][2], bs[RB][2];
@@ -195,13 +277,26 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
     }
   }
 
+#ifdef KB_P2_TRACE
+  const bool tracing = a.trace && blockIdx.x == gridDim.x / 2 && tid == 0;
+  int tn = 0;
+#define P2_STAMP() do { if (tracing && it == a.iters / 2) a.trace[tn++] = clock64(); } while (0)
+#else
+#define P2_STAMP() do { } while (0)
+#endif
   for (int it = 0; it < a.iters; ++it) {
     const int k = a.k0 + it + 1;
     // ---- phase 1: R = A Y - B on this CTA's rows
     if (nr > 0) {
+      P2_STAMP();
+      if (a.flags) wait_neighbours(2 * it);
+      P2_STAMP();
       stage(a.Y);
-      axis0(a.fa);
+      P2_STAMP();
+      axis0(a.fa, a.Y);
+      P2_STAMP();
       __syncthreads();
+      P2_STAMP();
 #pragma unroll
       for (int j = 0; j < RB; ++j) {
         const int mb = warp + 8 * j;
@@ -213,12 +308,19 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
         }
       }
     }
-    grid.sync();
+    P2_STAMP();
+    phase_end(2 * it + 1);
+    P2_STAMP();
     // ---- phase 2: G = A^T R, FISTA update with projection and momentum
     if (nr > 0) {
+      if (a.flags) wait_neighbours(2 * it + 1);
+      P2_STAMP();
       stage(a.R);
-      axis0(a.aa);
+      P2_STAMP();
+      axis0(a.aa, a.R);
+      P2_STAMP();
       __syncthreads();
+      P2_STAMP();
       const double bk = a.beta[it];
       bool bad = false;
 #pragma unroll
@@ -241,7 +343,9 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
       }
       if (bad) atomicMin(a.nonfinite, k);
     }
-    grid.sync();
+    P2_STAMP();
+    phase_end(2 * it + 2);
+    P2_STAMP();
   }
 #pragma unroll
   for (int j = 0; j < RB; ++j) {
