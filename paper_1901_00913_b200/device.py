@@ -155,7 +155,7 @@ def _stream_handle():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-_PIECE_BYTES = 1 << 20  # host <-> device transfers move in 1 MiB pieces
+_PIECE_BYTES = 4 << 20  # host <-> device transfers move in 4 MiB pieces (tools/copy_bench.py)
 _copy_pool = None
 
 
@@ -166,7 +166,7 @@ def _pool():
     if _copy_pool is None:
         from concurrent.futures import ThreadPoolExecutor
 
-        _copy_pool = ThreadPoolExecutor(max_workers=max(1, min(8, os.cpu_count() or 1)),
+        _copy_pool = ThreadPoolExecutor(max_workers=max(1, min(16, os.cpu_count() or 1)),
                                         thread_name_prefix="kb-copy")
     return _copy_pool
 
@@ -181,6 +181,10 @@ def upload_pieces(dst, src: np.ndarray, stage) -> None:
     hs, hn, dflat = stage.view(-1), stage.view(-1).numpy(), dst.view(-1)
     step = max(1, _PIECE_BYTES // stage.element_size())
     spans = [(a, min(flat.size, a + step)) for a in range(0, flat.size, step)]
+    if len(spans) == 1:  # small images: no worker hand-off
+        hn[:flat.size] = flat
+        dflat[:flat.size].copy_(hs[:flat.size], non_blocking=True)
+        return
 
     def put(a, b):
         hn[a:b] = flat[a:b]
@@ -191,14 +195,39 @@ def upload_pieces(dst, src: np.ndarray, stage) -> None:
         dflat[a:b].copy_(hs[a:b], non_blocking=True)
 
 
-def download_pieces(src, stage, out: np.ndarray) -> np.ndarray:
+def prefault(out: np.ndarray) -> list:
+    """Touch every page of a freshly allocated host array on the copy workers and return their
+    futures. The public solvers call it right after the (asynchronous) solve launch, so the
+    first-touch page faults of the result array (2 GB at cfg5) are taken while the GPU iterates
+    rather than inside download_pieces."""
+    flat = out.reshape(-1)
+    if flat.nbytes < (8 << 20):
+        return []
+    per_page = max(1, 4096 // flat.itemsize)
+    step = max(per_page, (flat.size // 64 + per_page - 1) // per_page * per_page)
+
+    def touch(a, b):
+        flat[a:b:per_page] = 0
+
+    return [_pool().submit(touch, a, min(flat.size, a + step)) for a in range(0, flat.size, step)]
+
+
+def download_pieces(src, stage, out: np.ndarray, after=()) -> np.ndarray:
     """out (host array) <- src (device tensor) through the pinned `stage`: every piece's DMA is
-    queued at once; the copy workers move (and convert) each piece into `out` once it landed."""
+    queued at once; the copy workers move (and convert) each piece into `out` once it landed.
+    `after`: futures (prefault) to finish before the host copies start."""
     torch = _torch()
+    for f in after:
+        f.result()
     sflat, hs, hn = src.view(-1), stage.view(-1), stage.view(-1).numpy()
     oflat = out.reshape(-1)
     step = max(1, _PIECE_BYTES // stage.element_size())
     stream = torch.cuda.current_stream()
+    if sflat.numel() <= step:  # small images: one DMA, converted by the caller
+        hs.copy_(sflat, non_blocking=True)
+        stream.synchronize()
+        oflat[:] = hn
+        return out
     marks = []
     for a in range(0, sflat.numel(), step):
         b = min(sflat.numel(), a + step)

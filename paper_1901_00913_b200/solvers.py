@@ -256,7 +256,7 @@ def sfista(op, B, cfg: SolveConfig, X0=None, truth=None, exact_apply=None, *,
     """Accelerated solve of the matrix model against a KronOperator, on the B200."""
     import torch
 
-    from .device import INT_MAX, device_operator, download_pieces, upload_pieces
+    from .device import INT_MAX, device_operator, download_pieces, prefault, upload_pieces
 
     opts = options or SolveOptions()
     fast = not cfg.record_history and not cfg.record_iterates and cfg.rel_tol == 0
@@ -303,7 +303,11 @@ def sfista(op, B, cfg: SolveConfig, X0=None, truth=None, exact_apply=None, *,
             start.record(stream)
             dev.sfista_run(Bd, Xd, Yd, beta, 0, K, L, lam, opts.project, flag, use_graph=use_graph)
             stop.record(stream)
-            x = Xd.to(torch.float64, copy=True) if on_device else download_pieces(Xd, hX, np.empty(B.shape))
+            if on_device:
+                x = Xd.to(torch.float64, copy=True)
+            else:  # the result array's pages are first touched while the GPU iterates
+                out = np.empty(B.shape)
+                x = download_pieces(Xd, hX, out, after=prefault(out))
             torch.cuda.current_stream().synchronize()
             bad = int(flag.item())
             if bad <= K:
@@ -454,7 +458,7 @@ def sfista_batch(ops, B, lipschitz, lam: float, iters: int, *, options: SolveOpt
     and momentum. B: (batch, m, n) numpy or CUDA tensor. Returns (x, solve_ms) with x like B."""
     import torch
 
-    from .device import INT_MAX, DeviceOperator, download_pieces, upload_pieces
+    from .device import INT_MAX, DeviceOperator, download_pieces, prefault, upload_pieces
 
     opts = options or SolveOptions()
     dev = ops if isinstance(ops, DeviceOperator) else DeviceOperator(list(ops), opts.dtype)
@@ -477,9 +481,13 @@ def sfista_batch(ops, B, lipschitz, lam: float, iters: int, *, options: SolveOpt
     dev.sfista_run(Bd, Xd, Yd, beta, 0, int(iters), lipschitz, lam, opts.project, flag,
                    use_graph=bool(opts.use_graph))
     stop.record(stream)
+    out, touched = None, ()
+    if not on_device:  # the result array's pages are first touched while the GPU iterates
+        out = np.empty(tuple(Xd.shape))
+        touched = prefault(out)
     stop.synchronize()
     bad = int(flag.item())
     if bad <= iters:
         raise NumericError(f"non-finite iterate at iteration {bad}")
-    x = Xd if on_device else download_pieces(Xd, dev.staging("host_x", pinned=True), np.empty(tuple(Xd.shape)))
+    x = Xd if on_device else download_pieces(Xd, dev.staging("host_x", pinned=True), out, after=touched)
     return x, float(start.elapsed_time(stop))
