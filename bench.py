@@ -429,9 +429,13 @@ def measure_config(name, dtype, steps, warmup, rank, world, local, clocks=False,
         per_it_s = ms * 1e-3 / iters
         ach = sum(flops_phase) / per_it_s / 1e12
         pk, src = engine_peak("dmma")
+        # kb_capi.cu persist2_plan: zero BC, half widths <= 15, r <= 4, n % 64 == 0, n <= 512
+        second = (dev.bc == (0, 0) and max(dev.half_widths) <= 15 and cfg.r <= 4 and m % 64 == 0 and m <= 512
+                  and os.environ.get("KB_PERSIST2", "1") != "0")
         res["roofline"].update({
             "bound": "tensor", "unit": "TFLOP/s",
-            "kernel": "kb_solve_persistent (whole solve in one cooperative launch, 2 grid barriers per iteration)",
+            "kernel": ("kb_solve_persistent2" if second else "kb_solve_persistent")
+                      + " (whole solve in one cooperative launch, 2 grid barriers per iteration)",
             "achieved": round(ach, 3), "peak": round(pk, 3), "frac": round(ach / pk, 4),
             "flops_per_launch": sum(flops_phase) * iters,
             "peak_source": "measured live by kb_fma_peak in this run: " + src + " (FP64 FMA has the same nominal rate)"})
