@@ -1847,6 +1847,9 @@ Ps2Kernel ps2_kernel(int r, int RB) {
     default: return ps2_kernel_r<4>(RB);
   }
 }
+#ifndef KB_P2_SYNC_DEFAULT
+#define KB_P2_SYNC_DEFAULT 0  // KB_PERSIST2_SYNC unset: 0 grid.sync, 1 neighbour flags, 2 arrival counter
+#endif
 // The second whole-solve form (kb_persist2.cuh): zero BC on both axes, half widths <= 15,
 // r <= 4, n a multiple of 64 up to 512. KB_PERSIST2=0 keeps the first form; KB_PERSIST_RB picks
 // the rows per CTA (1 or 2).
@@ -1952,16 +1955,19 @@ int launch_persist(const kb_op* op, const PsPlan& pp, const double* B, double* X
     a.m = op->m;
     a.n = op->n;
     a.project = project;
-    // neighbour phase epochs instead of grid-wide barriers (KB_PERSIST2_SYNC=grid|flags): the
+    // KB_PERSIST2_SYNC=grid|flags|counter: cooperative-groups barrier, neighbour phase epochs, or one
+    // release/acquire arrival counter: the
     // flags, one 128-byte line per CTA, sit behind the beta table in the partials region
-    static const bool p2_flags = [] {
+    static const int p2_sync = [] {
       const char* v = std::getenv("KB_PERSIST2_SYNC");
-      return v ? std::string(v) == "flags" : false;
+      const std::string m = v ? v : "";
+      return m == "flags" ? 1 : m == "counter" ? 2 : m == "grid" ? 0 : KB_P2_SYNC_DEFAULT;
     }();
     const int fdoubles = (pp.nblk * kb::kP2FlagStride + 1) / 2 + 16;
     const int cap2 = (int)partials_doubles(op) - fdoubles - 2;
-    const bool use_flags = p2_flags && cap2 >= 1;
+    const bool use_flags = p2_sync != 0 && cap2 >= 1;
     const int capv = use_flags ? cap2 : cap;
+    a.sync_mode = use_flags ? p2_sync : 0;
     if (use_flags)  // 128-byte aligned
       a.flags = reinterpret_cast<int*>((reinterpret_cast<uintptr_t>(w.partials + capv + 1) + 127) & ~(uintptr_t)127);
     // centred 31-tap windows: window tap k' <-> table tap k' - 15 + H

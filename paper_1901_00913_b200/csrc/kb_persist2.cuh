@@ -29,6 +29,8 @@
 #pragma once
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 namespace kb {
 
 constexpr int kP2H = 15;             // window half width (taps centred, zero-padded)
@@ -46,6 +48,7 @@ struct P2Args {
   int* nonfinite;
   long long* trace;  // KB_P2_TRACE builds: clock64 stamps of the middle CTA's middle iteration
   int* flags;  // [gridDim.x] phase epochs, zeroed before the launch; nullptr = grid-wide barriers
+  int sync_mode;  // 0: cooperative-groups grid.sync, 1: neighbour flags, 2: one arrival counter (flags[0])
   double L, denom;
   int m, n, k0, iters, project;
   // centred taps: forward axis 0 Z[s] = sum_k fa[i][k] Y[s - 15 + k]; aa = the adjoint's
@@ -80,6 +83,9 @@ constexpr int kP2Piece = KB_P2_PIECE;  // staged rows per bulk copy / mbarrier (
 constexpr int kP2FlagStride = KB_P2_FSTRIDE;  // ints between two CTAs' phase flags (32: a 128-byte line each)
 #ifndef KB_P2_DIRECT
 #define KB_P2_DIRECT 0  // 1: axis 0 reads its source rows from L2 straight into registers (measured slower)
+#endif
+#ifndef KB_P2_BREG
+#define KB_P2_BREG 1
 #endif
 #ifndef KB_P2_CHAINS
 #define KB_P2_CHAINS 2
@@ -127,24 +133,23 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
   // contiguous) and one mbarrier each, so axis 0 starts on the first rows while the rest arrive;
   // pieces wholly outside the image only arrive
   auto stage = [&](const double* src) {
-    if (!KB_P2_DIRECT && tid == 0) {
-      // rows written by other CTAs before the grid barrier (generic proxy) -> bulk copy (async)
+    // lane p of warp 0 issues piece p (the pieces' issue latencies overlap)
+    if (!KB_P2_DIRECT && warp == 0 && lane < NP) {
+      // rows written by other CTAs before the barrier (generic proxy) -> bulk copy (async proxy)
       asm volatile("fence.proxy.async.global;" ::: "memory");
-#pragma unroll
-      for (int p = 0; p < NP; ++p) {
-        const int lo = max(g_lo, r0 - kP2H + kP2Piece * p);
-        const int hi = min(g_hi, r0 - kP2H + min(kP2Piece * (p + 1), RB + 2 * kP2H));
-        if (hi > lo) {
-          const unsigned bytes = (unsigned)((hi - lo) * n * sizeof(double));
-          mbar_arrive_expect_tx(&bar[p], bytes);
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  smem_u32(Ys + (size_t)(lo - (r0 - kP2H)) * n)),
-              "l"(src + (size_t)lo * n), "r"(bytes), "r"(smem_u32(&bar[p]))
-              : "memory");
-        } else {
-          mbar_arrive(&bar[p]);
-        }
+      const int p = lane;
+      const int lo = max(g_lo, r0 - kP2H + kP2Piece * p);
+      const int hi = min(g_hi, r0 - kP2H + min(kP2Piece * (p + 1), RB + 2 * kP2H));
+      if (hi > lo) {
+        const unsigned bytes = (unsigned)((hi - lo) * n * sizeof(double));
+        mbar_arrive_expect_tx(&bar[p], bytes);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(Ys + (size_t)(lo - (r0 - kP2H)) * n)),
+            "l"(src + (size_t)lo * n), "r"(bytes), "r"(smem_u32(&bar[p]))
+            : "memory");
+      } else {
+        mbar_arrive(&bar[p]);
       }
     }
   };
@@ -196,8 +201,20 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
   // lane's outputs in its block: column 64 mbc + 8 (lane >> 2) + 2 (lane & 3) + {0, 1}
   // KB_P2_CHAINS independent accumulator chains per term (K-steps dealt round robin), the terms
   // interleaved: a warp has one or two blocks per phase, so one chain of 10 r dependent DMMAs
-  // would run at the instruction's latency
-  auto axis1 = [&](int mb, int adj, double (&d)[2]) {
+  // would run at the instruction's latency. KB_P2_BREG: the lane's B fragments (both directions,
+  // 20 r doubles) stay in registers for the whole solve instead of being re-read from shared
+  // memory for every block (half of axis 1's shared-memory traffic).
+#if KB_P2_BREG
+  double bfr[2][R][kP2KS];
+#pragma unroll
+  for (int adj = 0; adj < 2; ++adj)
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int s = 0; s < kP2KS; ++s) bfr[adj][i][s] = Bf[((size_t)(adj * R + i) * kP2KS + s) * 32 + lane];
+#endif
+  auto axis1 = [&](int mb, auto adj_c, double (&d)[2]) {
+    constexpr int adj = decltype(adj_c)::value;
     const int t = mb / nmb, mbc = mb - t * nmb;
     const int j0 = 64 * mbc + 8 * (lane >> 2) + (lane & 3);
     double acc[R][KB_P2_CHAINS][2];
@@ -208,9 +225,14 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
 #pragma unroll
     for (int s = 0; s < kP2KS; ++s)
 #pragma unroll
-      for (int i = 0; i < R; ++i)
-        p2_dmma(acc[i][s % KB_P2_CHAINS], Zs[((size_t)i * RB + t) * NZ + p2_zidx(j0 + 4 * s)],
-                Bf[((size_t)(adj * R + i) * kP2KS + s) * 32 + lane]);
+      for (int i = 0; i < R; ++i) {
+#if KB_P2_BREG
+        const double b = bfr[adj][i][s];
+#else
+        const double b = Bf[((size_t)(adj * R + i) * kP2KS + s) * 32 + lane];
+#endif
+        p2_dmma(acc[i][s % KB_P2_CHAINS], Zs[((size_t)i * RB + t) * NZ + p2_zidx(j0 + 4 * s)], b);
+      }
     d[0] = d[1] = 0.0;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
@@ -233,7 +255,7 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
   // neighbours finish the phase that read the previous R (resp. Y).
   const int b_lo = max(0, (r0 - kP2H) / RB), b_hi = min((int)gridDim.x - 1, (r0 + RB - 1 + kP2H) / RB);
   auto wait_neighbours = [&](int epoch) {  // b_hi - b_lo < 32: one lane of warp 0 per neighbour
-    if (epoch > 0) {
+    if (epoch > 0 && a.sync_mode == 1) {
       if (warp == 0) {
         if (b_lo + lane <= b_hi) {
           int v;
@@ -252,10 +274,23 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
     }
   };
   auto phase_end = [&](int epoch) {
-    if (a.flags) {
+    if (a.sync_mode == 1) {
       __syncthreads();  // the CTA's stores happen before thread 0's release (cumulative)
       if (tid == 0)
         asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.flags + (size_t)blockIdx.x * kP2FlagStride), "r"(epoch) : "memory");
+    } else if (a.sync_mode == 2) {
+      // grid barrier on one monotonic counter: release-add, relaxed polls, one acquire fence
+      __syncthreads();
+      if (tid == 0) {
+        const int target = epoch * (int)gridDim.x;
+        int v;
+        asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.flags) : "memory");
+        do {
+          asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a.flags) : "memory");
+        } while (v < target);
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      }
+      __syncthreads();
     } else {
       grid.sync();
     }
@@ -289,7 +324,7 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
     // ---- phase 1: R = A Y - B on this CTA's rows
     if (nr > 0) {
       P2_STAMP();
-      if (a.flags) wait_neighbours(2 * it);
+      if (a.sync_mode == 1) wait_neighbours(2 * it);
       P2_STAMP();
       stage(a.Y);
       P2_STAMP();
@@ -302,7 +337,7 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
         const int mb = warp + 8 * j;
         if (mb < nblk) {
           double d[2];
-          axis1(mb, 0, d);
+          axis1(mb, std::integral_constant<int, 0>{}, d);
           const size_t e = (size_t)(r0 + mb / nmb) * n + out_col(mb);
           *reinterpret_cast<double2*>(a.R + e) = make_double2(__dsub_rn(d[0], bs[j][0]), __dsub_rn(d[1], bs[j][1]));
         }
@@ -313,7 +348,7 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
     P2_STAMP();
     // ---- phase 2: G = A^T R, FISTA update with projection and momentum
     if (nr > 0) {
-      if (a.flags) wait_neighbours(2 * it + 1);
+      if (a.sync_mode == 1) wait_neighbours(2 * it + 1);
       P2_STAMP();
       stage(a.R);
       P2_STAMP();
@@ -328,7 +363,7 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
         const int mb = warp + 8 * j;
         if (mb < nblk) {
           double g[2];
-          axis1(mb, 1, g);
+          axis1(mb, std::integral_constant<int, 1>{}, g);
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             double x = __ddiv_rn(__dsub_rn(__dmul_rn(a.L, ys[j][q]), g[q]), a.denom);
