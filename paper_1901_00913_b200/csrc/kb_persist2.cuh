@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
       __syncthreads();
       P2_STAMP();
       const double bk = a.beta[it];
+      const double rdenom = 1.0 / a.denom;
       bool bad = false;
 #pragma unroll
       for (int j = 0; j < RB; ++j) {
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
           axis1(mb, std::integral_constant<int, 1>{}, g);
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
-            double x = __ddiv_rn(__dsub_rn(__dmul_rn(a.L, ys[j][q]), g[q]), a.denom);
+            double x = kb_quot(__dsub_rn(__dmul_rn(a.L, ys[j][q]), g[q]), a.denom, rdenom);  // correctly rounded (kb_dmma.cuh)
             if (a.project && !(x > 0.0) && !isnan(x)) x = 0.0;  // np.maximum(x, 0): NaN kept (F3)
             bad |= !isfinite(x);
             ys[j][q] = __dadd_rn(x, __dmul_rn(bk, __dsub_rn(x, xs[j][q])));
