@@ -1958,7 +1958,7 @@ int launch_persist(const kb_op* op, const PsPlan& pp, const double* B, double* X
     // KB_PERSIST2_SYNC=grid|flags|counter: cooperative-groups barrier, neighbour phase epochs, or one
     // release/acquire arrival counter: the
     // flags, one 128-byte line per CTA, sit behind the beta table in the partials region
-    static const int p2_sync = [] {
+    const int p2_sync = [] {  // read per launch (the tests switch it)
       const char* v = std::getenv("KB_PERSIST2_SYNC");
       const std::string m = v ? v : "";
       return m == "flags" ? 1 : m == "counter" ? 2 : m == "grid" ? 0 : KB_P2_SYNC_DEFAULT;

@@ -94,6 +94,28 @@ def test_persist2_matches_oracle(m, n, r, ha, hb, iters, rb):
         assert rel(got, first) <= 1e-11
 
 
+@pytest.mark.parametrize("sync", ["flags", "counter"])
+@pytest.mark.parametrize("m,n,r,ha,hb,iters", [CASES[0], CASES[3], CASES[4]])
+def test_persist2_other_synchronisations_match_grid_barrier(m, n, r, ha, hb, iters, sync):
+    """KB_PERSIST2_SYNC=flags (neighbour phase epochs, one 128-byte line per CTA) and =counter (one
+    release/acquire arrival counter) order the same memory operations as the cooperative grid
+    barrier: the solves must agree bit for bit (same arithmetic, only the waiting differs), over
+    enough iterations for a missed wait to show, twice (the flags are re-zeroed per launch)."""
+    rng = np.random.default_rng(11 * m + n)
+    op = operator(rng, m, n, r, ha, hb)
+    B = rng.random((m, n))
+    L = 1.05 * float(np.sum([np.abs(t.H.c).sum() * np.abs(t.K.c).sum() for t in op.terms])) ** 2 / r
+    cfg = kb.SolveConfig(lam=0.05, lipschitz=L, max_iter=3 * iters, record_history=False)
+    opts = kb.SolveOptions(dtype="float64", project=True, use_graph=False)
+    with env(KB_PERSIST2_SYNC="grid"):
+        want = kb.sfista(op, B, cfg, options=opts).x
+    for _ in range(2):
+        with env(KB_PERSIST2_SYNC=sync):
+            got = kb.sfista(op, B, cfg, options=opts).x
+        np.testing.assert_array_equal(got, want)
+    assert device_operator(op, "float64").last_engines() == ["persist_f64"] * 4
+
+
 @pytest.mark.parametrize("rb", [1, 2])
 def test_persist2_bit_exact_on_integers(rb):
     """Integer generators and data with L + lam^2 = 1: the first two iterations are exact (see
