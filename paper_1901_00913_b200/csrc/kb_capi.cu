@@ -1985,8 +1985,8 @@ int launch_persist(const kb_op* op, const PsPlan& pp, const double* B, double* X
     const Ps2Kernel kern = ps2_kernel(op->r, pp.RB);
 #ifdef KB_P2_TRACE
     static long long* trace_d = nullptr;
-    if (!trace_d) cudaMalloc(&trace_d, 64 * sizeof(long long));
-    cudaMemsetAsync(trace_d, 0, 64 * sizeof(long long), s);
+    if (!trace_d) cudaMalloc(&trace_d, 16 * 1024 * sizeof(long long));
+    cudaMemsetAsync(trace_d, 0, 16 * 1024 * sizeof(long long), s);
     a.trace = trace_d;
 #endif
     for (int done = 0; done < iters;) {
@@ -2001,15 +2001,31 @@ int launch_persist(const kb_op* op, const PsPlan& pp, const double* B, double* X
     }
 #ifdef KB_P2_TRACE
     if (std::getenv("KB_P2_TRACE")) {
-      long long h[64];
+      std::vector<long long> h(16 * 1024);
       cudaStreamSynchronize(s);
-      cudaMemcpy(h, trace_d, sizeof(h), cudaMemcpyDeviceToHost);
+      cudaMemcpy(h.data(), trace_d, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
       static const char* names[] = {"p1 start", "p1 waited", "p1 staged(issued)", "p1 axis0", "p1 sync", "p1 axis1+store",
                                     "p1 phase_end", "p2 waited", "p2 staged(issued)", "p2 axis0", "p2 sync",
                                     "p2 axis1+update", "p2 phase_end"};
-      std::fprintf(stderr, "[p2 trace]");
-      for (int i = 1; i < 13; ++i) std::fprintf(stderr, " %s +%lld;", names[i], h[i] - h[i - 1]);
-      std::fprintf(stderr, " total %lld\n", h[12] - h[0]);
+      // per segment: min / mean / max over the CTAs (cycles of each CTA's own SM clock)
+      const int nb = std::min(pp.nblk, 1024);
+      std::fprintf(stderr, "[p2 trace] %d CTAs, min/mean/max cycles per segment:", nb);
+      for (int i = 1; i < 13; ++i) {
+        long long lo = LLONG_MAX, hi = 0, sum = 0;
+        for (int b = 0; b < nb; ++b) {
+          const long long d = h[16 * b + i] - h[16 * b + i - 1];
+          lo = std::min(lo, d);
+          hi = std::max(hi, d);
+          sum += d;
+        }
+        std::fprintf(stderr, " %s %lld/%lld/%lld;", names[i], lo, sum / nb, hi);
+      }
+      long long tl = LLONG_MAX, th = 0;
+      for (int b = 0; b < nb; ++b) {
+        tl = std::min(tl, h[16 * b + 12] - h[16 * b]);
+        th = std::max(th, h[16 * b + 12] - h[16 * b]);
+      }
+      std::fprintf(stderr, " total %lld..%lld\n", tl, th);
     }
 #endif
     for (int i = 0; i < 4; ++i) w.ctx.phase[i] = KB_ENGINE_PERSIST_F64;

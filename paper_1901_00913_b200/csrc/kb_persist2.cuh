@@ -46,7 +46,7 @@ struct P2Args {
   double* R;
   const double* beta;  // [iters] momentum coefficients beta_{k0+1 ..}
   int* nonfinite;
-  long long* trace;  // KB_P2_TRACE builds: clock64 stamps of the middle CTA's middle iteration
+  long long* trace;  // KB_P2_TRACE builds: clock64 stamps [CTA][16] of the middle iteration
   int* flags;  // [gridDim.x] phase epochs, zeroed before the launch; nullptr = grid-wide barriers
   int sync_mode;  // 0: cooperative-groups grid.sync, 1: neighbour flags, 2: one arrival counter (flags[0])
   double L, denom;
@@ -313,9 +313,9 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
   }
 
 #ifdef KB_P2_TRACE
-  const bool tracing = a.trace && blockIdx.x == gridDim.x / 2 && tid == 0;
+  const bool tracing = a.trace && tid == 0;  // every CTA: [blockIdx.x][16] stamps of the middle iteration
   int tn = 0;
-#define P2_STAMP() do { if (tracing && it == a.iters / 2) a.trace[tn++] = clock64(); } while (0)
+#define P2_STAMP() do { if (tracing && it == a.iters / 2) a.trace[16 * blockIdx.x + tn++] = clock64(); } while (0)
 #else
 #define P2_STAMP() do { } while (0)
 #endif
