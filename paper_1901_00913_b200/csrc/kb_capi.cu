@@ -1832,19 +1832,21 @@ struct PsPlan {
   int RB = 0, nblk = 0;
   size_t smem = 0;
   int v2 = 0;  // kb_solve_persistent2 (zero BC, narrow bands) instead of kb_solve_persistent
+  bool breg = false;  // v2: the register-resident-B-fragment instantiation (one CTA per SM)
 };
 
 using Ps2Kernel = void (*)(kb::P2Args);
 template <int R>
-Ps2Kernel ps2_kernel_r(int RB) {
-  return RB == 1 ? kb::kb_solve_persistent2<R, 1> : kb::kb_solve_persistent2<R, 2>;
+Ps2Kernel ps2_kernel_r(int RB, bool breg) {
+  if (breg) return RB == 1 ? kb::kb_solve_persistent2<R, 1, true> : kb::kb_solve_persistent2<R, 2, true>;
+  return RB == 1 ? kb::kb_solve_persistent2<R, 1, false> : kb::kb_solve_persistent2<R, 2, false>;
 }
-Ps2Kernel ps2_kernel(int r, int RB) {
+Ps2Kernel ps2_kernel(int r, int RB, bool breg) {
   switch (r) {
-    case 1: return ps2_kernel_r<1>(RB);
-    case 2: return ps2_kernel_r<2>(RB);
-    case 3: return ps2_kernel_r<3>(RB);
-    default: return ps2_kernel_r<4>(RB);
+    case 1: return ps2_kernel_r<1>(RB, breg);
+    case 2: return ps2_kernel_r<2>(RB, breg);
+    case 3: return ps2_kernel_r<3>(RB, breg);
+    default: return ps2_kernel_r<4>(RB, breg);
   }
 }
 #ifndef KB_P2_SYNC_DEFAULT
@@ -1863,18 +1865,23 @@ PsPlan persist2_plan(const kb_op* op) {
   const char* rbv = std::getenv("KB_PERSIST_RB");
   const int want = rbv ? std::atoi(rbv) : 0;
   const int sms = sm_count();
+  // two rows per CTA before one; the register-resident-B instantiation (one CTA per SM) when the
+  // CTAs fit that way, else the lean one (two per SM)
   for (int RB = want == 1 || want == 2 ? want : 2; RB >= 1; --RB) {
-    const Ps2Kernel k = ps2_kernel(op->r, RB);
-    const size_t smem = kb::p2_smem_bytes(RB, op->n, op->r);
-    int per_sm = 0;
-    if (smem <= 200 * 1024 && allow_smem(k, smem) == KB_OK &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kb::kP2Threads, smem) == cudaSuccess &&
-        per_sm >= 1 && (op->m + RB - 1) / RB <= per_sm * sms) {
-      p.RB = RB;
-      p.nblk = (op->m + RB - 1) / RB;
-      p.smem = smem;
-      p.v2 = 1;
-      return p;
+    for (int breg = 1; breg >= 0; --breg) {
+      const Ps2Kernel k = ps2_kernel(op->r, RB, breg != 0);
+      const size_t smem = kb::p2_smem_bytes(RB, op->n, op->r);
+      int per_sm = 0;
+      if (smem <= 200 * 1024 && allow_smem(k, smem) == KB_OK &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kb::kP2Threads, smem) == cudaSuccess &&
+          per_sm >= 1 && (op->m + RB - 1) / RB <= per_sm * sms) {
+        p.RB = RB;
+        p.nblk = (op->m + RB - 1) / RB;
+        p.smem = smem;
+        p.v2 = 1;
+        p.breg = breg != 0;
+        return p;
+      }
     }
     if (want == 1 || want == 2) break;
   }
@@ -1982,7 +1989,7 @@ int launch_persist(const kb_op* op, const PsPlan& pp, const double* B, double* X
     centre(op->h_corr[0], op->Ha, op->Wpa, a.aa);
     centre(op->h_conv[1], op->Hb, op->Wpb, a.fb);
     centre(op->h_corr[1], op->Hb, op->Wpb, a.ab);
-    const Ps2Kernel kern = ps2_kernel(op->r, pp.RB);
+    const Ps2Kernel kern = ps2_kernel(op->r, pp.RB, pp.breg);
 #ifdef KB_P2_TRACE
     static long long* trace_d = nullptr;
     if (!trace_d) cudaMalloc(&trace_d, 16 * 1024 * sizeof(long long));

@@ -97,7 +97,9 @@ __device__ __forceinline__ void p2_dmma(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-template <int R, int RB>
+// BREG: the lane's axis-1 B fragments stay in registers for the whole solve (~200 registers: one
+// CTA per SM); without it the kernel fits two CTAs per SM (images of up to 2 x 148 x RB rows)
+template <int R, int RB, bool BREG = (KB_P2_BREG != 0)>
 __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_constant__ P2Args a) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -204,15 +206,15 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
   // would run at the instruction's latency. KB_P2_BREG: the lane's B fragments (both directions,
   // 20 r doubles) stay in registers for the whole solve instead of being re-read from shared
   // memory for every block (half of axis 1's shared-memory traffic).
-#if KB_P2_BREG
-  double bfr[2][R][kP2KS];
+  double bfr[BREG ? 2 : 1][BREG ? R : 1][BREG ? kP2KS : 1];
+  if constexpr (BREG) {
 #pragma unroll
-  for (int adj = 0; adj < 2; ++adj)
+    for (int adj = 0; adj < 2; ++adj)
 #pragma unroll
-    for (int i = 0; i < R; ++i)
+      for (int i = 0; i < R; ++i)
 #pragma unroll
-      for (int s = 0; s < kP2KS; ++s) bfr[adj][i][s] = Bf[((size_t)(adj * R + i) * kP2KS + s) * 32 + lane];
-#endif
+        for (int s = 0; s < kP2KS; ++s) bfr[adj][i][s] = Bf[((size_t)(adj * R + i) * kP2KS + s) * 32 + lane];
+  }
   auto axis1 = [&](int mb, auto adj_c, double (&d)[2]) {
     constexpr int adj = decltype(adj_c)::value;
     const int t = mb / nmb, mbc = mb - t * nmb;
@@ -226,11 +228,9 @@ __global__ void __launch_bounds__(kP2Threads) kb_solve_persistent2(const __grid_
     for (int s = 0; s < kP2KS; ++s)
 #pragma unroll
       for (int i = 0; i < R; ++i) {
-#if KB_P2_BREG
-        const double b = bfr[adj][i][s];
-#else
-        const double b = Bf[((size_t)(adj * R + i) * kP2KS + s) * 32 + lane];
-#endif
+        double b;
+        if constexpr (BREG) b = bfr[adj][i][s];
+        else b = Bf[((size_t)(adj * R + i) * kP2KS + s) * 32 + lane];
         p2_dmma(acc[i][s % KB_P2_CHAINS], Zs[((size_t)i * RB + t) * NZ + p2_zidx(j0 + 4 * s)], b);
       }
     d[0] = d[1] = 0.0;

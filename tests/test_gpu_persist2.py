@@ -94,6 +94,25 @@ def test_persist2_matches_oracle(m, n, r, ha, hb, iters, rb):
         assert rel(got, first) <= 1e-11
 
 
+def test_persist2_two_ctas_per_sm():
+    """512 x 256: 256 CTAs at two rows each, two per SM -- the instantiation without
+    register-resident B fragments (the ~200-register one fits one CTA per SM only)."""
+    m, n, r, iters = 512, 256, 3, 12
+    rng = np.random.default_rng(5)
+    op = operator(rng, m, n, r, 15, 15)
+    B = rng.random((m, n))
+    L = 1.05 * float(np.sum([np.abs(t.H.c).sum() * np.abs(t.K.c).sum() for t in op.terms])) ** 2 / r
+    _, beta = kb.momentum_table(iters)
+    want = C.sfista(C.OracleOp(op), B, L, 0.05, iters, beta, project=True)
+    cfg = kb.SolveConfig(lam=0.05, lipschitz=L, max_iter=iters, record_history=False)
+    got = kb.sfista(op, B, cfg, options=kb.SolveOptions(dtype="float64", project=True, use_graph=False)).x
+    assert device_operator(op, "float64").last_engines() == ["persist_f64"] * 4
+    assert rel(got, want) <= 1e-10
+    with env(KB_PERSIST2=0):
+        first = kb.sfista(op, B, cfg, options=kb.SolveOptions(dtype="float64", project=True, use_graph=False)).x
+    assert rel(got, first) <= 1e-11
+
+
 @pytest.mark.parametrize("sync", ["flags", "counter"])
 @pytest.mark.parametrize("m,n,r,ha,hb,iters", [CASES[0], CASES[3], CASES[4]])
 def test_persist2_other_synchronisations_match_grid_barrier(m, n, r, ha, hb, iters, sync):
